@@ -1,0 +1,475 @@
+#!/usr/bin/env python
+"""Benchmark: layout conversion + transfer of record collections on B200.
+
+Workload (BASELINE.json configs[4], the north-star shape): a collection of
+1,000,000,000 Obj8 records (8 x f32/i32 fields, 32-byte packed AoS) sharded by
+contiguous object-index range over the N GPUs of one box. One step converts
+every rank's AoS shard into per-field planes (SoA) in HBM through the public
+API (copy_collection -> b200-convert -> one launch of the conversion engine).
+No collective on the data path (objects are independent), so `scaling` is
+"strong": the 1B-object total is fixed as N grows.
+
+value      whole-job algorithmic GB/s (64 B per object: 32 read + 32 written),
+           inputs resident in HBM, device time (CUDA events), max over ranks
+e2e        the same metric through copy_collection with the AoS in pinned HOST
+           memory: chunked H2D | convert | result read-back inside the timed
+           region (bounded sample per rank, stated in e2e.sample)
+roofline   the conversion kernel vs the measured HBM copy peak
+cpu_baseline  the reference's per-leaf numpy path (oracle port), 1 core, on a
+           bounded sample (rank 0, N=1 only)
+
+--impl reference runs the reference's CPU path (oracle port) sharded over all
+host cores instead, on rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "layout-convert+transfer GB/s and objects/s vs HBM roofline, 1/2/4/8 B200"
+UNIT = "GB/s"
+WORKLOAD = "config5: Obj8 AoS->SoA (8 x f32/i32, 32 B records), 1e9 objects sharded by object index"
+BYTES_PER_OBJECT = 64
+
+
+def _peaks() -> dict:
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except OSError:
+        return {}
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int) -> None:
+        self.device = device
+        self.lines: list[str] = []
+        self.proc = None
+        self.thread = None
+
+    def start(self) -> None:
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "200",
+                 "-i", str(self.device)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self) -> None:
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sms, maxes, reasons = [], [], set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sms.append(float(parts[1]))
+                maxes.append(float(parts[2]))
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[5:9]):
+                if val.lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sms) if sms else None, "sm_max_mhz": max(maxes) if maxes else None,
+                "reasons": sorted(reasons), "samples": len(sms)}
+
+
+def _dist():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def _cpu_info() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+# ---- our arm -------------------------------------------------------------------------------------
+
+def run_ours(args) -> None:
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    rank, world, local = _dist()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+
+    import paper_2511_04853_b200 as sk
+    from paper_2511_04853_b200 import _native as nat
+    from paper_2511_04853_b200 import layouts as ly, memctx as mc, schema as sc, shard, transfer as tr
+    from paper_2511_04853_b200 import workloads as wl
+
+    dev = local
+    cuda = mc.ContextInfo.cuda(dev)
+
+    def barrier():
+        nat.sync(dev)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item())
+
+    def device_collection(schema, kind, n):
+        c = sk.Collection(schema, kind, cuda)
+        with mc.execution_scope(mc.CUDA):
+            c.reserve(n)
+        with c.layout.engine_ops():
+            c.layout._set_sizes_for_engine({sc.MAIN_TAG: n})
+        return c
+
+    n_total = args.objects
+    free_b, _ = torch.cuda.mem_get_info(dev)
+    lo, hi = shard.shard_range(n_total, rank, world)
+    n = hi - lo
+    if 2 * n * 32 > free_b * 0.9:
+        raise SystemExit(f"rank {rank}: shard of {n} objects needs {2 * n * 32 / 1e9:.1f} GB, {free_b / 1e9:.1f} GB free")
+
+    aos = device_collection(wl.OBJ8_SCHEMA, ly.AOS, n)
+    soa = device_collection(wl.OBJ8_SCHEMA, ly.PER_FIELD, n)
+    # the global 1e9-record image is splitmix64(seed, word); this shard is its slice
+    wl.fill_random_device(aos.layout._struct_buf.ptr, n * 32, seed=20251104, device=dev, first_word=lo * 4)
+
+    def step():
+        tr.copy_collection(soa, aos, {"async": True})
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    clocks = Clocks(dev) if rank == 0 else None
+    if clocks:
+        clocks.start()
+    evs = [nat.Event() for _ in range(args.steps + 1)]
+    barrier()
+    evs[0].record(dev)
+    for k in range(args.steps):
+        step()
+        evs[k + 1].record(dev)
+    barrier()
+    clk = clocks.stop() if clocks else None
+    per_launch = [evs[k].elapsed_ms(evs[k + 1]) for k in range(args.steps)]
+    local_ms = evs[0].elapsed_ms(evs[-1]) / args.steps
+    ms = max_over_ranks(local_ms)
+    value = n_total * BYTES_PER_OBJECT / (ms / 1e3) / 1e9
+    launch_ms = max_over_ranks(statistics.mean(per_launch))
+    achieved = n * BYTES_PER_OBJECT / (launch_ms / 1e3) / 1e9  # per GPU, slowest rank's launch time
+
+    # parity spot check of the timed output (first 4096 records of this shard)
+    probe = 4096 if n >= 4096 else n
+    raw = np.empty(probe * 32, np.uint8)
+    nat.memcpy(raw.ctypes.data, aos.layout._struct_buf.ptr, raw.nbytes, dev)
+    nat.sync(dev)
+    rec = raw.view(wl.OBJ8_AOS_DTYPE)
+    for i in range(8):
+        got = np.empty(probe, rec.dtype[i])
+        nat.memcpy(got.ctypes.data, soa.layout.plane_address(soa.plan.leaf(f"f{i}")), got.nbytes, dev)
+        nat.sync(dev)
+        if got.tobytes() != np.ascontiguousarray(rec[f"f{i}"]).tobytes():
+            raise SystemExit(f"rank {rank}: converted plane f{i} differs from the AoS input")
+
+    # ---- e2e: pinned HOST AoS -> device SoA through the public API, result read back ----
+    m = min(args.e2e_objects, n)
+    host = sk.Collection(wl.OBJ8_SCHEMA, ly.AOS, mc.ContextInfo.pinned())
+    host.resize(m)
+    nat.memcpy(host.layout._struct_buf.ptr, aos.layout._struct_buf.ptr, m * 32, dev)  # same records as the shard head
+    dst = device_collection(wl.OBJ8_SCHEMA, ly.PER_FIELD, m)
+    result = np.empty(8, np.uint32)
+    tails = [dst.layout.plane_address(dst.plan.leaf(f"f{i}")) + (m - 1) * 4 for i in range(8)]
+
+    def e2e_step():
+        tr.copy_collection(dst, host)  # H2D + convert, pipelined; returns when done
+        for i, p in enumerate(tails):  # device->host read of the step's result (last record)
+            nat.memcpy(result.ctypes.data + 4 * i, p, 4, dev)
+        nat.sync(dev)
+
+    for _ in range(max(1, args.warmup)):
+        e2e_step()
+    e0, e1 = nat.Event(), nat.Event()
+    e2e_steps = max(2, min(args.steps, 5))
+    barrier()
+    e0.record(dev)
+    for _ in range(e2e_steps):
+        e2e_step()
+    e1.record(dev)
+    barrier()
+    e2e_ms = max_over_ranks(e0.elapsed_ms(e1) / e2e_steps)
+    m_total = sum_over_ranks(m)
+    e2e_value = m_total * BYTES_PER_OBJECT / (e2e_ms / 1e3) / 1e9
+    host.free()
+    dst.free()
+
+    extra = {}
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_extra:
+        extra = run_extras(args, dev)
+    if rank == 0 and world == 1 and not args.no_cpu:
+        from oracle import cpu_baseline
+
+        cb = cpu_baseline.single_core(args.cpu_objects, budget_s=args.cpu_seconds)
+        cpu = {"value": round(cb["gbs"], 3), "unit": UNIT, "cores": 1, "kind": "port",
+               "objects_per_s": round(cb["objects_per_s"]),
+               "sample": f"{args.cpu_objects} Obj8 objects, reference per-leaf numpy path "
+                         f"(transfer.py:196-228) restated in oracle/cpu_baseline.py, mean of fastest of "
+                         f"{cb['reps']} reps; host: {os.cpu_count()} x {_cpu_info()}"}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    peaks = _peaks()
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    traffic = _traffic(n)
+    line = {
+        "metric": METRIC,
+        "value": round(value, 2),
+        "unit": UNIT,
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(ms, 4),
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "u8",
+        "data": "synthetic (splitmix64 record images generated on-device, seed 20251104)",
+        "config": {"workload": WORKLOAD, "objects_total": n_total, "objects_per_gpu": n, "record_bytes": 32,
+                   "algorithmic_bytes_per_object": BYTES_PER_OBJECT,
+                   "sharding": "contiguous object-index ranges, no data-path collective",
+                   "l2": "inputs (32 GB AoS at N=1) far larger than the 126 MB L2; no flush needed",
+                   "timing": "CUDA events on the library stream, barrier + sync both sides, max over ranks"},
+        "objects_per_s": round(n_total / (ms / 1e3)),
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "traffic": traffic,
+                     "kernel": "sk::conv::convert_kernel (word-mode AoS->planes, TMA bulk in/out)",
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (torch copy, read+write)" if peaks else
+                                    "fallback 6650 GB/s (B200_PROFILING.md)"},
+        "e2e": {"value": round(e2e_value, 2), "unit": UNIT, "h2d_bytes_per_step": m * 32 * world,
+                "d2h_bytes_per_step": 32 * world, "ms_per_step": round(e2e_ms, 3),
+                "sample": f"{m} objects per rank in pinned host memory -> device per_field via copy_collection "
+                          "(chunked H2D | convert | on 3 streams), then D2H of the last converted record"},
+        "gpu_launches": args.steps,
+        "clocks": clk,
+        "cpu_baseline": cpu,
+    }
+    if extra:
+        line["configs"] = extra
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def _traffic(n: int):
+    """dram bytes per launch from the committed ncu capture (profiles/), scaled to
+    this launch's object count; None when no capture is committed."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            t = json.load(f)
+        return round(t["dram_bytes_per_object"] * n)
+    except (OSError, KeyError, ValueError):
+        return None
+
+
+def run_extras(args, dev: int) -> dict:
+    """Configs 1-4 on one GPU (device-resident inputs, CUDA-event timing)."""
+    import numpy as np
+
+    import paper_2511_04853_b200 as sk
+    from paper_2511_04853_b200 import _native as nat
+    from paper_2511_04853_b200 import jagged, layouts as ly, memctx as mc, schema as sc, sensor, transfer as tr
+    from paper_2511_04853_b200 import workloads as wl
+    from paper_2511_04853_b200.devarray import DeviceArray
+
+    cuda = mc.ContextInfo.cuda(dev)
+    peak = float(_peaks().get("hbm_gbs", 6650.0))
+
+    def coll(schema, kind, n, info=cuda):
+        c = sk.Collection(schema, kind, info)
+        with mc.execution_scope(mc.CUDA if info.context == mc.CUDA else mc.HOST):
+            c.reserve(n)
+        with c.layout.engine_ops():
+            c.layout._set_sizes_for_engine({sc.MAIN_TAG: n})
+        return c
+
+    def timed(fn, steps=5, warmup=2):
+        for _ in range(warmup):
+            fn()
+        nat.sync(dev)
+        a, b = nat.Event(), nat.Event()
+        a.record(dev)
+        for _ in range(steps):
+            fn()
+        b.record(dev)
+        return a.elapsed_ms(b) / steps
+
+    out = {}
+    # config 1: 1M Obj8 AoS -> SoA (launch-bound size), device-resident and from pinned host
+    n = 1_000_000
+    a1, p1 = coll(wl.OBJ8_SCHEMA, ly.AOS, n), coll(wl.OBJ8_SCHEMA, ly.PER_FIELD, n)
+    wl.fill_random_device(a1.layout._struct_buf.ptr, n * 32, 1, dev)
+    ms = timed(lambda: tr.copy_collection(p1, a1, {"async": True}), steps=20)
+    h1 = coll(wl.OBJ8_SCHEMA, ly.AOS, n, mc.ContextInfo.pinned())
+    ms_h = timed(lambda: tr.copy_collection(p1, h1), steps=5)
+    out["config1_obj8_1M"] = {"device_ms": round(ms, 4), "device_gbs": round(n * 64 / ms / 1e6, 1),
+                              "frac": round(n * 64 / ms / 1e6 / peak, 3), "pinned_h2d_e2e_ms": round(ms_h, 3),
+                              "e2e_gbs": round(n * 64 / ms_h / 1e6, 1)}
+    for c in (a1, p1, h1):
+        c.free()
+
+    # config 2: case study, 64 events x 190,096 cells, fused AoS(30 B) -> planes + energy + noise
+    cells = 64 * 436 * 436
+    a2 = coll(sensor.SENSOR_SCHEMA, ly.AOS, cells)
+    p2 = coll(sensor.SENSOR_SCHEMA, ly.PER_FIELD, cells)
+    wl.fill_random_device(a2.layout._struct_buf.ptr, (cells * 30) // 8 * 8, 2, dev)
+    noise = DeviceArray(cells, np.float32, cuda)
+    ms = timed(lambda: sensor.transfer_calibrate(p2, a2, noise, sync=False))
+    h2 = coll(sensor.SENSOR_SCHEMA, ly.AOS, cells, mc.ContextInfo.pinned())
+    ms_h = timed(lambda: sensor.transfer_calibrate(p2, h2, noise, sync=True), steps=3, warmup=1)
+    out["config2_sensor_64x190096"] = {
+        "device_ms": round(ms, 3), "device_cells_per_s": round(cells / ms * 1e3),
+        "device_gbs": round(cells * 64 / ms / 1e6, 1), "frac": round(cells * 64 / ms / 1e6 / peak, 3),
+        "pinned_h2d_e2e_ms": round(ms_h, 3), "e2e_cells_per_s": round(cells / ms_h * 1e3),
+        "h2d_gbs": round(cells * 30 / ms_h / 1e6, 1),
+        "note": "random-bit sensor records (fused kernel cost is data independent)"}
+    for c in (a2, p2, h2):
+        c.free()
+    noise.free()
+
+    # config 3: 1M clusters, ~10M u64 members, shuffled source pool
+    nc = 1_000_000
+    lens, offsets, pool = wl.cluster_inputs(nc, seed=7)
+    d_lens, d_off, d_pool = DeviceArray.from_numpy(lens, cuda), DeviceArray.from_numpy(offsets, cuda), \
+        DeviceArray.from_numpy(pool, cuda)
+    c3 = sk.Collection(wl.CLUSTER_SCHEMA, ly.PER_FIELD, cuda)
+    with mc.execution_scope(mc.CUDA):
+        c3.resize(nc)
+    members = int(lens.sum())
+    ms = timed(lambda: jagged.pack(c3, "members", d_lens, d_off, d_pool), steps=5)
+    algo = nc * 16 + members * 16
+    out["config3_jagged_1M"] = {"members": members, "ms": round(ms, 3), "members_per_s": round(members / ms * 1e3),
+                                "gbs": round(algo / ms / 1e6, 1), "frac": round(algo / ms / 1e6 / peak, 3),
+                                "note": "includes the D2H read of the total between scan and gather"}
+    c3.free()
+    for d in (d_lens, d_off, d_pool):
+        d.free()
+
+    # config 4: 100M Track records (60 B) -> AoSoA T=128 of [pz, px, x, charge] with f64->f32
+    n4 = 100_000_000
+    a4 = coll(wl.TRACK_SCHEMA, ly.AOS, n4)
+    wl.fill_random_device(a4.layout._struct_buf.ptr, n4 * 60, 4, dev)
+    fields = [sk.AosoaField("pz", "f32"), sk.AosoaField("px", "f32"), sk.AosoaField("x", "f32"),
+              sk.AosoaField("charge", "i32")]
+    ao = sk.Aosoa(n4, 128, fields, cuda)
+    ms = timed(lambda: sk.to_aosoa(a4, fields, 128, out=ao, sync=False))
+    out["config4_aosoa_100M"] = {"ms": round(ms, 3), "gbs": round(n4 * 76 / ms / 1e6, 1),
+                                 "frac": round(n4 * 76 / ms / 1e6 / peak, 3), "objects_per_s": round(n4 / ms * 1e3)}
+    ao.free()
+    a4.free()
+    return out
+
+
+# ---- the reference arm -----------------------------------------------------------------------------
+
+def run_reference(args) -> None:
+    rank, world, _ = _dist()
+    if rank != 0:
+        return
+    from oracle import cpu_baseline
+
+    procs = os.cpu_count() or 1
+    n = args.ref_objects
+    r = cpu_baseline.multi_core(n, args.steps, max(1, args.warmup), procs)
+    times = r["step_seconds"]
+    t = statistics.mean(times)
+    value = n * BYTES_PER_OBJECT / t / 1e9
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(t * 1e3, 3), "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "u8", "data": "synthetic (random Obj8 records)", "impl": "reference",
+        "config": {"workload": WORKLOAD, "objects_per_step": n, "record_bytes": 32,
+                   "algorithmic_bytes_per_object": BYTES_PER_OBJECT},
+        "cpu_baseline": {"value": round(value, 3), "unit": UNIT, "cores": procs, "kind": "port",
+                         "sample": f"{n} Obj8 objects per step, reference per-leaf numpy path "
+                                   f"(oracle/cpu_baseline.py) sharded over {procs} processes; "
+                                   f"host: {_cpu_info()}"},
+        "e2e": {"value": round(value, 3), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--objects", type=int, default=1_000_000_000)
+    ap.add_argument("--e2e-objects", type=int, default=64_000_000)
+    ap.add_argument("--cpu-objects", type=int, default=16_000_000)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--ref-objects", type=int, default=64_000_000)
+    ap.add_argument("--no-extra", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

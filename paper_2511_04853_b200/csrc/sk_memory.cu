@@ -1,0 +1,396 @@
+// Memory-context plumbing of libsoakit_b200: allocation, copies, memset,
+// memmove, streams/events, peer access, IPC. Replaces the mock device and the
+// default copier of the reference (memctx.py:115-143, 304-360).
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "sk_internal.cuh"
+
+namespace sk {
+
+static thread_local std::string g_last_error;
+
+int set_error(int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return code;
+}
+
+void clear_error() { g_last_error.clear(); }
+
+int cuda_fail(cudaError_t e, const char* what) {
+  int code = SK_ERR_CUDA;
+  if (e == cudaErrorMemoryAllocation) code = SK_ERR_ALLOC;
+  if (e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver) code = SK_ERR_NO_DEVICE;
+  cudaGetLastError();  // clear sticky-free error state
+  return set_error(code, "%s failed: %s (%s)", what, cudaGetErrorName(e), cudaGetErrorString(e));
+}
+
+static std::mutex g_dev_mu;
+static DeviceState g_dev[64];
+
+int device_state(int device, DeviceState** out) {
+  if (device < 0 || device >= 64) return set_error(SK_ERR_INVALID, "device id %d out of range", device);
+  std::lock_guard<std::mutex> lk(g_dev_mu);
+  DeviceState& d = g_dev[device];
+  if (!d.init) {
+    int count = 0;
+    SK_TRY(cudaGetDeviceCount(&count));
+    if (device >= count) return set_error(SK_ERR_NO_DEVICE, "device %d not present (%d devices)", device, count);
+    SK_TRY(cudaSetDevice(device));
+    SK_TRY(cudaDeviceGetAttribute(&d.sm_count, cudaDevAttrMultiProcessorCount, device));
+    SK_TRY(cudaDeviceGetAttribute(&d.max_smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+    SK_TRY(cudaStreamCreateWithFlags(&d.stream, cudaStreamNonBlocking));
+    SK_TRY(cudaStreamCreateWithFlags(&d.copy_in, cudaStreamNonBlocking));
+    SK_TRY(cudaStreamCreateWithFlags(&d.copy_out, cudaStreamNonBlocking));
+    // keep freed pool memory cached: layout growth reallocates often
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      uint64_t threshold = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold);
+    }
+    d.init = true;
+  } else {
+    SK_TRY(cudaSetDevice(device));
+  }
+  *out = &d;
+  return SK_OK;
+}
+
+cudaStream_t resolve_stream(int device, uintptr_t s) {
+  if (s) return reinterpret_cast<cudaStream_t>(s);
+  DeviceState* d = nullptr;
+  if (device_state(device, &d) != SK_OK) return nullptr;
+  return d->stream;
+}
+
+static int stream_device(cudaStream_t s, int* device) {
+  // the library's streams know their device; foreign streams use the current one
+  for (int i = 0; i < 64; ++i) {
+    if (g_dev[i].init && (g_dev[i].stream == s || g_dev[i].copy_in == s || g_dev[i].copy_out == s)) {
+      *device = i;
+      return SK_OK;
+    }
+  }
+  SK_TRY(cudaGetDevice(device));
+  return SK_OK;
+}
+
+static int stream_of(uintptr_t s, cudaStream_t* out) {
+  if (s) {
+    *out = reinterpret_cast<cudaStream_t>(s);
+    int dev = 0;
+    int rc = stream_device(*out, &dev);
+    if (rc) return rc;
+    SK_TRY(cudaSetDevice(dev));
+    return SK_OK;
+  }
+  int dev = 0;
+  SK_TRY(cudaGetDevice(&dev));
+  DeviceState* d = nullptr;
+  int rc = device_state(dev, &d);
+  if (rc) return rc;
+  *out = d->stream;
+  return SK_OK;
+}
+
+}  // namespace sk
+
+using namespace sk;
+
+extern "C" {
+
+const char* sk_last_error(void) { return g_last_error.c_str(); }
+
+int sk_version(void) { return 0x000100; }
+
+int sk_device_count(int* count) {
+  if (!count) return set_error(SK_ERR_INVALID, "null count");
+  cudaError_t e = cudaGetDeviceCount(count);
+  if (e != cudaSuccess) {
+    *count = 0;
+    return cuda_fail(e, "cudaGetDeviceCount");
+  }
+  return SK_OK;
+}
+
+int sk_device_info(int device, int* sm_count, int* cc_major, int* cc_minor, size_t* total_mem) {
+  DeviceState* d = nullptr;
+  int rc = device_state(device, &d);
+  if (rc) return rc;
+  cudaDeviceProp prop;
+  SK_TRY(cudaGetDeviceProperties(&prop, device));
+  if (sm_count) *sm_count = prop.multiProcessorCount;
+  if (cc_major) *cc_major = prop.major;
+  if (cc_minor) *cc_minor = prop.minor;
+  if (total_mem) *total_mem = prop.totalGlobalMem;
+  return SK_OK;
+}
+
+int sk_malloc(int device, size_t nbytes, void** out) {
+  if (!out) return set_error(SK_ERR_INVALID, "null out pointer");
+  *out = nullptr;
+  if (nbytes == 0) return SK_OK;
+  DeviceState* d = nullptr;
+  int rc = device_state(device, &d);
+  if (rc) return rc;
+  // round up so vectorised tails never leave the allocation
+  size_t padded = (nbytes + 255) & ~size_t(255);
+  cudaError_t e = cudaMallocAsync(out, padded, d->stream);
+  if (e != cudaSuccess) {
+    *out = nullptr;
+    return cuda_fail(e, "cudaMallocAsync");
+  }
+  return SK_OK;
+}
+
+int sk_free(int device, void* ptr) {
+  if (!ptr) return SK_OK;
+  DeviceState* d = nullptr;
+  int rc = device_state(device, &d);
+  if (rc) return rc;
+  SK_TRY(cudaFreeAsync(ptr, d->stream));
+  return SK_OK;
+}
+
+int sk_host_alloc_pinned(size_t nbytes, void** out) {
+  if (!out) return set_error(SK_ERR_INVALID, "null out pointer");
+  *out = nullptr;
+  if (nbytes == 0) return SK_OK;
+  cudaError_t e = cudaHostAlloc(out, nbytes, cudaHostAllocPortable);
+  if (e != cudaSuccess) {
+    *out = nullptr;
+    return cuda_fail(e, "cudaHostAlloc");
+  }
+  return SK_OK;
+}
+
+int sk_host_free_pinned(void* ptr) {
+  if (!ptr) return SK_OK;
+  SK_TRY(cudaFreeHost(ptr));
+  return SK_OK;
+}
+
+int sk_host_register(void* ptr, size_t nbytes) {
+  if (!ptr || !nbytes) return SK_OK;
+  SK_TRY(cudaHostRegister(ptr, nbytes, cudaHostRegisterPortable));
+  return SK_OK;
+}
+
+int sk_host_unregister(void* ptr) {
+  if (!ptr) return SK_OK;
+  SK_TRY(cudaHostUnregister(ptr));
+  return SK_OK;
+}
+
+int sk_stream_default(int device, uintptr_t* stream) {
+  DeviceState* d = nullptr;
+  int rc = device_state(device, &d);
+  if (rc) return rc;
+  *stream = reinterpret_cast<uintptr_t>(d->stream);
+  return SK_OK;
+}
+
+int sk_stream_sync(uintptr_t stream) {
+  cudaStream_t s;
+  int rc = stream_of(stream, &s);
+  if (rc) return rc;
+  SK_TRY(cudaStreamSynchronize(s));
+  return SK_OK;
+}
+
+int sk_device_sync(int device) {
+  SK_TRY(cudaSetDevice(device));
+  SK_TRY(cudaDeviceSynchronize());
+  return SK_OK;
+}
+
+int sk_event_create(uintptr_t* event) {
+  cudaEvent_t e;
+  SK_TRY(cudaEventCreate(&e));
+  *event = reinterpret_cast<uintptr_t>(e);
+  return SK_OK;
+}
+
+int sk_event_destroy(uintptr_t event) {
+  SK_TRY(cudaEventDestroy(reinterpret_cast<cudaEvent_t>(event)));
+  return SK_OK;
+}
+
+int sk_event_record(uintptr_t event, uintptr_t stream) {
+  cudaStream_t s;
+  int rc = stream_of(stream, &s);
+  if (rc) return rc;
+  SK_TRY(cudaEventRecord(reinterpret_cast<cudaEvent_t>(event), s));
+  return SK_OK;
+}
+
+int sk_event_elapsed_ms(uintptr_t start, uintptr_t stop, float* ms) {
+  SK_TRY(cudaEventSynchronize(reinterpret_cast<cudaEvent_t>(stop)));
+  SK_TRY(cudaEventElapsedTime(ms, reinterpret_cast<cudaEvent_t>(start), reinterpret_cast<cudaEvent_t>(stop)));
+  return SK_OK;
+}
+
+int sk_memset_async(void* dst, int byte, size_t nbytes, uintptr_t stream) {
+  if (nbytes == 0) return SK_OK;
+  if (byte < 0 || byte > 255) return set_error(SK_ERR_INVALID, "memset byte %d outside [0, 255]", byte);
+  cudaPointerAttributes a;
+  SK_TRY(cudaPointerGetAttributes(&a, dst));
+  if (a.type != cudaMemoryTypeDevice && a.type != cudaMemoryTypeManaged) {
+    memset(dst, byte, nbytes);  // host-resident buffer
+    return SK_OK;
+  }
+  cudaStream_t s;
+  int rc = stream_of(stream, &s);
+  if (rc) return rc;
+  SK_TRY(cudaMemsetAsync(dst, byte, nbytes, s));
+  return SK_OK;
+}
+
+int sk_memcpy_async(void* dst, const void* src, size_t nbytes, uintptr_t stream) {
+  if (nbytes == 0) return SK_OK;
+  cudaStream_t s;
+  int rc = stream_of(stream, &s);
+  if (rc) return rc;
+  SK_TRY(cudaMemcpyAsync(dst, src, nbytes, cudaMemcpyDefault, s));
+  return SK_OK;
+}
+
+int sk_memmove_async(void* dst, const void* src, size_t nbytes, uintptr_t stream) {
+  if (nbytes == 0 || dst == src) return SK_OK;
+  const char* d = static_cast<const char*>(dst);
+  const char* sp = static_cast<const char*>(src);
+  bool overlap = (d < sp + nbytes) && (sp < d + nbytes);
+  if (!overlap) return sk_memcpy_async(dst, src, nbytes, stream);
+  cudaPointerAttributes a;
+  SK_TRY(cudaPointerGetAttributes(&a, dst));
+  if (a.type != cudaMemoryTypeDevice && a.type != cudaMemoryTypeManaged) {
+    memmove(dst, src, nbytes);
+    return SK_OK;
+  }
+  // device overlap: go through a stream-ordered temporary (copy-via-temp is the
+  // exact memmove contract, memctx.py:356-357)
+  cudaStream_t s;
+  int rc = stream_of(stream, &s);
+  if (rc) return rc;
+  void* tmp = nullptr;
+  SK_TRY(cudaMallocAsync(&tmp, nbytes, s));
+  SK_TRY(cudaMemcpyAsync(tmp, src, nbytes, cudaMemcpyDeviceToDevice, s));
+  SK_TRY(cudaMemcpyAsync(dst, tmp, nbytes, cudaMemcpyDeviceToDevice, s));
+  SK_TRY(cudaFreeAsync(tmp, s));
+  return SK_OK;
+}
+
+int sk_peer_enable(int device, int peer) {
+  if (device == peer) return SK_OK;
+  int can = 0;
+  SK_TRY(cudaDeviceCanAccessPeer(&can, device, peer));
+  if (!can) return set_error(SK_ERR_UNSUPPORTED, "device %d cannot access peer %d", device, peer);
+  SK_TRY(cudaSetDevice(device));
+  cudaError_t e = cudaDeviceEnablePeerAccess(peer, 0);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) {
+    cudaGetLastError();
+    return SK_OK;
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceEnablePeerAccess");
+  return SK_OK;
+}
+
+int sk_malloc_shareable(int device, size_t nbytes, void** out) {
+  if (!out) return set_error(SK_ERR_INVALID, "null out pointer");
+  *out = nullptr;
+  if (nbytes == 0) return SK_OK;
+  DeviceState* d = nullptr;
+  int rc = device_state(device, &d);
+  if (rc) return rc;
+  SK_TRY(cudaStreamSynchronize(d->stream));
+  cudaError_t e = cudaMalloc(out, (nbytes + 255) & ~size_t(255));
+  if (e != cudaSuccess) {
+    *out = nullptr;
+    return cuda_fail(e, "cudaMalloc");
+  }
+  return SK_OK;
+}
+
+int sk_free_shareable(int device, void* ptr) {
+  if (!ptr) return SK_OK;
+  DeviceState* d = nullptr;
+  int rc = device_state(device, &d);
+  if (rc) return rc;
+  SK_TRY(cudaStreamSynchronize(d->stream));
+  SK_TRY(cudaFree(ptr));
+  return SK_OK;
+}
+
+int sk_ipc_handle_size(size_t* nbytes) {
+  *nbytes = sizeof(cudaIpcMemHandle_t);
+  return SK_OK;
+}
+
+int sk_ipc_get_handle(void* dev_ptr, void* handle_out) {
+  cudaIpcMemHandle_t h;
+  SK_TRY(cudaIpcGetMemHandle(&h, dev_ptr));
+  memcpy(handle_out, &h, sizeof(h));
+  return SK_OK;
+}
+
+int sk_ipc_open_handle(int device, const void* handle, void** dev_ptr) {
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  SK_TRY(cudaSetDevice(device));
+  SK_TRY(cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return SK_OK;
+}
+
+int sk_ipc_close_handle(int device, void* dev_ptr) {
+  SK_TRY(cudaSetDevice(device));
+  SK_TRY(cudaIpcCloseMemHandle(dev_ptr));
+  return SK_OK;
+}
+
+}  // extern "C"
+
+// ---- synthetic inputs -----------------------------------------------------------------
+
+namespace sk {
+
+__device__ __forceinline__ uint64_t splitmix64(uint64_t seed, uint64_t k) {
+  uint64_t z = seed + (k + 1) * 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__global__ void fill_random_kernel(uint8_t* dst, size_t nbytes, uint64_t seed, uint64_t first) {
+  const size_t nw = nbytes / 8;
+  const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+  for (size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < nw; i += stride)
+    reinterpret_cast<uint64_t*>(dst)[i] = splitmix64(seed, first + i);
+  const size_t tail = nbytes - nw * 8;
+  if (blockIdx.x == 0 && threadIdx.x < tail)
+    dst[nw * 8 + threadIdx.x] = static_cast<uint8_t>(splitmix64(seed, first + nw) >> (8 * threadIdx.x));
+}
+
+}  // namespace sk
+
+extern "C" int sk_fill_random(void* dst, size_t nbytes, uint64_t seed, uint64_t first_word, uintptr_t stream) {
+  if (nbytes == 0) return SK_OK;
+  if (reinterpret_cast<uintptr_t>(dst) & 7) return set_error(SK_ERR_INVALID, "fill target must be 8-byte aligned");
+  cudaStream_t s;
+  int rc = stream_of(stream, &s);
+  if (rc) return rc;
+  int dev = 0;
+  SK_TRY(cudaGetDevice(&dev));
+  DeviceState* d = nullptr;
+  rc = device_state(dev, &d);
+  if (rc) return rc;
+  sk::fill_random_kernel<<<d->sm_count * 8, 256, 0, s>>>(static_cast<uint8_t*>(dst), nbytes, seed, first_word);
+  SK_TRY(cudaGetLastError());
+  return SK_OK;
+}

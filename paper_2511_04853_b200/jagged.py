@@ -1,0 +1,137 @@
+"""GPU jagged-collection packer (K4): prefix sum + member gather.
+
+Reference semantics (collection.py:537-556, transfer.py:297-320):
+  prefix[0] = 0, prefix[i+1] = sum(len[:i+1]) computed in int64 and stored
+  truncated to the jagged index dtype; pool = concatenation of the segments;
+  multi-leaf members split per leaf into separate pools, all leaves sharing
+  the segment lengths.
+
+Input here is the image of per-object variable-length vectors: a source pool
+of member records (any order, any slack) plus per-record (length, offset)
+pairs. `pack` scans the lengths on the device (single-pass decoupled
+look-back), resizes the jagged tag to the total, and gathers every member into
+the collection's per-leaf pools in record order. Every step runs on the B200;
+host-resident collections are staged through device temporaries.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from typing import Mapping
+
+import numpy as np
+
+from . import _native as nat
+from . import memctx
+from .devarray import DeviceArray
+from .errors import BoundsError, KindError
+from .schema import MAIN_TAG, ROLE_ELEMENT
+
+_NP_CODE = {np.dtype(np.uint8): "u8", np.dtype(np.uint16): "u16", np.dtype(np.uint32): "u32",
+            np.dtype(np.uint64): "u64", np.dtype(np.int32): "i32", np.dtype(np.int64): "i64"}
+
+
+def _as_device(a, dtype, dev: int, keep: list) -> DeviceArray:
+    if isinstance(a, DeviceArray):
+        if a.device != dev:
+            raise KindError(f"device array lives on device {a.device}, packer runs on {dev}")
+        return a
+    arr = np.ascontiguousarray(a, dtype=dtype) if dtype is not None else np.ascontiguousarray(a)
+    d = DeviceArray.from_numpy(arr, memctx.ContextInfo.cuda(dev))
+    keep.append(d)
+    return d
+
+
+def scan(lens: DeviceArray, prefix_ptr: int, prefix_code: str, dev: int, keep: list) -> int:
+    """Exclusive scan of lens into prefix[0..n]; returns the int64 total."""
+    n = lens.n
+    need = C.c_size_t(0)
+    nat.call("sk_jagged_scratch_bytes", n, C.byref(need))
+    scratch = DeviceArray(max(need.value, 16), np.uint8, memctx.ContextInfo.cuda(dev))
+    total = DeviceArray(1, np.int64, memctx.ContextInfo.cuda(dev))
+    keep += [scratch, total]
+    lens_code = _NP_CODE[lens.dtype]
+    nat.call("sk_jagged_scan", n, lens.ptr, nat.TYPE_CODES[lens_code], prefix_ptr, nat.TYPE_CODES[prefix_code],
+             scratch.ptr, need.value, total.ptr, nat.stream(dev))
+    return int(total.numpy()[0])
+
+
+def pack(coll, path: str, lens, src_offsets, src_pool, member_stride: int | None = None,
+         member_offsets: Mapping[str, int] | None = None) -> int:
+    """Fill jagged vector `path` of `coll` from a member pool; returns the total.
+
+    lens[i] members of record i start at member index src_offsets[i] of
+    src_pool (a byte pool of `member_stride`-byte records, or a typed array for
+    single-leaf vectors). member_offsets maps each element leaf of the vector
+    to its byte offset inside a member record (multi-leaf vectors).
+    """
+    desc = coll._jagged_desc(path)
+    plan = coll.plan
+    leaves = [lf for lf in plan.leaves if lf.size_tag == path and lf.role == ROLE_ELEMENT]
+    if any(lf.extent_multiplier != 1 for lf in leaves):
+        raise KindError(f"multi-slot jagged leaves of {path!r} are not supported")
+    n = coll.size()
+    lay = coll.layout
+    dev = lay.device if lay.device is not None else 0
+    keep: list = []
+    lens_d = _as_device(lens, None if isinstance(lens, DeviceArray) else np.int64, dev, keep)
+    if lens_d.n != n:
+        raise BoundsError(f"expected {n} segment lengths, got {lens_d.n}")
+    off_d = _as_device(src_offsets, np.int64, dev, keep)
+    if off_d.n != n:
+        raise BoundsError(f"expected {n} segment offsets, got {off_d.n}")
+    if member_offsets is None:
+        if len(leaves) != 1:
+            raise KindError(f"jagged vector {path!r} has {len(leaves)} leaves; pass member_offsets")
+        member_offsets = {leaves[0].dotted: 0}
+        member_stride = leaves[0].value_type.size_bytes
+    if set(member_offsets) != {lf.dotted for lf in leaves}:
+        raise KindError(f"member_offsets must name exactly the leaves {[lf.dotted for lf in leaves]}")
+    pool_d = _as_device(src_pool, None, dev, keep)
+
+    pleaf = plan.leaf(path + ".prefix_sum")
+    pcode = pleaf.value_type.storage_code
+    psz = pleaf.value_type.size_bytes
+    device_resident = not lay.host_visible
+    if device_resident:
+        prefix_ptr = lay.plane_address(pleaf, 0)
+    else:
+        tmp_p = DeviceArray(n + 1, pleaf.value_type.np_dtype, memctx.ContextInfo.cuda(dev))
+        keep.append(tmp_p)
+        prefix_ptr = tmp_p.ptr
+    total = scan(lens_d, prefix_ptr, pcode, dev, keep)
+
+    coll._bump()
+    with lay.engine_ops():
+        lay.reserve(path, total)
+        lay._set_sizes_for_engine({path: total})
+
+    # the scatter needs true positions: if the index dtype wrapped, rescan into int64
+    scatter_ptr, scatter_code = prefix_ptr, pcode
+    if total >= (1 << (8 * psz - (1 if pcode.startswith("i") else 0))):
+        p64 = DeviceArray(n + 1, np.int64, memctx.ContextInfo.cuda(dev))
+        keep.append(p64)
+        scan(lens_d, p64.ptr, "i64", dev, keep)
+        scatter_ptr, scatter_code = p64.ptr, "i64"
+
+    nf = len(leaves)
+    offs = (C.c_int64 * nf)(*[member_offsets[lf.dotted] for lf in leaves])
+    sizes = (C.c_int32 * nf)(*[lf.value_type.size_bytes for lf in leaves])
+    if device_resident:
+        dsts = [lay.plane_address(lf, 0) for lf in leaves]
+    else:
+        tmps = [DeviceArray(total, lf.value_type.np_dtype, memctx.ContextInfo.cuda(dev)) for lf in leaves]
+        keep += tmps
+        dsts = [t.ptr for t in tmps]
+    ptrs = (C.c_void_p * nf)(*dsts)
+    nat.call("sk_jagged_scatter", n, scatter_ptr, nat.TYPE_CODES[scatter_code], off_d.ptr, pool_d.ptr,
+             int(member_stride), nf, offs, sizes, ptrs, total, nat.stream(dev))
+    if not device_resident:
+        nat.memcpy(lay.plane_address(pleaf, 0), prefix_ptr, (n + 1) * psz, dev)
+        for lf, src in zip(leaves, dsts):
+            if total:
+                nat.memcpy(lay.plane_address(lf, 0), src, total * lf.value_type.size_bytes, dev)
+    nat.sync(dev)
+    for t in keep:
+        t.free()
+    return total

@@ -1,0 +1,150 @@
+"""The paper's case study on the B200: sensor/particle schemas, the per-object
+calibration/noise kernel (K5) and the fused transfer + calibrate path.
+
+Schemas follow detector/schemas.py:56-90 (Listings 1, 2, 4 of the paper);
+SENSOR_AOS_DTYPE is the 30-byte packed record of detector/baselines.py:19-35,
+byte-identical to AosLayout's image of the Sensor plan.
+
+The collection-target behaviors registered under "sensor_funcs" launch K5 on
+CUDA-resident collections. Host-resident collections are refused with
+AccessError: in this framework the case-study kernel is device code, as
+inside the reference's execution_scope(mockdev) (memctx.py:369-395).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _native as nat
+from . import behaviors as bh
+from . import convert as cv
+from . import layouts as ly
+from . import memctx
+from . import schema as sc
+from .devarray import DeviceArray
+from .errors import AccessError, UnsupportedTransferError
+
+NUM_SENSOR_TYPES = 4
+SENSOR_TYPE = sc.enum_type("SensorType", NUM_SENSOR_TYPES)
+
+SENSOR_AOS_DTYPE = np.dtype([
+    ("type", "u1"), ("counts", "<u8"), ("energy", "<f4"),
+    ("calibration_data", [("noisy", "?"), ("parameter_A", "<f4"), ("parameter_B", "<f4"),
+                          ("noise_A", "<f4"), ("noise_B", "<f4")]),
+])
+
+_COUNTS, _ENERGY, _NOISY = "counts", "energy", "calibration_data.noisy"
+_A, _B = "calibration_data.parameter_A", "calibration_data.parameter_B"
+_NA, _NB = "calibration_data.noise_A", "calibration_data.noise_B"
+
+
+def _device_planes(coll) -> tuple[int, dict]:
+    lay = coll.layout
+    if lay.host_visible:
+        raise AccessError(
+            f"the case-study kernel runs on the B200; move the collection to ContextInfo.cuda() first "
+            f"(it is {coll.info.context!r}-resident)"
+        )
+    if isinstance(lay, ly.AosLayout):
+        raise UnsupportedTransferError("case-study kernel reads per_field/arena planes; convert the AoS collection first")
+    names = (_COUNTS, _ENERGY, _NOISY, _A, _B, _NA, _NB)
+    return lay.device, {k: lay.plane_address(coll.plan.leaf(k), 0) for k in names}
+
+
+def calibrate_collection(coll, sync: bool = True) -> None:
+    """energy = A * f32(counts) + B on the device (detector/schemas.py:29-33)."""
+    dev, p = _device_planes(coll)
+    n = coll.size()
+    nat.call("sk_sensor_calibrate", n, p[_COUNTS], p[_A], p[_B], p[_ENERGY], nat.stream(dev))
+    if sync:
+        nat.sync(dev)
+
+
+def noise_for_collection(coll, out: DeviceArray | None = None, sync: bool = True) -> DeviceArray:
+    """Per-sensor noise as a device f32 array (detector/schemas.py:36-41)."""
+    dev, p = _device_planes(coll)
+    n = coll.size()
+    if out is None:
+        out = DeviceArray(n, np.float32, memctx.ContextInfo.cuda(dev))
+    nat.call("sk_sensor_noise", n, p[_ENERGY], p[_NA], p[_NB], p[_NOISY], out.ptr, nat.stream(dev))
+    if sync:
+        nat.sync(dev)
+    return out
+
+
+def transfer_calibrate(dst, src, noise: DeviceArray | None = None, sync: bool = True) -> DeviceArray:
+    """Fused K1+K5: AoS sensor records (any placement) -> per_field/arena planes
+    on the device with energy calibrated, plus the noise column, one HBM pass.
+
+    Equivalent to copy_collection(dst, src) followed by calibrate_energy() and
+    get_noise() (bench.py:174-178 prepare phase)."""
+    sl, dl = src.layout, dst.layout
+    if not isinstance(sl, ly.AosLayout) or isinstance(dl, ly.AosLayout):
+        raise UnsupportedTransferError("fused sensor path converts AoS records into planes")
+    if dl.host_visible:
+        raise AccessError("fused sensor path writes a device-resident destination")
+    if dst.plan != src.plan or dst.plan != SENSOR_PLAN:
+        raise UnsupportedTransferError("fused sensor path needs the Sensor plan on both sides")
+    from .transfer import _match_sizes  # same reserve-then-size contract as copy_collection
+
+    _match_sizes(dst, src)
+    n = sl.size(sc.MAIN_TAG)
+    dev = dl.device
+    if noise is None:
+        noise = DeviceArray(n, np.float32, memctx.ContextInfo.cuda(dev))
+    desc = cv.plan_desc(dl, sl, n)
+    names = [lf.dotted for lf, _ in cv.main_slots(sl)]
+    idx = [names.index(k) for k in (_COUNTS, _ENERGY, _NOISY, _A, _B, _NA, _NB)]
+    if n:
+        nat.call("sk_sensor_convert_calibrate", C.byref(desc), *idx, noise.ptr, dev, nat.stream(dev))
+    dst._bump()
+    if sync:
+        nat.sync(dev)
+    return noise
+
+
+def _calibrate_behavior(coll) -> None:
+    calibrate_collection(coll)
+
+
+def _noise_behavior(coll) -> DeviceArray:
+    return noise_for_collection(coll)
+
+
+if not bh.is_registered("sensor_funcs"):
+    bh.register_bundle("sensor_funcs", [
+        bh.BehaviorFunction("calibrate_energy", bh.TARGET_COLLECTION, _calibrate_behavior),
+        bh.BehaviorFunction("get_noise", bh.TARGET_COLLECTION, _noise_behavior),
+    ])
+
+SENSOR_SCHEMA = sc.Schema("Sensor", (
+    sc.declare_per_item("type", SENSOR_TYPE),
+    sc.declare_per_item("counts", sc.U64),
+    sc.declare_per_item("energy", sc.F32),
+    sc.declare_subgroup("calibration_data", [
+        sc.declare_per_item("noisy", sc.BOOL),
+        sc.declare_per_item("parameter_A", sc.F32),
+        sc.declare_per_item("parameter_B", sc.F32),
+        sc.declare_per_item("noise_A", sc.F32),
+        sc.declare_per_item("noise_B", sc.F32),
+    ]),
+    sc.declare_behavior("funcs", "sensor_funcs"),
+))
+
+PARTICLE_SCHEMA = sc.Schema("Particle", (
+    sc.declare_per_item("energy", sc.F32),
+    sc.declare_per_item("x", sc.F32),
+    sc.declare_per_item("y", sc.F32),
+    sc.declare_per_item("origin", sc.U64),
+    sc.declare_jagged("sensors", sc.I32, sc.U64),
+    sc.declare_per_item("x_variance", sc.F32),
+    sc.declare_per_item("y_variance", sc.F32),
+    sc.declare_array("significance", NUM_SENSOR_TYPES, sc.F32),
+    sc.declare_array("E_contribution", NUM_SENSOR_TYPES, sc.F32),
+    sc.declare_array("noisy_count", NUM_SENSOR_TYPES, sc.U8),
+))
+
+SENSOR_PLAN = sc.flatten(SENSOR_SCHEMA)
+PARTICLE_PLAN = sc.flatten(PARTICLE_SCHEMA)

@@ -1,0 +1,217 @@
+"""Collection-to-collection transfers through a priority-ordered registry.
+
+Same registry contract as soakit/transfer.py (register_transfer 67-77,
+resolution by (priority, registration order) 90-91, copy_collection 94-116
+returning the chosen spec name, move_collection 119-124). Built-ins:
+
+  b200-convert     EXACT_PAIR. Any pair whose record representations differ
+                   (AoS <-> planes) between host/pinned/cuda placements. Main-
+                   tag element leaves go through ONE launch of the conversion
+                   engine (sk_convert): device-resident endpoints are converted
+                   in HBM, host endpoints stream through the chunked H2D |
+                   convert | D2H pipeline, a peer-device source is pulled over
+                   NVLink. Side leaves (prefix sums, jagged pools, globals) are
+                   plane copies. Replaces per-leaf-default (transfer.py:171-236)
+                   and lifts its restriction that AoS destinations must be on
+                   the host (transfer.py:165-167).
+  bulk-same-kind   SAME_LAYOUT_KIND. Identical to the reference
+                   (transfer.py:130-146): refit, one copy per buffer.
+  plane-copy       PER_LEAF_DEFAULT. Planes on both sides (per_field <->
+                   arena, arenas with different specs): one copy per plane on
+                   the copy engines.
+
+There is no CPU conversion path: a conversion without a usable B200 raises.
+"""
+
+from __future__ import annotations
+
+import itertools
+from dataclasses import dataclass, field
+from enum import IntEnum
+from typing import Any, Callable, Mapping
+
+from . import _native as nat
+from . import convert as cv
+from . import layouts as ly
+from . import memctx
+from .collection import Collection
+from .errors import RegistryError, SchemaMismatchError, TransferError, UnsupportedTransferError
+from .schema import MAIN_TAG, ROLE_ELEMENT
+
+
+class TransferPriority(IntEnum):
+    EXACT_PAIR = 0
+    SAME_LAYOUT_KIND = 1
+    PER_LEAF_DEFAULT = 2
+
+
+@dataclass(frozen=True)
+class TransferSpec:
+    name: str
+    priority: TransferPriority
+    applies: Callable[[Collection, Collection], bool]
+    execute: Callable[[Collection, Collection, Mapping[str, Any] | None], None]
+    seq: int = field(default=0, compare=False)
+
+
+_specs: dict[str, TransferSpec] = {}
+_seq = itertools.count()
+_chosen: dict[str, int] = {}
+
+
+def chosen_transfer_counts() -> dict[str, int]:
+    return dict(_chosen)
+
+
+def reset_transfer_counts() -> None:
+    _chosen.clear()
+
+
+def register_transfer(name: str, priority: TransferPriority, applies, execute) -> None:
+    if name in _specs:
+        raise RegistryError(f"transfer spec {name!r} is already registered")
+    _specs[name] = TransferSpec(name, TransferPriority(priority), applies, execute, next(_seq))
+
+
+def unregister_transfer(name: str) -> None:
+    if name not in _specs:
+        raise RegistryError(f"no transfer spec named {name!r}")
+    del _specs[name]
+
+
+def _ordered() -> list[TransferSpec]:
+    return sorted(_specs.values(), key=lambda s: (int(s.priority), s.seq))
+
+
+def registered_transfers() -> tuple[str, ...]:
+    return tuple(s.name for s in _ordered())
+
+
+def copy_collection(dst: Collection, src: Collection, opts: Mapping[str, Any] | None = None) -> str:
+    """Copy src's logical content into dst; returns the name of the spec used."""
+    if dst is src or dst.layout is src.layout:
+        raise TransferError("source and destination alias the same storage")
+    if dst.plan != src.plan:
+        raise SchemaMismatchError(f"collections flatten differently: {src.schema.name!r} vs {dst.schema.name!r}")
+    for spec in _ordered():
+        if spec.applies(dst, src):
+            spec.execute(dst, src, opts)
+            dst._bump()
+            _chosen[spec.name] = _chosen.get(spec.name, 0) + 1
+            return spec.name
+    raise UnsupportedTransferError(
+        f"no transfer applies for ({src.kind}, {src.info.context}) -> ({dst.kind}, {dst.info.context}); "
+        f"tried {[s.name for s in _ordered()]}"
+    )
+
+
+def move_collection(dst: Collection, src: Collection, opts: Mapping[str, Any] | None = None) -> str:
+    name = copy_collection(dst, src, opts)
+    with src.layout.engine_ops():
+        src.clear()
+    return name
+
+
+# ---- shared helpers -----------------------------------------------------------------------------
+
+_ENGINE_CONTEXTS = (memctx.HOST, memctx.PINNED, memctx.CUDA)
+
+
+def _engine_device(dst: Collection, src: Collection) -> int:
+    """The GPU that runs the conversion: the destination's if device-resident,
+    else the source's, else device 0 (host <-> host staged through HBM)."""
+    for c in (dst, src):
+        if c.device is not None:
+            return c.device
+    return 0
+
+
+def _match_sizes(dst: Collection, src: Collection) -> None:
+    """Reserve then set sizes: capacity errors surface before any write
+    (transfer.py:177-180, test_transfer.py:292-300)."""
+    sl, dl = src.layout, dst.layout
+    with dl.engine_ops():
+        for tag in sl.tags():
+            dl.reserve(tag, sl.size(tag))
+        dl._set_sizes_for_engine({tag: sl.size(tag) for tag in sl.tags()})
+
+
+def _copy_planes(dst: Collection, src: Collection, leaves, opts) -> None:
+    sl, dl = src.layout, dst.layout
+    for leaf in leaves:
+        n = sl.plane_len(leaf)
+        if n == 0:
+            continue
+        isz = leaf.value_type.size_bytes
+        for k in range(sl.plane_count(leaf)):
+            s_buf, s_off = sl._plane_region(leaf, k)
+            d_buf, d_off = dl._plane_region(leaf, k)
+            memctx.memcopy_with_context(d_buf, d_off, s_buf, s_off, n * isz, opts)
+
+
+def _sync(dst: Collection, src: Collection, opts, engine: int | None = None) -> None:
+    if opts and opts.get("async"):
+        return
+    for dev in {dst.device, src.device, engine} - {None}:
+        nat.sync(dev)
+
+
+# ---- b200-convert ------------------------------------------------------------------------------
+
+def _has_struct(c: Collection) -> bool:
+    return isinstance(c.layout, ly.AosLayout) and c.layout._struct_buf is not None
+
+
+def _convert_applies(dst: Collection, src: Collection) -> bool:
+    if src.info.context not in _ENGINE_CONTEXTS or dst.info.context not in _ENGINE_CONTEXTS:
+        return False
+    return _has_struct(src) != _has_struct(dst)
+
+
+def _convert_execute(dst: Collection, src: Collection, opts: Mapping[str, Any] | None = None) -> None:
+    _match_sizes(dst, src)
+    sl, dl = src.layout, dst.layout
+    n = sl.size(MAIN_TAG)
+    dev = _engine_device(dst, src)
+    desc = cv.plan_desc(dl, sl, n)
+    if desc is not None and n:
+        cv.run(desc, dev)
+    side = [lf for lf in sl.plan.leaves if not (lf.size_tag == MAIN_TAG and lf.role == ROLE_ELEMENT)]
+    _copy_planes(dst, src, side, {"async": True})
+    _sync(dst, src, opts, dev)
+
+
+# ---- bulk-same-kind (transfer.py:130-146) -------------------------------------------------------
+
+def _bulk_applies(dst: Collection, src: Collection) -> bool:
+    if src.kind != dst.kind or not memctx.has_copier(src.info.context, dst.info.context):
+        return False
+    return not (src.kind == ly.ARENA and src.layout.arena_spec != dst.layout.arena_spec)
+
+
+def _bulk_execute(dst: Collection, src: Collection, opts: Mapping[str, Any] | None = None) -> None:
+    sl, dl = src.layout, dst.layout
+    with dl.engine_ops():
+        dl._refit_for_engine(sl)
+    for sb, db in zip(sl.buffers(), dl.buffers()):
+        if sb.length_bytes:
+            memctx.memcopy_with_context(db, 0, sb, 0, sb.length_bytes, {"async": True})
+    _sync(dst, src, opts)
+
+
+# ---- plane-copy ---------------------------------------------------------------------------------
+
+def _planes_applies(dst: Collection, src: Collection) -> bool:
+    return (not _has_struct(src) and not _has_struct(dst)
+            and memctx.has_copier(src.info.context, dst.info.context))
+
+
+def _planes_execute(dst: Collection, src: Collection, opts: Mapping[str, Any] | None = None) -> None:
+    _match_sizes(dst, src)
+    _copy_planes(dst, src, src.plan.leaves, {"async": True})
+    _sync(dst, src, opts)
+
+
+register_transfer("b200-convert", TransferPriority.EXACT_PAIR, _convert_applies, _convert_execute)
+register_transfer("bulk-same-kind", TransferPriority.SAME_LAYOUT_KIND, _bulk_applies, _bulk_execute)
+register_transfer("plane-copy", TransferPriority.PER_LEAF_DEFAULT, _planes_applies, _planes_execute)

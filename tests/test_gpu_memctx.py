@@ -1,0 +1,96 @@
+"""The cuda / pinned memory contexts: copier matrix, device memmove contract
+(C5, test_acceptance.py:558-583), device-side size changes, migration."""
+
+import numpy as np
+import pytest
+
+import paper_2511_04853_b200 as sk
+from gpuhelp import CUDA, HOST, PINNED
+from paper_2511_04853_b200 import layouts as ly
+from paper_2511_04853_b200 import memctx as mc
+from paper_2511_04853_b200 import sensor, transfer as tr
+
+pytestmark = pytest.mark.gpu
+
+
+def test_copier_matrix_round_trips():
+    pattern = np.random.default_rng(1).integers(0, 256, 4096, dtype=np.uint8)
+    infos = [HOST, PINNED, CUDA]
+    for a in infos:
+        for b in infos:
+            src = mc.allocate(HOST, 4096)
+            src._data[:] = pattern
+            x = mc.allocate(a, 4096)
+            y = mc.allocate(b, 4096)
+            mc.memcopy_with_context(x, 0, src, 0, 4096)
+            mc.memcopy_with_context(y, 100, x, 0, 3000)
+            out = mc.allocate(HOST, 4096)
+            out._data[:] = 0
+            mc.memcopy_with_context(out, 0, y, 100, 3000)
+            assert np.array_equal(out._data[:3000], pattern[:3000]), (a, b)
+            for buf in (src, x, y, out):
+                mc.deallocate(buf)
+
+
+def test_device_memmove_overlap_oracle():
+    """Exhaustive same-buffer copies on a 48-byte device buffer vs copy-via-temp."""
+    size = 48
+    buf = mc.allocate(CUDA, size)
+    stage = mc.allocate(PINNED, size)
+    base = np.arange(size, dtype=np.uint8)
+    bad = 0
+    for count in range(0, size + 1, 3):
+        for s in range(size + 1 - count):
+            for d in range(size + 1 - count):
+                stage._data[:] = base
+                mc.memcopy_with_context(buf, 0, stage, 0, size)
+                mc.memcopy_with_context(buf, d, buf, s, count)
+                mc.memcopy_with_context(stage, 0, buf, 0, size)
+                exp = base.copy()
+                exp[d : d + count] = base[s : s + count]
+                bad += not np.array_equal(stage._data, exp)
+    assert bad == 0
+
+
+def test_device_resize_insert_erase_match_host():
+    rng = np.random.default_rng(2)
+    host = sk.Collection(sensor.PARTICLE_SCHEMA, ly.PER_FIELD, HOST)
+    dev = sk.Collection(sensor.PARTICLE_SCHEMA, ly.PER_FIELD, CUDA)
+    host.resize(20)
+    host.column("energy").np[:] = rng.standard_normal(20).astype(np.float32)
+    host.column("noisy_count").np[:] = rng.integers(0, 255, (4, 20))
+    host.jagged_fill("sensors", [rng.integers(0, 99, rng.integers(0, 4), dtype=np.uint64) for _ in range(20)])
+    tr.copy_collection(dev, host)
+    for c, scope in ((host, mc.HOST), (dev, mc.CUDA)):
+        with mc.execution_scope(scope):
+            c.insert_records(3, 5)
+            c.erase_records(10, 4)
+            c.jagged_resize("sensors", 2, 7)
+            c.resize(30)
+            c.resize(25)
+    back = sk.Collection(sensor.PARTICLE_SCHEMA, ly.PER_FIELD, HOST)
+    tr.copy_collection(back, dev)
+    assert back.dump() == host.dump()
+
+
+def test_device_collection_refuses_host_scope_access():
+    dev = sk.Collection(sensor.SENSOR_SCHEMA, ly.PER_FIELD, CUDA)
+    with pytest.raises(sk.NotResizableError):
+        dev.resize(3)
+    with mc.execution_scope(mc.CUDA):
+        dev.resize(3)
+    with pytest.raises(sk.AccessError):
+        dev.column("energy").read()
+    with mc.execution_scope(mc.CUDA), pytest.raises(sk.AccessError):
+        dev.column("energy").np
+
+
+def test_migration_round_trip_keeps_contents():
+    c = sk.Collection(sensor.PARTICLE_SCHEMA, ly.AOS, HOST)
+    c.resize(11)
+    c.column("origin").np[:] = np.arange(11, dtype=np.uint64) * 3
+    c.jagged_fill("sensors", [[i] * (i % 3) for i in range(11)])
+    ref = c.dump()
+    for info in (CUDA, PINNED, CUDA, HOST):
+        c.update_memory_context_info(info)
+    assert c.dump() == ref

@@ -1,0 +1,116 @@
+"""Case-study kernel (K5) and the fused transfer + calibrate path vs the
+reference's golden energies/noises (bit-exact: the reference pins energy bytes
+across layouts, test_detector.py:200-214)."""
+
+import numpy as np
+import pytest
+
+import paper_2511_04853_b200 as sk
+from gpuhelp import CUDA, HOST, PINNED, aos_collection, to_host_planes
+from oracle import restate as R
+from paper_2511_04853_b200 import layouts as ly
+from paper_2511_04853_b200 import memctx as mc
+from paper_2511_04853_b200 import sensor, transfer as tr
+from skhelp import golden
+
+pytestmark = pytest.mark.gpu
+
+EVENTS = ["sensor_16x16_s5.npz", "sensor_64x64_s3.npz", "sensor_101x37_s11.npz"]
+
+
+@pytest.mark.parametrize("name", EVENTS)
+def test_behaviors_on_device_match_reference(name):
+    g = golden(name)
+    n = int(g["w"] * g["h"])
+    host = aos_collection(sensor.SENSOR_SCHEMA, g["aos"], n, HOST)
+    dev = sk.Collection(sensor.SENSOR_SCHEMA, ly.PER_FIELD, CUDA)
+    assert tr.copy_collection(dev, host) == "b200-convert"
+    with mc.execution_scope(mc.CUDA):
+        dev.funcs.calibrate_energy()
+        noise = dev.funcs.get_noise()
+        energy = dev.column("energy").read()
+    assert energy.tobytes() == g["energy"].tobytes()
+    assert noise.numpy().tobytes() == g["noise"].tobytes()
+
+
+@pytest.mark.parametrize("name", EVENTS)
+@pytest.mark.parametrize("src_ctx", ["host", "pinned", "cuda"])
+def test_fused_transfer_calibrate_matches_reference(name, src_ctx):
+    g = golden(name)
+    n = int(g["w"] * g["h"])
+    src = aos_collection(sensor.SENSOR_SCHEMA, g["aos"], n, PINNED if src_ctx == "pinned" else HOST)
+    if src_ctx == "cuda":
+        d = sk.Collection(sensor.SENSOR_SCHEMA, ly.AOS, CUDA)
+        tr.copy_collection(d, src)
+        src = d
+    dev = sk.Collection(sensor.SENSOR_SCHEMA, ly.PER_FIELD, CUDA)
+    noise = sensor.transfer_calibrate(dev, src)
+    assert noise.numpy().tobytes() == g["noise"].tobytes()
+    planes = to_host_planes(dev)
+    assert planes["energy#0"] == g["energy"].tobytes()
+    recs = g["aos"].view(R.SENSOR_AOS_DTYPE)
+    assert planes["counts#0"] == np.ascontiguousarray(recs["counts"]).tobytes()
+    assert planes["calibration_data.noise_B#0"] == np.ascontiguousarray(recs["calibration_data"]["noise_B"]).tobytes()
+
+
+def test_golden_values_and_exact_doubling():
+    # test_detector.py:184-187 and 228-239
+    dev = sk.Collection(sensor.SENSOR_SCHEMA, ly.PER_FIELD, CUDA)
+    host = sk.Collection(sensor.SENSOR_SCHEMA, ly.PER_FIELD, HOST)
+    host.resize(3)
+    host.column("counts").np[:] = [100, 0, 7]
+    host.column("calibration_data.parameter_A").np[:] = [0.5, 1.0, 1.25]
+    host.column("calibration_data.parameter_B").np[:] = [2.0, 0.0, 0.75]
+    host.column("calibration_data.noise_A").np[:] = [1.25, 1.0, 1.25]
+    host.column("calibration_data.noise_B").np[:] = [0.75, 0.1, 0.75]
+    host.column("calibration_data.noisy").np[:] = [False, False, True]
+    tr.copy_collection(dev, host)
+    sensor.calibrate_collection(dev)
+    nz = sensor.noise_for_collection(dev).numpy()
+    with mc.execution_scope(mc.CUDA):
+        e = dev.column("energy").read()
+    assert e[0] == np.float32(52.0) and e[1] == np.float32(0.0)
+    assert nz[1] == np.float32(0.1)
+    quiet = np.float32(1.25) * np.sqrt(e[2]) + np.float32(0.75)
+    assert nz[2] == np.float32(2.0) * quiet
+
+
+def test_batched_full_size_events_vs_oracle():
+    """Config 2 shape: 436 x 436 = 190,096 cells per event, 8 events batched."""
+    evs = [R.generate_event(436, 436, seed=s, density=0.002) for s in range(8)]
+    recs = np.concatenate([R.sensor_aos(ev) for ev in evs])
+    n = recs.size
+    src = aos_collection(sensor.SENSOR_SCHEMA, recs, n, PINNED)
+    dev = sk.Collection(sensor.SENSOR_SCHEMA, ly.PER_FIELD, CUDA)
+    noise = sensor.transfer_calibrate(dev, src).numpy()
+    e = R.calibrate(recs["counts"], recs["calibration_data"]["parameter_A"], recs["calibration_data"]["parameter_B"])
+    nz = R.noise(e, recs["calibration_data"]["noise_A"], recs["calibration_data"]["noise_B"],
+                 recs["calibration_data"]["noisy"])
+    assert to_host_planes(dev)["energy#0"] == e.tobytes()
+    assert noise.tobytes() == nz.tobytes()
+
+
+def test_special_values_vs_oracle():
+    rng = np.random.default_rng(11)
+    n = 65537
+    recs = np.zeros(n, R.SENSOR_AOS_DTYPE)
+    recs["counts"] = rng.integers(0, np.iinfo(np.uint64).max, n, dtype=np.uint64, endpoint=True)
+    cal = recs["calibration_data"]
+    for k in ("parameter_A", "parameter_B", "noise_A", "noise_B"):
+        cal[k] = (rng.standard_normal(n) * 10 ** rng.integers(-40, 30, n)).astype(np.float32)
+    cal["parameter_A"][:16] = [np.nan, np.inf, -np.inf, 0.0, -0.0, 1e-45, -1e-45, 3e38] * 2
+    cal["noisy"] = rng.integers(0, 2, n).astype(bool)
+    src = aos_collection(sensor.SENSOR_SCHEMA, recs, n, HOST)
+    dev = sk.Collection(sensor.SENSOR_SCHEMA, ly.PER_FIELD, CUDA)
+    with np.errstate(all="ignore"):
+        e = R.calibrate(recs["counts"], cal["parameter_A"], cal["parameter_B"])
+        nz = R.noise(e, cal["noise_A"], cal["noise_B"], cal["noisy"])
+    noise = sensor.transfer_calibrate(dev, src).numpy()
+    assert to_host_planes(dev)["energy#0"] == e.tobytes()
+    assert noise.tobytes() == nz.tobytes()
+
+
+def test_host_resident_collection_is_refused():
+    host = sk.Collection(sensor.SENSOR_SCHEMA, ly.PER_FIELD, HOST)
+    with pytest.raises(sk.AccessError):
+        host.funcs.calibrate_energy()

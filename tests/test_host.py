@@ -1,0 +1,211 @@
+"""Host-side logic (no GPU): plans, byte geometry, registries, descriptors, ABI."""
+
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_2511_04853_b200 as sk
+from paper_2511_04853_b200 import _native as nat
+from paper_2511_04853_b200 import convert as cv
+from paper_2511_04853_b200 import layouts as ly
+from paper_2511_04853_b200 import memctx as mc
+from paper_2511_04853_b200 import schema as sc
+from paper_2511_04853_b200 import sensor, shard, transfer as tr, workloads as wl
+from skhelp import ROOT, golden
+
+
+def _leaf_sig(plan):
+    return [f"{lf.dotted}|{lf.value_type.np_dtype.str}|{lf.size_tag}|{lf.extent_multiplier}|{lf.role}"
+            for lf in plan.leaves]
+
+
+def test_flatten_matches_reference_plans():
+    g = golden("geometry.npz")
+    assert _leaf_sig(sensor.PARTICLE_PLAN) == list(g["particle_leaves"])
+    assert _leaf_sig(sensor.SENSOR_PLAN) == list(g["sensor_leaves"])
+
+
+def test_record_strides_match_reference():
+    g = golden("geometry.npz")
+    for schema, key in ((sensor.PARTICLE_SCHEMA, "particle_stride"), (sensor.SENSOR_SCHEMA, "sensor_stride")):
+        lay = ly.build_layout(ly.AOS, sc.flatten(schema))
+        assert lay.record_stride == int(g[key])
+        lay.free()
+    assert ly.build_layout(ly.AOS, sc.flatten(wl.OBJ8_SCHEMA)).record_stride == 32
+    assert ly.build_layout(ly.AOS, sc.flatten(wl.TRACK_SCHEMA)).record_stride == 60
+
+
+def test_sensor_struct_dtype_is_the_handwritten_aos_image():
+    lay = ly.build_layout(ly.AOS, sensor.SENSOR_PLAN)
+    offs = lay.struct_offsets
+    assert [offs[k] for k in ("type", "counts", "energy", "calibration_data.noisy",
+                              "calibration_data.parameter_A", "calibration_data.noise_B")] == [0, 1, 9, 13, 14, 26]
+    assert sensor.SENSOR_AOS_DTYPE.itemsize == 30
+
+
+@pytest.mark.parametrize("align", [16, 64, 4096])
+def test_arena_offsets_match_reference(align):
+    g = golden("geometry.npz")
+    lay = ly.build_layout(ly.ARENA, sensor.PARTICLE_PLAN, None, ly.ArenaSpec({sc.MAIN_TAG: 10, "sensors": 33}, align))
+    assert [lay.leaf_offset(lf) for lf in sensor.PARTICLE_PLAN.leaves] == list(g[f"arena_offsets_{align}"])
+    assert lay.total_bytes == int(g[f"arena_total_{align}"])
+    assert all(lay.leaf_offset(lf) % align == 0 for lf in sensor.PARTICLE_PLAN.leaves)
+
+
+def test_growth_policy_matches_reference():
+    g = golden("geometry.npz")
+    lay = ly.build_layout(ly.PER_FIELD, sensor.PARTICLE_PLAN)
+    caps = []
+    for n in (1, 5, 17):
+        lay.resize(sc.MAIN_TAG, n)
+        caps.append(lay.capacity(sc.MAIN_TAG))
+    assert caps == list(g["growth"]) == [4, 8, 17]
+
+
+def test_per_field_slot_planes_at_capacity_pitch():
+    c = sk.Collection(sensor.PARTICLE_SCHEMA, ly.PER_FIELD)
+    c.resize(6)
+    lay = c.layout
+    leaf = c.plan.leaf("E_contribution.value")
+    assert lay.plane_address(leaf, 2) - lay.plane_address(leaf, 0) == 2 * lay.capacity() * 4
+    for flat in range(24):
+        lay.write_element(leaf, flat, np.float32(flat * 0.5))
+    col = lay.column_np(leaf)
+    assert col[3, 5] == np.float32((3 * 6 + 5) * 0.5)
+
+
+def test_plan_desc_aos_to_planes_fields():
+    src = sk.Collection(sensor.PARTICLE_SCHEMA, ly.AOS)
+    dst = sk.Collection(sensor.PARTICLE_SCHEMA, ly.PER_FIELD)
+    for c in (src, dst):
+        c.resize(9)
+    d = cv.plan_desc(dst.layout, src.layout, 9)
+    assert d.src_kind == nat.KIND_AOS and d.dst_kind == nat.KIND_PLANES
+    assert d.src_stride == 64 and d.nfields == 6 + 4 + 4 + 4
+    offs = [d.fields[i].src_off for i in range(d.nfields)]
+    assert offs[:6] == [0, 4, 8, 12, 20, 24] and offs[6:10] == [28, 32, 36, 40] and offs[-4:] == [60, 61, 62, 63]
+    leaf = dst.plan.leaf("noisy_count.value")
+    assert d.fields[d.nfields - 1].dst_plane == dst.layout.plane_address(leaf, 3)
+    assert d.fields[3].src_type == nat.TYPE_CODES["u64"]
+
+
+def test_host_memmove_contract_exhaustive_small():
+    # the C5 overlap oracle (test_acceptance.py:558-583) on the host copier, n=24
+    buf = mc.allocate(mc.ContextInfo.host(), 24)
+    base = np.arange(24, dtype=np.uint8)
+    for count in range(25):
+        for s in range(25 - count):
+            for d in range(25 - count):
+                buf._data[:] = base
+                mc.memcopy_with_context(buf, d, buf, s, count)
+                exp = base.copy()
+                exp[d : d + count] = base[s : s + count]
+                assert np.array_equal(buf._data, exp)
+    mc.deallocate(buf)
+
+
+def test_memcopy_validation_errors():
+    a = mc.allocate(mc.ContextInfo.host(), 8)
+    b = mc.allocate(mc.ContextInfo.host(), 8)
+    with pytest.raises(sk.CopyError):
+        mc.memcopy_with_context(a, 0, b, 4, 8)
+    with pytest.raises(sk.CopyError):
+        mc.memcopy_with_context(a, 0, b, 0, 4, {"stream": 3})  # test_memctx.py:139-146
+    mc.deallocate(b)
+    with pytest.raises(sk.BufferStateError):
+        mc.memcopy_with_context(a, 0, b, 0, 4)
+    with pytest.raises(sk.BufferStateError):
+        mc.deallocate(b)
+    mc.deallocate(a)
+
+
+def test_cuda_context_params_and_guards():
+    ctx = mc.get_context(mc.CUDA)
+    ctx.validate_params({"device_id": 1})
+    for bad in ({"device_id": -1}, {"device_id": "0"}, {"stream": 1}):
+        with pytest.raises(sk.MemoryContextError):
+            ctx.validate_params(bad)
+    assert ctx.device_of({"device_id": 3}) == 3
+    assert not ctx.host_visible and mc.get_context(mc.PINNED).host_visible
+
+
+def test_registry_order_and_choice_predicates():
+    assert tr.registered_transfers()[:3] == ("b200-convert", "bulk-same-kind", "plane-copy")
+    with pytest.raises(sk.RegistryError):
+        tr.register_transfer("bulk-same-kind", tr.TransferPriority.SAME_LAYOUT_KIND, lambda d, s: False, None)
+    a = sk.Collection(wl.OBJ8_SCHEMA, ly.AOS)
+    p = sk.Collection(wl.OBJ8_SCHEMA, ly.PER_FIELD)
+    r = sk.Collection(wl.OBJ8_SCHEMA, ly.ARENA, None, ly.ArenaSpec({sc.MAIN_TAG: 16}))
+    assert tr._convert_applies(p, a) and tr._convert_applies(a, p)
+    assert not tr._convert_applies(p, r) and tr._planes_applies(p, r) and tr._planes_applies(r, p)
+    assert tr._bulk_applies(a, sk.Collection(wl.OBJ8_SCHEMA, ly.AOS))
+
+
+def test_copy_collection_rejects_alias_and_mismatch():
+    a = sk.Collection(wl.OBJ8_SCHEMA, ly.PER_FIELD)
+    with pytest.raises(sk.TransferError):
+        tr.copy_collection(a, a)
+    with pytest.raises(sk.SchemaMismatchError):
+        tr.copy_collection(sk.Collection(wl.TRACK_SCHEMA), a)
+
+
+def test_same_kind_host_transfer_is_bulk_and_exact():
+    src = sk.Collection(wl.OBJ8_SCHEMA, ly.PER_FIELD)
+    src.resize(50)
+    src.column("f0").np[:] = np.arange(50, dtype=np.float32)
+    dst = sk.Collection(wl.OBJ8_SCHEMA, ly.PER_FIELD)
+    assert tr.copy_collection(dst, src) == "bulk-same-kind"
+    assert np.array_equal(dst.column("f0").read(), np.arange(50, dtype=np.float32))
+    r = sk.Collection(wl.OBJ8_SCHEMA, ly.ARENA, None, ly.ArenaSpec({sc.MAIN_TAG: 64}))
+    assert tr.copy_collection(r, src) == "plane-copy"
+    assert r.dump() == src.dump()
+
+
+def test_device_collection_guards_from_host_scope():
+    # mockdev semantics (memctx.py:386-395): device elements are not touchable from host code
+    c = sk.Collection.__new__(sk.Collection)
+    lay = ly.LayoutInstance.__new__(ly.LayoutInstance)
+    lay.info = mc.ContextInfo.cuda(0)
+    lay.capabilities = ly.LayoutInstance._build_capabilities(lay)
+    assert lay.capabilities.flags("host") == ly.AccessFlags()
+    assert lay.capabilities.flags("cuda").resizable
+
+
+def test_shard_ranges_cover_exactly():
+    for n in (0, 1, 7, 1000, 10**9):
+        for world in (1, 2, 3, 8):
+            spans = [shard.shard_range(n, r, world) for r in range(world)]
+            assert spans[0][0] == 0 and spans[-1][1] == n
+            assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
+            assert max(h - l for l, h in spans) - min(h - l for l, h in spans) <= 1
+    assert shard.exclusive_offsets([3, 0, 5, 2]) == [0, 3, 3, 8]
+
+
+# ---- the C-ABI library ---------------------------------------------------------------------
+
+def _header_functions():
+    text = open(os.path.join(ROOT, "include", "soakit_b200.h")).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(sk_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_library_exports_every_header_symbol():
+    lib = ctypes.CDLL(nat.LIB_PATH)
+    names = _header_functions()
+    assert len(names) >= 30
+    missing = [n for n in names if not hasattr(lib, n)]
+    assert not missing, missing
+    assert sorted(nat.exported_names()) == names  # the ctypes binding covers the header exactly
+
+
+def test_library_loads_and_reports_no_device_cleanly():
+    lib = nat.lib()
+    assert lib.sk_version() == 0x000100
+    n = ctypes.c_int(-1)
+    st = lib.sk_device_count(ctypes.byref(n))
+    assert st in (nat.SK_OK, nat.SK_ERR_NO_DEVICE, nat.SK_ERR_CUDA)
+    if st != nat.SK_OK:
+        assert n.value == 0 and lib.sk_last_error()
