@@ -26,7 +26,7 @@ namespace conv {
 
 constexpr int NT = 256;
 constexpr int MAX_WORDS = 256;     // word table -> AoS strides up to 1 KiB use word moves
-constexpr int TILE_TARGET = 16384; // bytes of the larger tile side
+constexpr int TILE_TARGET = 24576; // bytes of the larger tile side (sweep: profiles/r01_sweep.md)
 constexpr int MAX_STAGES = 4;
 
 enum { MODE_ELEM = 0, MODE_WORD_A2P = 1, MODE_WORD_P2A = 2 };
@@ -64,6 +64,7 @@ struct Plan {
   uint8_t* dst;
   int32_t smem_bar_off, smem_tab_off, smem_in_off, smem_out_off, smem_total;
   int32_t any_elem;
+  int32_t cache_hint;       // 0 none, 1 evict_first on loads and stores, 2 loads only
   FieldPlan f[SK_MAX_FIELDS];
   int32_t wtab[MAX_WORDS];  // (segment byte base << 4) | element size ; -1 = not a word-moved word
 };
@@ -204,17 +205,28 @@ __device__ __forceinline__ void coop_copy(uint8_t* dst, const uint8_t* src, int6
   }
 }
 
+__device__ __forceinline__ void g2s(const Plan& P, void* s, const void* g, uint32_t bytes, uint64_t* bar,
+                                    uint64_t pol) {
+  if (P.cache_hint) bulk_g2s(s, g, bytes, bar, pol);
+  else bulk_g2s_plain(s, g, bytes, bar);
+}
+
+__device__ __forceinline__ void s2g(const Plan& P, void* g, const void* s, uint32_t bytes, uint64_t pol) {
+  if (P.cache_hint == 1) bulk_s2g(g, s, bytes, pol);
+  else bulk_s2g_plain(g, s, bytes);
+}
+
 __device__ void issue_bulk_load(const Plan& P, int64_t t, uint8_t* in, uint64_t* bar, uint64_t pol) {
   const int64_t r0 = t * P.R;
   mbar_expect_tx(bar, static_cast<uint32_t>(P.in_tile_bytes));
   if (P.src_kind == SK_KIND_PLANES) {
     for (int i = 0; i < P.nfields; ++i) {
       const FieldPlan& F = P.f[i];
-      bulk_g2s(in + F.sloc, F.splane + r0 * F.sisz, static_cast<uint32_t>(P.R * F.sisz), bar, pol);
+      g2s(P, in + F.sloc, F.splane + r0 * F.sisz, static_cast<uint32_t>(P.R * F.sisz), bar, pol);
     }
   } else {
     const int64_t off = P.src_kind == SK_KIND_AOS ? r0 * P.src_stride : (r0 >> P.src_lshift) * P.src_stride;
-    bulk_g2s(in, P.src + off, static_cast<uint32_t>(P.in_tile_bytes), bar, pol);
+    g2s(P, in, P.src + off, static_cast<uint32_t>(P.in_tile_bytes), bar, pol);
   }
 }
 
@@ -236,13 +248,13 @@ __device__ void issue_bulk_store(const Plan& P, int64_t t, const uint8_t* out, u
   if (P.dst_kind == SK_KIND_PLANES) {
     for (int i = 0; i < P.nfields; ++i) {
       const FieldPlan& F = P.f[i];
-      bulk_s2g(F.dplane + r0 * F.disz, out + F.dloc, static_cast<uint32_t>(P.R * F.disz), pol);
+      s2g(P, F.dplane + r0 * F.disz, out + F.dloc, static_cast<uint32_t>(P.R * F.disz), pol);
     }
   } else {
     const int64_t off = P.dst_kind == SK_KIND_AOS ? r0 * P.dst_stride : (r0 >> P.dst_lshift) * P.dst_stride;
-    bulk_s2g(P.dst + off, out, static_cast<uint32_t>(P.out_tile_bytes), pol);
+    s2g(P, P.dst + off, out, static_cast<uint32_t>(P.out_tile_bytes), pol);
   }
-  if (P.extra_plane) bulk_s2g(P.extra_plane + r0 * 4, out + P.extra_loc, static_cast<uint32_t>(P.R * 4), pol);
+  if (P.extra_plane) s2g(P, P.extra_plane + r0 * 4, out + P.extra_loc, static_cast<uint32_t>(P.R * 4), pol);
 }
 
 __device__ void coop_store(const Plan& P, int64_t t, int rows, const uint8_t* out) {
@@ -275,7 +287,42 @@ __device__ __forceinline__ void transform(const Plan& P, const uint8_t* __restri
     int q = tid - r * wpr;
     const int dr = NT / wpr;
     const int dq = NT - dr * wpr;
-    if (P.mode == MODE_WORD_A2P) {
+    if (dq == 0) {
+      // NT is a multiple of the record's word count: every word this thread
+      // touches sits at the same record slot q, so the table entry is loop
+      // invariant and the loop is a pure, unrolled LDS->STS stream (4 loads in
+      // flight per thread).
+      const int e = wtab[q];
+      if (e >= 0) {
+        const int base = e >> 4, isz = e & 15;
+        if (P.mode == MODE_WORD_A2P) {
+          const uint32_t* in32 = reinterpret_cast<const uint32_t*>(in);
+          int w = tid;
+          for (; w + 3 * NT < total; w += 4 * NT, r += 4 * dr) {
+            const uint32_t v0 = in32[w], v1 = in32[w + NT], v2 = in32[w + 2 * NT], v3 = in32[w + 3 * NT];
+            *reinterpret_cast<uint32_t*>(out + base + r * isz) = v0;
+            *reinterpret_cast<uint32_t*>(out + base + (r + dr) * isz) = v1;
+            *reinterpret_cast<uint32_t*>(out + base + (r + 2 * dr) * isz) = v2;
+            *reinterpret_cast<uint32_t*>(out + base + (r + 3 * dr) * isz) = v3;
+          }
+          for (; w < total; w += NT, r += dr) *reinterpret_cast<uint32_t*>(out + base + r * isz) = in32[w];
+        } else {
+          uint32_t* out32 = reinterpret_cast<uint32_t*>(out);
+          int w = tid;
+          for (; w + 3 * NT < total; w += 4 * NT, r += 4 * dr) {
+            const uint32_t v0 = *reinterpret_cast<const uint32_t*>(in + base + r * isz);
+            const uint32_t v1 = *reinterpret_cast<const uint32_t*>(in + base + (r + dr) * isz);
+            const uint32_t v2 = *reinterpret_cast<const uint32_t*>(in + base + (r + 2 * dr) * isz);
+            const uint32_t v3 = *reinterpret_cast<const uint32_t*>(in + base + (r + 3 * dr) * isz);
+            out32[w] = v0;
+            out32[w + NT] = v1;
+            out32[w + 2 * NT] = v2;
+            out32[w + 3 * NT] = v3;
+          }
+          for (; w < total; w += NT, r += dr) out32[w] = *reinterpret_cast<const uint32_t*>(in + base + r * isz);
+        }
+      }
+    } else if (P.mode == MODE_WORD_A2P) {
       const uint32_t* in32 = reinterpret_cast<const uint32_t*>(in);
       for (int w = tid; w < total; w += NT) {
         const int e = wtab[q];
@@ -301,6 +348,7 @@ __device__ __forceinline__ void transform(const Plan& P, const uint8_t* __restri
     const FieldPlan& F = P.f[i];
     if (F.wordable) continue;
     const int st = F.st, dt = F.dt, sisz = F.sisz, disz = F.disz;
+#pragma unroll 4
     for (int r = tid; r < rows; r += NT) {
       const uint32_t sa = rec_addr(P.src_kind, F.sloc, sisz, P.src_stride, P.src_lshift, r);
       const uint32_t da = rec_addr(P.dst_kind, F.dloc, disz, P.dst_stride, P.dst_lshift, r);
@@ -319,12 +367,9 @@ __device__ __forceinline__ void sensor_epilogue(const Plan& P, uint8_t* out, int
     const float na = *reinterpret_cast<const float*>(out + P.epi_seg[5] + r * 4);
     const float nb = *reinterpret_cast<const float*>(out + P.epi_seg[6] + r * 4);
     const uint8_t noisy = out[P.epi_seg[2] + r];
-    const float e = __fadd_rn(__fmul_rn(a, __ull2float_rn(c)), b);
-    const float m = (e >= 0.0f || e != e) ? e : 0.0f;  // np.maximum propagates NaN
-    float nz = __fadd_rn(__fmul_rn(na, __fsqrt_rn(m)), nb);
-    if (noisy) nz = __fmul_rn(nz, 2.0f);
+    const float e = sensor_energy(c, a, b);
     *reinterpret_cast<float*>(out + P.epi_seg[1] + r * 4) = e;
-    *reinterpret_cast<float*>(out + P.extra_loc + r * 4) = nz;
+    *reinterpret_cast<float*>(out + P.extra_loc + r * 4) = sensor_noise(e, na, nb, noisy != 0);
   }
 }
 
@@ -506,6 +551,32 @@ int validate(const sk_conv_desc& d, int64_t* granule, int64_t* in_rec_x1000, int
 
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
+// Tiling knobs; defaults are the measured best on B200 (profiles/), the
+// environment overrides exist for sweeps (SK_TILE_BYTES, SK_STAGES, SK_CTAS,
+// SK_CACHE_HINT).
+struct Tunables {
+  int tile_bytes = TILE_TARGET;
+  int max_stages = MAX_STAGES;
+  int ctas_per_sm = 4;
+  int cache_hint = 1;
+};
+
+static int env_int(const char* name, int dflt, int lo, int hi) {
+  const char* v = getenv(name);
+  if (!v || !*v) return dflt;
+  const int x = atoi(v);
+  return x < lo ? lo : (x > hi ? hi : x);
+}
+
+static Tunables tunables() {
+  Tunables t;
+  t.tile_bytes = env_int("SK_TILE_BYTES", t.tile_bytes, 1024, 65536);
+  t.max_stages = env_int("SK_STAGES", t.max_stages, 1, 8);
+  t.ctas_per_sm = env_int("SK_CTAS", t.ctas_per_sm, 1, 8);
+  t.cache_hint = env_int("SK_CACHE_HINT", t.cache_hint, 0, 2);
+  return t;
+}
+
 // Build the kernel plan. `in_bulk_ok`/`out_bulk_ok` veto bulk copies (peer or
 // host pointers); alignment is checked here.
 int make_plan(const sk_conv_desc& d, const DeviceState& ds, bool in_bulk_ok, bool out_bulk_ok, int epi, Plan* out,
@@ -528,9 +599,11 @@ int make_plan(const sk_conv_desc& d, const DeviceState& ds, bool in_bulk_ok, boo
   P.epi = epi;
   if (epi == EPI_SENSOR) out_rec += 4000;
 
-  // records per tile: multiple of the granule, larger side ~TILE_TARGET bytes
+  // records per tile: multiple of the granule, larger side ~tile_bytes
+  const Tunables tun = tunables();
+  P.cache_hint = tun.cache_hint;
   const int64_t rec = std::max<int64_t>(std::max(in_rec, out_rec), 1000);
-  int64_t R = (static_cast<int64_t>(TILE_TARGET) * 1000 / rec) / g * g;
+  int64_t R = (static_cast<int64_t>(tun.tile_bytes) * 1000 / rec) / g * g;
   R = std::max<int64_t>(R, g);
   R = std::min<int64_t>(R, std::max<int64_t>(g, 4096));
   P.R = static_cast<int32_t>(R);
@@ -652,16 +725,20 @@ int make_plan(const sk_conv_desc& d, const DeviceState& ds, bool in_bulk_ok, boo
   P.in_stage_stride = align_up(in_span + 16, 128);
   P.out_stage_stride = align_up(P.out_tile_bytes + 16, 128);
 
-  // shared memory budget: aim for two CTAs per SM
+  // shared memory budget: `ctas` CTAs per SM (228 KB per SM, 1 KB reserved per CTA)
   const int32_t fixed = 128 /*barriers*/ + (P.mode != MODE_ELEM ? 4 * MAX_WORDS : 0);
-  const int32_t budget2 = (ds.max_smem_optin > 0 ? std::min(ds.max_smem_optin, 232448) : 232448) / 2 - 1024;
-  const int32_t budget1 = (ds.max_smem_optin > 0 ? ds.max_smem_optin : 232448) - 1024;
-  int stages = (budget2 - fixed - 2 * P.out_stage_stride) / std::max(P.in_stage_stride, 1);
-  if (stages < 2) stages = (budget1 - fixed - 2 * P.out_stage_stride) / std::max(P.in_stage_stride, 1);
+  const int32_t optin = ds.max_smem_optin > 0 ? ds.max_smem_optin : 232448;
+  int ctas = tun.ctas_per_sm;
+  int stages = 0;
+  for (; ctas >= 1; --ctas) {
+    const int32_t budget = std::min(optin, 233472 / ctas - 1024);
+    stages = (budget - fixed - 2 * P.out_stage_stride) / std::max(P.in_stage_stride, 1);
+    if (stages >= 2 || ctas == 1) break;
+  }
   if (stages < 1)
     return set_error(SK_ERR_UNSUPPORTED, "records too large for the shared-memory tile (%lld B)",
                      (long long)rec / 1000);
-  P.stages = std::min(stages, MAX_STAGES);
+  P.stages = std::min(stages, tun.max_stages);
   P.smem_bar_off = 0;
   P.smem_tab_off = 128;
   P.smem_in_off = align_up(fixed, 128);
@@ -674,7 +751,7 @@ int make_plan(const sk_conv_desc& d, const DeviceState& ds, bool in_bulk_ok, boo
       per_sm < 1)
     per_sm = 1;
   cudaGetLastError();
-  const int64_t want = static_cast<int64_t>(ds.sm_count) * per_sm;
+  const int64_t want = static_cast<int64_t>(ds.sm_count) * std::min(per_sm, std::max(ctas, 1));
   *grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, P.ntiles)));
   return SK_OK;
 }

@@ -48,6 +48,59 @@ inline int dtype_size(int t) {
   }
 }
 
+// ---- numpy-on-x86 float32 arithmetic ----------------------------------------------
+// The reference computes the case study with numpy on x86 (SSE/AVX). IEEE fixes
+// every finite and infinite result, but not NaN bits: x86 returns the first
+// NaN operand (quieted) and the "real indefinite" 0xFFC00000 for invalid
+// operations, where the GPU returns 0x7FFFFFFF. These wrappers restore the x86
+// rule so outputs are bit-exact, NaN payloads included. The _rn intrinsics
+// also keep ptxas from contracting a*b+c into an FMA.
+
+__device__ __forceinline__ float x86_quiet(float x) { return __uint_as_float(__float_as_uint(x) | 0x00400000u); }
+
+__device__ __forceinline__ float x86_nan_result(float a, float b) {
+  if (a != a) return x86_quiet(a);
+  if (b != b) return x86_quiet(b);
+  return __uint_as_float(0xffc00000u);
+}
+
+__device__ __forceinline__ float x86_mul(float a, float b) {
+  const float r = __fmul_rn(a, b);
+  return r == r ? r : x86_nan_result(a, b);
+}
+
+__device__ __forceinline__ float x86_add(float a, float b) {
+  const float r = __fadd_rn(a, b);
+  return r == r ? r : x86_nan_result(a, b);
+}
+
+__device__ __forceinline__ float x86_sqrt(float m) {
+  if (m != m) return x86_quiet(m);
+  const float r = __fsqrt_rn(m);
+  return r == r ? r : __uint_as_float(0xffc00000u);
+}
+
+// np.maximum(e, 0.0f) as numpy's vectorised loop computes it: NaN propagates
+// unchanged, and for two zeros vmaxps returns its second operand (+0.0).
+// Integer tests on purpose: a float select is rewritten by ptxas into
+// FMNMX.NAN, which returns the canonical NaN instead of the input bits.
+__device__ __forceinline__ float np_max0(float e) {
+  const uint32_t u = __float_as_uint(e);
+  if ((u & 0x7fffffffu) > 0x7f800000u) return e;           // NaN, bits unchanged
+  return ((u & 0x80000000u) || u == 0u) ? 0.0f : e;        // negatives and +-0 -> +0
+}
+
+// energy = A * f32(counts) + B ; noise = nA * sqrt(max(E, 0)) + nB, x2 if noisy
+// (detector/schemas.py:29-41)
+__device__ __forceinline__ float sensor_energy(uint64_t counts, float a, float b) {
+  return x86_add(x86_mul(a, __ull2float_rn(counts)), b);
+}
+
+__device__ __forceinline__ float sensor_noise(float e, float na, float nb, bool noisy) {
+  const float n = x86_add(x86_mul(na, x86_sqrt(np_max0(e))), nb);
+  return noisy ? x86_mul(n, 2.0f) : n;
+}
+
 // ---- PTX wrappers -------------------------------------------------------------
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -89,6 +142,19 @@ __device__ __forceinline__ void bulk_g2s(void* smem_dst, const void* gsrc, uint3
           smem_u32(smem_dst)),
       "l"(gsrc), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
       : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s_plain(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(smem_dst)),
+               "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void bulk_s2g_plain(void* gdst, const void* smem_src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_u32(smem_src)),
+               "r"(bytes)
+               : "memory");
 }
 
 // shared -> global bulk copy, tracked by the issuing thread's bulk groups.

@@ -16,14 +16,10 @@ namespace sensor {
 constexpr int NT = 256;
 constexpr int VEC = 4;
 
-__device__ __forceinline__ float calib(uint64_t c, float a, float b) {
-  return __fadd_rn(__fmul_rn(a, __ull2float_rn(c)), b);
-}
+__device__ __forceinline__ float calib(uint64_t c, float a, float b) { return sensor_energy(c, a, b); }
 
 __device__ __forceinline__ float noise_of(float e, float na, float nb, bool noisy) {
-  const float m = (e >= 0.0f || e != e) ? e : 0.0f;  // np.maximum(e, 0) propagates NaN
-  float nz = __fadd_rn(__fmul_rn(na, __fsqrt_rn(m)), nb);
-  return noisy ? __fmul_rn(nz, 2.0f) : nz;
+  return sensor_noise(e, na, nb, noisy);
 }
 
 __global__ void __launch_bounds__(NT) calibrate_kernel(int64_t n, const uint64_t* __restrict__ counts,

@@ -97,7 +97,7 @@ def test_special_values_vs_oracle():
     recs["counts"] = rng.integers(0, np.iinfo(np.uint64).max, n, dtype=np.uint64, endpoint=True)
     cal = recs["calibration_data"]
     for k in ("parameter_A", "parameter_B", "noise_A", "noise_B"):
-        cal[k] = (rng.standard_normal(n) * 10 ** rng.integers(-40, 30, n)).astype(np.float32)
+        cal[k] = (rng.standard_normal(n) * 10.0 ** rng.integers(-40, 30, n)).astype(np.float32)
     cal["parameter_A"][:16] = [np.nan, np.inf, -np.inf, 0.0, -0.0, 1e-45, -1e-45, 3e38] * 2
     cal["noisy"] = rng.integers(0, 2, n).astype(bool)
     src = aos_collection(sensor.SENSOR_SCHEMA, recs, n, HOST)
