@@ -34,7 +34,9 @@ enum { EPI_NONE = 0, EPI_SENSOR = 1 };
 
 struct FieldPlan {
   uint8_t st, dt, sisz, disz;
-  uint8_t wordable, pad0, pad1, pad2;
+  uint8_t wordable;
+  uint8_t op;        // element-path specialisation (ELEM_*), chosen on the host
+  uint8_t sal, dal;  // source / destination element always naturally aligned in smem
   int32_t sloc;  // AOS: offset in record; PLANES: smem segment offset; AOSOA: block offset in tile
   int32_t dloc;
   const uint8_t* splane;
@@ -48,6 +50,10 @@ struct Plan {
   int32_t src_kind, dst_kind;
   int32_t src_stride, dst_stride;  // AOS record bytes / AOSOA tile bytes
   int32_t src_lshift, dst_lshift;  // log2(lanes) for AOSOA
+  // smem element address of record r of a field, branch-free for every kind:
+  //   ((r >> lshift) * A) + ((r & msk) * itemsize) + loc
+  //   AOS: A = stride, msk = 0;  PLANES: A = 0, msk = ~0;  AOSOA: A = tile, msk = T-1
+  int32_t src_A, dst_A, src_msk, dst_msk;
   int32_t in_tile_bytes, out_tile_bytes;
   int32_t in_stage_stride, out_stage_stride;
   int32_t stages;
@@ -272,6 +278,90 @@ __device__ void coop_store(const Plan& P, int64_t t, int rows, const uint8_t* ou
 }
 
 // ---------------------------------------------------------------------------------
+// element path: one specialised loop per (size, alignment, cast) class; the
+// class is chosen on the host (FieldPlan::op/sal/dal) and dispatched once per
+// field, so the per-element body is a handful of instructions.
+
+enum { ELEM_GENERIC = 0, ELEM_MOVE = 1, ELEM_F64_F32 = 2, ELEM_F32_F64 = 3 };
+
+template <int SZ>
+__device__ __forceinline__ uint64_t lds_al(const uint8_t* p) {
+  if (SZ == 1) return *p;
+  if (SZ == 2) return *reinterpret_cast<const uint16_t*>(p);
+  if (SZ == 4) return *reinterpret_cast<const uint32_t*>(p);
+  return *reinterpret_cast<const uint64_t*>(p);
+}
+
+template <int SZ>
+__device__ __forceinline__ void sts_al(uint8_t* p, uint64_t v) {
+  if (SZ == 1) *p = static_cast<uint8_t>(v);
+  else if (SZ == 2) *reinterpret_cast<uint16_t*>(p) = static_cast<uint16_t>(v);
+  else if (SZ == 4) *reinterpret_cast<uint32_t*>(p) = static_cast<uint32_t>(v);
+  else *reinterpret_cast<uint64_t*>(p) = v;
+}
+
+template <int CV>
+__device__ __forceinline__ uint64_t convert_op(uint64_t v) {
+  if (CV == ELEM_F64_F32) return cast_bits(v, SK_F64, SK_F32);
+  if (CV == ELEM_F32_F64) return cast_bits(v, SK_F32, SK_F64);
+  return v;
+}
+
+template <int SI, int DI, int CV, bool SAL, bool DAL>
+__device__ __forceinline__ void elem_loop(const Plan& P, const FieldPlan& F, const uint8_t* __restrict__ in,
+                                          uint8_t* __restrict__ out, int rows) {
+  const int sl = P.src_lshift, dl = P.dst_lshift, sA = P.src_A, dA = P.dst_A, sm = P.src_msk, dm = P.dst_msk;
+  const int sloc = F.sloc, dloc = F.dloc;
+#pragma unroll 4
+  for (int r = threadIdx.x; r < rows; r += NT) {
+    const uint32_t sa = static_cast<uint32_t>((r >> sl) * sA + (r & sm) * SI + sloc);
+    const uint32_t da = static_cast<uint32_t>((r >> dl) * dA + (r & dm) * DI + dloc);
+    const uint64_t v = convert_op<CV>(SAL ? lds_al<SI>(in + sa) : lds_any(in + sa, SI));
+    if (DAL) sts_al<DI>(out + da, v);
+    else sts_any(out + da, v, DI);
+  }
+}
+
+template <int SI, int DI, int CV>
+__device__ __forceinline__ void elem_aligned(const Plan& P, const FieldPlan& F, const uint8_t* in, uint8_t* out,
+                                             int rows) {
+  if (F.sal) {
+    if (F.dal) elem_loop<SI, DI, CV, true, true>(P, F, in, out, rows);
+    else elem_loop<SI, DI, CV, true, false>(P, F, in, out, rows);
+  } else {
+    if (F.dal) elem_loop<SI, DI, CV, false, true>(P, F, in, out, rows);
+    else elem_loop<SI, DI, CV, false, false>(P, F, in, out, rows);
+  }
+}
+
+__device__ __noinline__ void elem_generic(const Plan& P, const FieldPlan& F, const uint8_t* in, uint8_t* out,
+                                          int rows) {
+  const int st = F.st, dt = F.dt, sisz = F.sisz, disz = F.disz;
+  for (int r = threadIdx.x; r < rows; r += NT) {
+    const uint32_t sa = static_cast<uint32_t>((r >> P.src_lshift) * P.src_A + (r & P.src_msk) * sisz + F.sloc);
+    const uint32_t da = static_cast<uint32_t>((r >> P.dst_lshift) * P.dst_A + (r & P.dst_msk) * disz + F.dloc);
+    sts_any(out + da, cast_bits(lds_any(in + sa, sisz), st, dt), disz);
+  }
+}
+
+__device__ __forceinline__ void elem_field(const Plan& P, const FieldPlan& F, const uint8_t* in, uint8_t* out,
+                                           int rows) {
+  switch (F.op) {
+    case ELEM_MOVE:
+      switch (F.sisz) {
+        case 1: elem_aligned<1, 1, ELEM_MOVE>(P, F, in, out, rows); break;
+        case 2: elem_aligned<2, 2, ELEM_MOVE>(P, F, in, out, rows); break;
+        case 4: elem_aligned<4, 4, ELEM_MOVE>(P, F, in, out, rows); break;
+        default: elem_aligned<8, 8, ELEM_MOVE>(P, F, in, out, rows); break;
+      }
+      break;
+    case ELEM_F64_F32: elem_aligned<8, 4, ELEM_F64_F32>(P, F, in, out, rows); break;
+    case ELEM_F32_F64: elem_aligned<4, 8, ELEM_F32_F64>(P, F, in, out, rows); break;
+    default: elem_generic(P, F, in, out, rows); break;
+  }
+}
+
+// ---------------------------------------------------------------------------------
 // in-smem transposition
 
 __device__ __forceinline__ void transform(const Plan& P, const uint8_t* __restrict__ in, uint8_t* __restrict__ out,
@@ -346,15 +436,7 @@ __device__ __forceinline__ void transform(const Plan& P, const uint8_t* __restri
   // element moves: one field at a time (uniform), lane -> record
   for (int i = 0; i < P.nfields; ++i) {
     const FieldPlan& F = P.f[i];
-    if (F.wordable) continue;
-    const int st = F.st, dt = F.dt, sisz = F.sisz, disz = F.disz;
-#pragma unroll 4
-    for (int r = tid; r < rows; r += NT) {
-      const uint32_t sa = rec_addr(P.src_kind, F.sloc, sisz, P.src_stride, P.src_lshift, r);
-      const uint32_t da = rec_addr(P.dst_kind, F.dloc, disz, P.dst_stride, P.dst_lshift, r);
-      const uint64_t v = cast_bits(lds_any(in + sa, sisz), st, dt);
-      sts_any(out + da, v, disz);
-    }
+    if (!F.wordable) elem_field(P, F, in, out, rows);
   }
 }
 
@@ -655,6 +737,27 @@ int make_plan(const sk_conv_desc& d, const DeviceState& ds, bool in_bulk_ok, boo
     out_bytes = P.extra_loc + static_cast<int32_t>(R) * 4;
   }
   P.out_tile_bytes = align_up(out_bytes, 16);
+
+  // branch-free element addressing + per-field element-path class
+  auto side_geo = [](int kind, int64_t stride, int32_t* A, int32_t* msk, int lanes) {
+    if (kind == SK_KIND_AOS) { *A = static_cast<int32_t>(stride); *msk = 0; }
+    else if (kind == SK_KIND_PLANES) { *A = 0; *msk = -1; }
+    else { *A = static_cast<int32_t>(stride); *msk = lanes - 1; }
+  };
+  side_geo(d.src_kind, d.src_stride, &P.src_A, &P.src_msk, d.src_lanes);
+  side_geo(d.dst_kind, d.dst_stride, &P.dst_A, &P.dst_msk, d.dst_lanes);
+  auto always_aligned = [](int kind, int64_t stride, int32_t loc, int isz) {
+    if (kind == SK_KIND_PLANES) return true;  // segments are 16-byte aligned
+    return stride % isz == 0 && loc % isz == 0;
+  };
+  for (int i = 0; i < d.nfields; ++i) {
+    FieldPlan& F = P.f[i];
+    F.sal = always_aligned(d.src_kind, d.src_stride, F.sloc, F.sisz);
+    F.dal = always_aligned(d.dst_kind, d.dst_stride, F.dloc, F.disz);
+    F.op = F.st == F.dt ? ELEM_MOVE
+                        : (F.st == SK_F64 && F.dt == SK_F32) ? ELEM_F64_F32
+                        : (F.st == SK_F32 && F.dt == SK_F64) ? ELEM_F32_F64 : ELEM_GENERIC;
+  }
 
   // word moves
   P.mode = MODE_ELEM;
