@@ -130,9 +130,17 @@ def run_ours(args) -> None:
     import torch.distributed as dist
 
     rank, world, local = _dist()
+    # SK_BENCH_DEVICE / SK_BENCH_BACKEND exist only to exercise the multi-rank
+    # code path on a single GPU (all ranks on one device, gloo plumbing).
+    local = int(os.environ.get("SK_BENCH_DEVICE", local))
+    backend = os.environ.get("SK_BENCH_BACKEND", "nccl")
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        else:
+            dist.init_process_group(backend)
+    tdev = f"cuda:{local}" if backend == "nccl" else "cpu"
 
     import paper_2511_04853_b200 as sk
     from paper_2511_04853_b200 import _native as nat
@@ -151,19 +159,19 @@ def run_ours(args) -> None:
     def max_over_ranks(x: float) -> float:
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
+        t = torch.tensor([x], dtype=torch.float64, device=tdev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
     def sum_over_ranks(x: float) -> float:
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
+        t = torch.tensor([x], dtype=torch.float64, device=tdev)
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
         return float(t.item())
 
-    def device_collection(schema, kind, n):
-        c = sk.Collection(schema, kind, cuda)
+    def device_collection(schema, kind, n, ipc=False):
+        c = sk.Collection(schema, kind, mc.ContextInfo.cuda(dev, ipc=True) if ipc else cuda)
         with mc.execution_scope(mc.CUDA):
             c.reserve(n)
         with c.layout.engine_ops():
@@ -174,10 +182,11 @@ def run_ours(args) -> None:
     free_b, _ = torch.cuda.mem_get_info(dev)
     lo, hi = shard.shard_range(n_total, rank, world)
     n = hi - lo
-    if 2 * n * 32 > free_b * 0.9:
-        raise SystemExit(f"rank {rank}: shard of {n} objects needs {2 * n * 32 / 1e9:.1f} GB, {free_b / 1e9:.1f} GB free")
+    need = (3 if world > 1 else 2) * n * 32 * (world if os.environ.get("SK_BENCH_DEVICE") else 1)
+    if need > free_b * 0.9:
+        raise SystemExit(f"rank {rank}: shard of {n} objects needs {need / 1e9:.1f} GB, {free_b / 1e9:.1f} GB free")
 
-    aos = device_collection(wl.OBJ8_SCHEMA, ly.AOS, n)
+    aos = device_collection(wl.OBJ8_SCHEMA, ly.AOS, n, ipc=world > 1)  # exportable: the P2P leg pulls it
     soa = device_collection(wl.OBJ8_SCHEMA, ly.PER_FIELD, n)
     # the global 1e9-record image is splitmix64(seed, word); this shard is its slice
     wl.fill_random_device(aos.layout._struct_buf.ptr, n * 32, seed=20251104, device=dev, first_word=lo * 4)
@@ -250,6 +259,48 @@ def run_ours(args) -> None:
     host.free()
     dst.free()
 
+    # ---- layout-changing peer pull (config 5b): rank r converts the AoS shard
+    # owned by rank (r+1) % N into planes on its own GPU; the kernel reads the
+    # peer's HBM over NVLink (CUDA IPC mapping), writes local HBM.
+    p2p = None
+    if world > 1 and not args.no_p2p:
+        from paper_2511_04853_b200 import shard as sh
+
+        mine = sh.export_collection(aos)
+        every = [None] * world
+        dist.all_gather_object(every, mine)
+        src_rank = (rank + 1) % world
+        remote = sh.import_collection(wl.OBJ8_SCHEMA, every[src_rank], dev)
+        n_src = remote.size()
+        pulled = device_collection(wl.OBJ8_SCHEMA, ly.PER_FIELD, n_src)
+
+        def p2p_step():
+            tr.copy_collection(pulled, remote, {"async": True})
+
+        for _ in range(2):
+            p2p_step()
+        barrier()
+        a, b = nat.Event(), nat.Event()
+        a.record(dev)
+        for _ in range(args.steps):
+            p2p_step()
+        b.record(dev)
+        barrier()
+        p_ms = max_over_ranks(a.elapsed_ms(b) / args.steps)
+        p_total = sum_over_ranks(n_src)
+        per_gpu_link = max_over_ranks(n_src) * 32 / (p_ms / 1e3) / 1e9
+        p2p = {"value": round(p_total * BYTES_PER_OBJECT / (p_ms / 1e3) / 1e9, 2), "unit": UNIT,
+               "ms_per_step": round(p_ms, 3), "objects_total": int(p_total),
+               "nvlink_read_gbs_per_gpu": round(per_gpu_link, 1),
+               "nvlink_roofline_gbs": 770.0, "nvlink_frac": round(per_gpu_link / 770.0, 3),
+               "note": "GPU r pulls rank (r+1)%N's AoS shard through a CUDA IPC mapping (32 B/object over "
+                       "NVLink read, 32 B/object local HBM write); roofline = measured 770 GB/s peer copy "
+                       "(B200_PROFILING.md)"}
+        barrier()
+        remote.free()
+        pulled.free()
+        barrier()
+
     extra = {}
     cpu = None
     if rank == 0 and world == 1 and not args.no_extra:
@@ -303,6 +354,8 @@ def run_ours(args) -> None:
         "clocks": clk,
         "cpu_baseline": cpu,
     }
+    if p2p:
+        line["p2p"] = p2p
     if extra:
         line["configs"] = extra
     print(json.dumps(line), flush=True)
@@ -462,6 +515,7 @@ def main() -> None:
     ap.add_argument("--ref-objects", type=int, default=64_000_000)
     ap.add_argument("--no-extra", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-p2p", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3

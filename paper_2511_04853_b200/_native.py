@@ -198,6 +198,16 @@ def free(device: int, ptr: int) -> None:
     call("sk_free", device, ptr)
 
 
+def malloc_shareable(device: int, nbytes: int) -> int:
+    out = C.c_void_p(0)
+    call("sk_malloc_shareable", device, nbytes, C.byref(out))
+    return out.value or 0
+
+
+def free_shareable(device: int, ptr: int) -> None:
+    call("sk_free_shareable", device, ptr)
+
+
 def host_alloc_pinned(nbytes: int) -> int:
     out = C.c_void_p(0)
     call("sk_host_alloc_pinned", nbytes, C.byref(out))

@@ -59,6 +59,52 @@ def rebase_prefix(prefix, offset: int):
     return prefix + offset
 
 
+# ---- whole collections across processes (layout-changing peer pulls) ----------------------
+
+def export_collection(coll) -> dict:
+    """Picklable description of a device collection allocated with
+    ContextInfo.cuda(dev, ipc=True): kind, sizes, capacities and one IPC
+    handle per buffer. The owner must keep the collection alive (and its sizes
+    unchanged) while importers use it."""
+    from . import memctx
+
+    if coll.info.context != memctx.CUDA or not coll.info.params.get("ipc", False):
+        raise ValueError("export needs a collection on ContextInfo.cuda(device, ipc=True)")
+    lay = coll.layout
+    bufs = [(ipc_handle(b.ptr) if b.ptr else b"", b.length_bytes) for b in lay.buffers()]
+    spec = None
+    if coll.kind == "arena":
+        spec = (dict(lay.arena_spec.capacities), lay.arena_spec.alignment)
+    return {"kind": coll.kind, "sizes": dict(lay._sizes), "caps": dict(lay._caps), "buffers": bufs,
+            "arena": spec, "owner_device": lay.device}
+
+
+def import_collection(schema, exported: dict, device: int):
+    """A collection on this process's `device` whose buffers are the exported
+    ones, mapped through CUDA IPC (context cuda_ipc). Layout-changing copies
+    out of it run on `device` and pull the bytes over NVLink (or locally when
+    both processes share the GPU). free() unmaps."""
+    from . import layouts as ly
+    from . import memctx
+    from .collection import Collection
+
+    arena = ly.ArenaSpec(exported["arena"][0], exported["arena"][1]) if exported["arena"] else None
+    coll = Collection(schema, exported["kind"], memctx.ContextInfo.cuda(device), arena)
+    lay = coll.layout
+    for b in lay.buffers():  # the zero-capacity placeholders
+        memctx.deallocate(b)
+    info = memctx.ContextInfo(memctx.CUDA_IPC, {"device_id": device})
+    ctx = memctx.get_context(memctx.CUDA_IPC)
+    adopted = [ctx.adopt(info, ipc_open(device, h) if h else 0, n) for h, n in exported["buffers"]]
+    lay._rebind_buffers(adopted)
+    lay.info = info
+    lay.capabilities = lay._build_capabilities()
+    lay._caps = dict(exported["caps"])
+    lay._sizes = dict(exported["sizes"])
+    coll._bump()
+    return coll
+
+
 # ---- IPC handles for cross-process peer pulls -----------------------------------------
 
 def ipc_handle(dev_ptr: int) -> bytes:

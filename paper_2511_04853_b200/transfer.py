@@ -114,7 +114,7 @@ def move_collection(dst: Collection, src: Collection, opts: Mapping[str, Any] | 
 
 # ---- shared helpers -----------------------------------------------------------------------------
 
-_ENGINE_CONTEXTS = (memctx.HOST, memctx.PINNED, memctx.CUDA)
+_ENGINE_CONTEXTS = (memctx.HOST, memctx.PINNED, memctx.CUDA, memctx.CUDA_IPC)
 
 
 def _engine_device(dst: Collection, src: Collection) -> int:
