@@ -175,6 +175,19 @@ int sk_sensor_convert_calibrate(const sk_conv_desc* desc, int f_counts,
                                 int f_na, int f_nb, float* noise, int device,
                                 uintptr_t stream);
 
+/* Deterministic sensor events on the device (detector/events.py:85-133):
+   nevents events of w*h cells, event e drawn from the splitmix64 stream of
+   seeds[e] (host array). Per cell: type = draw0 & 3, counts = draw1 & 15,
+   noisy = draw2 % 50 == 0, calibration parameters by type from draws 0..15;
+   then n_dep deposits per event add int(amp * footprint[dy][dx]) to a 5x5
+   window (footprint25 = the reference's exp(-(dx^2+dy^2)/2.88) table, row
+   major, passed from the host so every bit matches the reference's libm).
+   Writes per_field planes of nevents*w*h records; energy is zeroed. */
+int sk_sensor_generate(int64_t w, int64_t h, const uint64_t* seeds, int nevents,
+                       int64_t n_dep, const double* footprint25, uint8_t* type,
+                       uint64_t* counts, uint8_t* noisy, float* a, float* b, float* na,
+                       float* nb, float* energy, uintptr_t stream);
+
 /* ---- synthetic inputs ------------------------------------------------------- */
 /* Fill nbytes of device memory with splitmix64(seed, first_word + word index)
    bits (counter-based, so a shard starting at 8-byte word `first_word` of the

@@ -14,6 +14,7 @@ inside the reference's execution_scope(mockdev) (memctx.py:369-395).
 from __future__ import annotations
 
 import ctypes as C
+import math
 
 import numpy as np
 
@@ -103,6 +104,37 @@ def transfer_calibrate(dst, src, noise: DeviceArray | None = None, sync: bool = 
     if sync:
         nat.sync(dev)
     return noise
+
+
+def footprint() -> list[float]:
+    """The reference's 5x5 deposit footprint, evaluated with the same libm
+    (events.py:31-33), row-major."""
+    return [math.exp(-(dx * dx + dy * dy) / 2.88) for dy in range(-2, 3) for dx in range(-2, 3)]
+
+
+def generate_events(coll, width: int, height: int, seeds, density: float = 0.0, sync: bool = True) -> None:
+    """Fill a device-resident Sensor collection with len(seeds) events of
+    width x height cells generated on the GPU, event-major, energy zeroed:
+    byte-identical to generate_event + fill_sensor_collection
+    (detector/events.py:85-133, detector/reconstruct.py:142-154) per event."""
+    dev, p = _device_planes(coll)
+    seeds = [int(s) for s in seeds]
+    n = width * height
+    total = n * len(seeds)
+    lay = coll.layout
+    with lay.engine_ops():
+        lay.reserve(sc.MAIN_TAG, total)
+        lay._set_sizes_for_engine({sc.MAIN_TAG: total})
+    dev, p = _device_planes(coll)  # reserve may have reallocated the planes
+    n_dep = int(round(density * n))
+    c_seeds = (C.c_uint64 * max(len(seeds), 1))(*seeds)
+    foot = (C.c_double * 25)(*footprint())
+    ptype = lay.plane_address(coll.plan.leaf("type"), 0)
+    nat.call("sk_sensor_generate", width, height, c_seeds, len(seeds), n_dep, foot, ptype, p[_COUNTS], p[_NOISY],
+             p[_A], p[_B], p[_NA], p[_NB], p[_ENERGY], nat.stream(dev))
+    coll._bump()
+    if sync:
+        nat.sync(dev)
 
 
 def _calibrate_behavior(coll) -> None:

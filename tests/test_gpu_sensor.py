@@ -110,6 +110,38 @@ def test_special_values_vs_oracle():
     assert noise.tobytes() == nz.tobytes()
 
 
+COLS = {"type": "type", "counts": "counts", "noisy": "calibration_data.noisy",
+        "parameter_A": "calibration_data.parameter_A", "parameter_B": "calibration_data.parameter_B",
+        "noise_A": "calibration_data.noise_A", "noise_B": "calibration_data.noise_B"}
+
+
+@pytest.mark.parametrize("name", EVENTS)
+def test_device_event_generation_matches_reference(name):
+    """On-device splitmix64 events == the reference's generate_event columns."""
+    g = golden(name)
+    w, h = int(g["w"]), int(g["h"])
+    dev = sk.Collection(sensor.SENSOR_SCHEMA, ly.PER_FIELD, CUDA)
+    sensor.generate_events(dev, w, h, [int(g["seed"])], float(g["density"]))
+    planes = to_host_planes(dev)
+    for ev_key, leaf in COLS.items():
+        want = np.ascontiguousarray(g[f"ev:{ev_key}"])
+        if want.dtype == np.bool_:
+            want = want.view(np.uint8)
+        assert planes[f"{leaf}#0"] == want.tobytes(), ev_key
+    assert planes["energy#0"] == bytes(4 * w * h)
+
+
+def test_batched_device_events_vs_oracle():
+    seeds = [0, 1, 0xDEADBEEF, (1 << 64) - 1]
+    dev = sk.Collection(sensor.SENSOR_SCHEMA, ly.PER_FIELD, CUDA)
+    sensor.generate_events(dev, 436, 436, seeds, 0.002)
+    planes = to_host_planes(dev)
+    evs = [R.generate_event(436, 436, s, 0.002) for s in seeds]
+    for ev_key, leaf in COLS.items():
+        want = np.concatenate([ev[ev_key] for ev in evs])
+        assert planes[f"{leaf}#0"] == want.view(np.uint8).tobytes(), ev_key
+
+
 def test_host_resident_collection_is_refused():
     host = sk.Collection(sensor.SENSOR_SCHEMA, ly.PER_FIELD, HOST)
     with pytest.raises(sk.AccessError):
