@@ -163,6 +163,9 @@ def run_ours(args) -> None:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    def min_over_ranks(x: float) -> float:
+        return -max_over_ranks(-x)
+
     def sum_over_ranks(x: float) -> float:
         if world == 1:
             return x
@@ -256,6 +259,16 @@ def run_ours(args) -> None:
     e2e_ms = max_over_ranks(e0.elapsed_ms(e1) / e2e_steps)
     m_total = sum_over_ranks(m)
     e2e_value = m_total * BYTES_PER_OBJECT / (e2e_ms / 1e3) / 1e9
+    # the link the e2e leg is bound by: pinned host -> HBM copy of the same bytes
+    l0, l1 = nat.Event(), nat.Event()
+    nat.memcpy(aos.layout._struct_buf.ptr, host.layout._struct_buf.ptr, m * 32, dev)
+    barrier()
+    l0.record(dev)
+    for _ in range(3):
+        nat.memcpy(aos.layout._struct_buf.ptr, host.layout._struct_buf.ptr, m * 32, dev)
+    l1.record(dev)
+    barrier()
+    h2d_gbs = min_over_ranks(m * 32 * 3 / (l0.elapsed_ms(l1) / 1e3) / 1e9)
     host.free()
     dst.free()
 
@@ -348,6 +361,8 @@ def run_ours(args) -> None:
                                     "fallback 6650 GB/s (B200_PROFILING.md)"},
         "e2e": {"value": round(e2e_value, 2), "unit": UNIT, "h2d_bytes_per_step": m * 32 * world,
                 "d2h_bytes_per_step": 32 * world, "ms_per_step": round(e2e_ms, 3),
+                "h2d_link_gbs_measured": round(h2d_gbs, 1),
+                "frac_of_h2d_link": round(m * 32 * world / (e2e_ms / 1e3) / 1e9 / (h2d_gbs * world), 3),
                 "sample": f"{m} objects per rank in pinned host memory -> device per_field via copy_collection "
                           "(chunked H2D | convert | on 3 streams), then D2H of the last converted record"},
         "gpu_launches": args.steps,

@@ -17,6 +17,7 @@
 // destination byte written once, all through 16-byte-aligned bulk transfers.
 #include <algorithm>
 #include <cstring>
+#include <mutex>
 #include <vector>
 
 #include "sk_internal.cuh"
@@ -633,6 +634,30 @@ int validate(const sk_conv_desc& d, int64_t* granule, int64_t* in_rec_x1000, int
 
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
+// Opt-in shared memory and resident CTAs per SM for a dynamic smem size,
+// cached per device (these runtime queries cost microseconds per call, which
+// matters for small conversions).
+static int occupancy_for(int smem) {
+  static std::mutex mu;
+  static int max_set[64] = {0};
+  static std::vector<std::pair<int, int>> cache[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  for (const auto& e : cache[dev])
+    if (e.first == smem) return e.second;
+  if (smem > max_set[dev]) {
+    cudaFuncSetAttribute(convert_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    max_set[dev] = smem;
+  }
+  int per_sm = 1;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, convert_kernel, NT, smem) != cudaSuccess || per_sm < 1)
+    per_sm = 1;
+  cudaGetLastError();
+  if (cache[dev].size() < 256) cache[dev].push_back({smem, per_sm});
+  return per_sm;
+}
+
 // Tiling knobs; defaults are the measured best on B200 (profiles/), the
 // environment overrides exist for sweeps (SK_TILE_BYTES, SK_STAGES, SK_CTAS,
 // SK_CACHE_HINT).
@@ -848,12 +873,7 @@ int make_plan(const sk_conv_desc& d, const DeviceState& ds, bool in_bulk_ok, boo
   P.smem_out_off = P.smem_in_off + P.stages * P.in_stage_stride;
   P.smem_total = P.smem_out_off + 2 * P.out_stage_stride;
 
-  int per_sm = 1;
-  cudaFuncSetAttribute(convert_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, P.smem_total);
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, convert_kernel, NT, P.smem_total) != cudaSuccess ||
-      per_sm < 1)
-    per_sm = 1;
-  cudaGetLastError();
+  const int per_sm = occupancy_for(P.smem_total);
   const int64_t want = static_cast<int64_t>(ds.sm_count) * std::min(per_sm, std::max(ctas, 1));
   *grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, P.ntiles)));
   return SK_OK;

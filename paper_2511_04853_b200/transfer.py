@@ -168,12 +168,29 @@ def _convert_applies(dst: Collection, src: Collection) -> bool:
     return _has_struct(src) != _has_struct(dst)
 
 
+_desc_cache: dict = {}
+
+
+def _cached_desc(dl, sl, n):
+    """Descriptors are pure functions of the two layouts' buffer addresses,
+    capacities and n: reuse them across repeated transfers (host overhead is
+    what bounds small conversions)."""
+    key = (n, tuple(b.ptr for b in sl.buffers()), tuple(b.ptr for b in dl.buffers()),
+           tuple(sl._caps.values()), tuple(dl._caps.values()), type(sl), type(dl), id(sl.plan))
+    desc = _desc_cache.get(key)
+    if desc is None:
+        if len(_desc_cache) > 256:
+            _desc_cache.clear()
+        desc = _desc_cache[key] = cv.plan_desc(dl, sl, n)
+    return desc
+
+
 def _convert_execute(dst: Collection, src: Collection, opts: Mapping[str, Any] | None = None) -> None:
     _match_sizes(dst, src)
     sl, dl = src.layout, dst.layout
     n = sl.size(MAIN_TAG)
     dev = _engine_device(dst, src)
-    desc = cv.plan_desc(dl, sl, n)
+    desc = _cached_desc(dl, sl, n)
     if desc is not None and n:
         cv.run(desc, dev)
     side = [lf for lf in sl.plan.leaves if not (lf.size_tag == MAIN_TAG and lf.role == ROLE_ELEMENT)]
