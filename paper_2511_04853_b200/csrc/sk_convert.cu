@@ -27,7 +27,7 @@ namespace conv {
 
 constexpr int NT = 256;
 constexpr int MAX_WORDS = 256;     // word table -> AoS strides up to 1 KiB use word moves
-constexpr int TILE_TARGET = 24576; // bytes of the larger tile side (sweep: profiles/r01_sweep.md)
+constexpr int TILE_TARGET = 49152; // in+out bytes per tile (sweep: profiles/r01_sweep.md)
 constexpr int MAX_STAGES = 4;
 
 enum { MODE_ELEM = 0, MODE_WORD_A2P = 1, MODE_WORD_P2A = 2 };
@@ -70,7 +70,9 @@ struct Plan {
   const uint8_t* src;
   uint8_t* dst;
   int32_t smem_bar_off, smem_tab_off, smem_in_off, smem_out_off, smem_total;
-  int32_t any_elem;
+  int32_t n_elem;           // fields moved by the element path, their indices, records split
+  int32_t elem_chunks;
+  uint8_t elem_idx[SK_MAX_FIELDS];
   int32_t cache_hint;       // 0 none, 1 evict_first on loads and stores, 2 loads only
   FieldPlan f[SK_MAX_FIELDS];
   int32_t wtab[MAX_WORDS];  // (segment byte base << 4) | element size ; -1 = not a word-moved word
@@ -308,13 +310,14 @@ __device__ __forceinline__ uint64_t convert_op(uint64_t v) {
   return v;
 }
 
+// One warp moves records [r0, r1) of one field: lane l takes r0 + l, r0 + l + 32, ...
 template <int SI, int DI, int CV, bool SAL, bool DAL>
 __device__ __forceinline__ void elem_loop(const Plan& P, const FieldPlan& F, const uint8_t* __restrict__ in,
-                                          uint8_t* __restrict__ out, int rows) {
+                                          uint8_t* __restrict__ out, int r0, int r1) {
   const int sl = P.src_lshift, dl = P.dst_lshift, sA = P.src_A, dA = P.dst_A, sm = P.src_msk, dm = P.dst_msk;
   const int sloc = F.sloc, dloc = F.dloc;
-#pragma unroll 4
-  for (int r = threadIdx.x; r < rows; r += NT) {
+#pragma unroll 8
+  for (int r = r0 + static_cast<int>(threadIdx.x & 31); r < r1; r += 32) {
     const uint32_t sa = static_cast<uint32_t>((r >> sl) * sA + (r & sm) * SI + sloc);
     const uint32_t da = static_cast<uint32_t>((r >> dl) * dA + (r & dm) * DI + dloc);
     const uint64_t v = convert_op<CV>(SAL ? lds_al<SI>(in + sa) : lds_any(in + sa, SI));
@@ -325,20 +328,20 @@ __device__ __forceinline__ void elem_loop(const Plan& P, const FieldPlan& F, con
 
 template <int SI, int DI, int CV>
 __device__ __forceinline__ void elem_aligned(const Plan& P, const FieldPlan& F, const uint8_t* in, uint8_t* out,
-                                             int rows) {
+                                             int r0, int r1) {
   if (F.sal) {
-    if (F.dal) elem_loop<SI, DI, CV, true, true>(P, F, in, out, rows);
-    else elem_loop<SI, DI, CV, true, false>(P, F, in, out, rows);
+    if (F.dal) elem_loop<SI, DI, CV, true, true>(P, F, in, out, r0, r1);
+    else elem_loop<SI, DI, CV, true, false>(P, F, in, out, r0, r1);
   } else {
-    if (F.dal) elem_loop<SI, DI, CV, false, true>(P, F, in, out, rows);
-    else elem_loop<SI, DI, CV, false, false>(P, F, in, out, rows);
+    if (F.dal) elem_loop<SI, DI, CV, false, true>(P, F, in, out, r0, r1);
+    else elem_loop<SI, DI, CV, false, false>(P, F, in, out, r0, r1);
   }
 }
 
 __device__ __noinline__ void elem_generic(const Plan& P, const FieldPlan& F, const uint8_t* in, uint8_t* out,
-                                          int rows) {
+                                          int r0, int r1) {
   const int st = F.st, dt = F.dt, sisz = F.sisz, disz = F.disz;
-  for (int r = threadIdx.x; r < rows; r += NT) {
+  for (int r = r0 + static_cast<int>(threadIdx.x & 31); r < r1; r += 32) {
     const uint32_t sa = static_cast<uint32_t>((r >> P.src_lshift) * P.src_A + (r & P.src_msk) * sisz + F.sloc);
     const uint32_t da = static_cast<uint32_t>((r >> P.dst_lshift) * P.dst_A + (r & P.dst_msk) * disz + F.dloc);
     sts_any(out + da, cast_bits(lds_any(in + sa, sisz), st, dt), disz);
@@ -346,19 +349,19 @@ __device__ __noinline__ void elem_generic(const Plan& P, const FieldPlan& F, con
 }
 
 __device__ __forceinline__ void elem_field(const Plan& P, const FieldPlan& F, const uint8_t* in, uint8_t* out,
-                                           int rows) {
+                                           int r0, int r1) {
   switch (F.op) {
     case ELEM_MOVE:
       switch (F.sisz) {
-        case 1: elem_aligned<1, 1, ELEM_MOVE>(P, F, in, out, rows); break;
-        case 2: elem_aligned<2, 2, ELEM_MOVE>(P, F, in, out, rows); break;
-        case 4: elem_aligned<4, 4, ELEM_MOVE>(P, F, in, out, rows); break;
-        default: elem_aligned<8, 8, ELEM_MOVE>(P, F, in, out, rows); break;
+        case 1: elem_aligned<1, 1, ELEM_MOVE>(P, F, in, out, r0, r1); break;
+        case 2: elem_aligned<2, 2, ELEM_MOVE>(P, F, in, out, r0, r1); break;
+        case 4: elem_aligned<4, 4, ELEM_MOVE>(P, F, in, out, r0, r1); break;
+        default: elem_aligned<8, 8, ELEM_MOVE>(P, F, in, out, r0, r1); break;
       }
       break;
-    case ELEM_F64_F32: elem_aligned<8, 4, ELEM_F64_F32>(P, F, in, out, rows); break;
-    case ELEM_F32_F64: elem_aligned<4, 8, ELEM_F32_F64>(P, F, in, out, rows); break;
-    default: elem_generic(P, F, in, out, rows); break;
+    case ELEM_F64_F32: elem_aligned<8, 4, ELEM_F64_F32>(P, F, in, out, r0, r1); break;
+    case ELEM_F32_F64: elem_aligned<4, 8, ELEM_F32_F64>(P, F, in, out, r0, r1); break;
+    default: elem_generic(P, F, in, out, r0, r1); break;
   }
 }
 
@@ -433,11 +436,17 @@ __device__ __forceinline__ void transform(const Plan& P, const uint8_t* __restri
       }
     }
   }
-  if (!P.any_elem) return;
-  // element moves: one field at a time (uniform), lane -> record
-  for (int i = 0; i < P.nfields; ++i) {
-    const FieldPlan& F = P.f[i];
-    if (!F.wordable) elem_field(P, F, in, out, rows);
+  if (!P.n_elem) return;
+  // element moves: work items (field, record chunk) spread over the warps, so
+  // each warp dispatches once per item and walks a long, unrolled record loop
+  const int warp = tid >> 5;
+  const int chunks = P.elem_chunks;
+  const int items = P.n_elem * chunks;
+  for (int it = warp; it < items; it += NT / 32) {
+    const int fi = P.elem_idx[it / chunks];
+    const int c = it - (it / chunks) * chunks;
+    const int r0 = (rows * c) / chunks, r1 = (rows * (c + 1)) / chunks;
+    elem_field(P, P.f[fi], in, out, r0, r1);
   }
 }
 
@@ -706,11 +715,14 @@ int make_plan(const sk_conv_desc& d, const DeviceState& ds, bool in_bulk_ok, boo
   P.epi = epi;
   if (epi == EPI_SENSOR) out_rec += 4000;
 
-  // records per tile: multiple of the granule, larger side ~tile_bytes
+  // records per tile: multiple of the granule, in + out bytes of a tile ~tile_bytes
+  // (the sweeps in profiles/ put the optimum at a fixed smem footprint per tile,
+  // whatever the in/out split: 24+24 KB for Obj8, ~40+10 KB for a 60->16 B AoSoA)
   const Tunables tun = tunables();
   P.cache_hint = tun.cache_hint;
   const int64_t rec = std::max<int64_t>(std::max(in_rec, out_rec), 1000);
-  int64_t R = (static_cast<int64_t>(tun.tile_bytes) * 1000 / rec) / g * g;
+  const int64_t rec_sum = std::max<int64_t>(in_rec + out_rec, 1000);
+  int64_t R = (static_cast<int64_t>(tun.tile_bytes) * 1000 / rec_sum) / g * g;
   R = std::max<int64_t>(R, g);
   R = std::min<int64_t>(R, std::max<int64_t>(g, 4096));
   P.R = static_cast<int32_t>(R);
@@ -815,9 +827,11 @@ int make_plan(const sk_conv_desc& d, const DeviceState& ds, bool in_bulk_ok, boo
     }
     if (!nword) P.mode = MODE_ELEM;
   }
-  P.any_elem = 0;
+  P.n_elem = 0;
   for (int i = 0; i < d.nfields; ++i)
-    if (!P.f[i].wordable) P.any_elem = 1;
+    if (!P.f[i].wordable) P.elem_idx[P.n_elem++] = static_cast<uint8_t>(i);
+  // at least two work items per warp so a slow field does not idle the others
+  P.elem_chunks = P.n_elem ? std::max(1, (2 * (NT / 32) + P.n_elem - 1) / P.n_elem) : 1;
 
   // destination bytes covered by no field are written as zero
   if (d.dst_kind != SK_KIND_PLANES) {

@@ -71,6 +71,9 @@ SETTINGS = [dict()] + [dict(SK_TILE_BYTES=str(t), SK_CTAS=str(c), SK_STAGES=str(
                         for t in (8192, 12288, 16384, 24576, 32768) for c in (2, 3, 4, 6) for s in (2, 3)]
 if os.environ.get("SWEEP_SHORT"):
     SETTINGS = [dict()]
+if os.environ.get("SWEEP_BIG"):
+    SETTINGS = [dict()] + [dict(SK_TILE_BYTES=str(t), SK_CTAS=str(c), SK_STAGES="2")
+                           for t in (32768, 40960, 49152, 65536) for c in (1, 2)]
 
 
 def main():
