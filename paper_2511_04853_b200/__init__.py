@@ -56,6 +56,14 @@ from .schema import (
     declare_subgroup,
     enum_type,
 )
-from .transfer import TransferPriority, copy_collection, move_collection, register_transfer
+from .transfer import (
+    ExternalBinding,
+    TransferPriority,
+    copy_collection,
+    export_external,
+    import_external,
+    move_collection,
+    register_transfer,
+)
 
 __version__ = "0.1.0"

@@ -35,7 +35,7 @@ from . import convert as cv
 from . import layouts as ly
 from . import memctx
 from .collection import Collection
-from .errors import RegistryError, SchemaMismatchError, TransferError, UnsupportedTransferError
+from .errors import RegistryError, SchemaMismatchError, TransferError, UnboundLeafError, UnsupportedTransferError
 from .schema import MAIN_TAG, ROLE_ELEMENT
 
 
@@ -227,6 +227,111 @@ def _planes_execute(dst: Collection, src: Collection, opts: Mapping[str, Any] | 
     _match_sizes(dst, src)
     _copy_planes(dst, src, src.plan.leaves, {"async": True})
     _sync(dst, src, opts)
+
+
+# ---- external record import/export (transfer.py:246-346) ---------------------------------------
+
+@dataclass(frozen=True)
+class ExternalBinding:
+    """extractors: dotted element-leaf path -> fn(record) -> value (a slot list
+    for multi-slot leaves, the whole segment for jagged leaves); factory:
+    fn(dict of the same keys) -> new external record, for export."""
+
+    extractors: Mapping[str, Callable[[Any], Any]]
+    factory: Callable[[Mapping[str, Any]], Any] | None = None
+
+
+def _element_leaves(coll: Collection, binding: ExternalBinding):
+    element = [lf for lf in coll.plan.leaves if lf.role == ROLE_ELEMENT]
+    have = set(binding.extractors)
+    for lf in element:  # first hole in plan order
+        if lf.dotted not in have:
+            raise UnboundLeafError(f"binding has no extractor for leaf {lf.dotted!r}")
+    extra = sorted(have - {lf.dotted for lf in element})
+    if extra:
+        raise TransferError(f"binding names leaves outside the plan: {extra}")
+    return element
+
+
+def import_external(coll: Collection, binding: ExternalBinding, records) -> None:
+    """Replace coll's content with external records. Main-tag columns are
+    materialised from the Python objects into a host staging collection and
+    moved with copy_collection; jagged members go through the GPU packer
+    (multi-leaf members as one struct pool split per leaf)."""
+    import numpy as np
+
+    from . import jagged as jg
+    from .errors import KindError
+
+    element = _element_leaves(coll, binding)
+    records = list(records)
+    n = len(records)
+    stage = Collection(coll.schema, ly.PER_FIELD, memctx.ContextInfo.host())
+    stage.resize(n)
+    for leaf in element:
+        if leaf.size_tag != MAIN_TAG or n == 0:
+            continue
+        ex = binding.extractors[leaf.dotted]
+        col = stage.layout.column_np(leaf)
+        dt = leaf.value_type.np_dtype
+        if leaf.extent_multiplier == 1:
+            col[:] = np.asarray([ex(r) for r in records], dtype=dt)
+        else:
+            block = np.asarray([list(ex(r)) for r in records], dtype=dt)
+            if block.shape != (n, leaf.extent_multiplier):
+                raise TransferError(f"extractor for {leaf.dotted!r} produced shape {block.shape}, "
+                                    f"expected ({n}, {leaf.extent_multiplier})")
+            col[:] = block.T
+    segs = {}
+    for tag in coll.plan.jagged_tags():
+        jleaves = [lf for lf in element if lf.size_tag == tag.id]
+        if any(lf.extent_multiplier != 1 for lf in jleaves):
+            raise KindError(f"import into multi-slot jagged leaves of {tag.id!r} is not supported")
+        per_leaf = {lf.dotted: [np.asarray(list(binding.extractors[lf.dotted](r)), dtype=lf.value_type.np_dtype)
+                                for r in records] for lf in jleaves}
+        lengths = [a.size for a in per_leaf[jleaves[0].dotted]]
+        for lf in jleaves[1:]:
+            if [a.size for a in per_leaf[lf.dotted]] != lengths:
+                raise TransferError(f"jagged leaves {jleaves[0].dotted!r} and {lf.dotted!r} disagree on "
+                                    "segment lengths")
+        segs[tag.id] = (jleaves, per_leaf, np.asarray(lengths, np.int64))
+    with coll.layout.engine_ops():
+        coll.clear()
+    copy_collection(coll, stage)
+    for path, (jleaves, per_leaf, lengths) in segs.items():
+        dt = np.dtype([(lf.dotted, lf.value_type.np_dtype) for lf in jleaves])
+        pool = np.empty(int(lengths.sum()), dt)
+        for lf in jleaves:
+            pool[lf.dotted] = np.concatenate(per_leaf[lf.dotted]) if n else []
+        offsets = np.concatenate([[0], np.cumsum(lengths)[:-1]]) if n else np.empty(0, np.int64)
+        jg.pack(coll, path, lengths, offsets, pool.view(np.uint8), member_stride=dt.itemsize,
+                member_offsets={lf.dotted: dt.fields[lf.dotted][1] for lf in jleaves})
+    stage.free()
+
+
+def export_external(coll: Collection, binding: ExternalBinding) -> list:
+    """One external record per collection record via binding.factory."""
+    element = _element_leaves(coll, binding)
+    if binding.factory is None:
+        raise TransferError("binding has no factory; cannot export")
+    host = coll
+    if not coll.layout.host_visible or isinstance(coll.layout, ly.AosLayout):
+        host = Collection(coll.schema, ly.PER_FIELD, memctx.ContextInfo.host())
+        copy_collection(host, coll)
+    cols = {lf.dotted: host.layout.column_np(lf, writable=False) for lf in element}
+    prefixes = {t.id: host.prefix_sums(t.id) for t in host.plan.jagged_tags()}
+    out = []
+    for i in range(host.size()):
+        row = {}
+        for lf in element:
+            col = cols[lf.dotted]
+            if lf.size_tag == MAIN_TAG:
+                row[lf.dotted] = col[i].item() if lf.extent_multiplier == 1 else col[:, i].tolist()
+            else:
+                pv = prefixes[lf.size_tag]
+                row[lf.dotted] = col[int(pv[i]):int(pv[i + 1])].tolist()
+        out.append(binding.factory(row))
+    return out
 
 
 register_transfer("b200-convert", TransferPriority.EXACT_PAIR, _convert_applies, _convert_execute)
