@@ -224,6 +224,10 @@ __device__ __forceinline__ void store_member(uint8_t* p, uint64_t v, int isz) {
   }
 }
 
+// one padding word per 32 keeps both the consecutive-per-thread scan reads and
+// the strided member reads at <= 2-way bank conflicts
+__device__ __forceinline__ int cpad(int e) { return e + (e >> 5); }
+
 // first record of every member tile: starts[b] = last record c with
 // prefix[c] <= b * SC_TILE (one warp per tile, all tiles in parallel), and
 // starts[ntiles] = the last record holding a member.
@@ -240,6 +244,8 @@ __global__ void __launch_bounds__(SC_NT) scatter_kernel(const __grid_constant__ 
                                                         const int64_t* __restrict__ starts) {
   __shared__ int64_t sP[SC_CMAX + 1];
   __shared__ int64_t sOff[SC_CMAX];
+  __shared__ int32_t sCl[SC_TILE + SC_TILE / 32];  // member -> record (relative), padded
+  __shared__ int32_t sWarpMax[SC_NT / 32];
   const int tid = threadIdx.x;
   const int64_t j0 = static_cast<int64_t>(blockIdx.x) * SC_TILE;
   const int64_t j1 = min(j0 + SC_TILE, A.total);
@@ -254,6 +260,36 @@ __global__ void __launch_bounds__(SC_NT) scatter_kernel(const __grid_constant__ 
     }
   }
   __syncthreads();
+  if (staged) {
+    // record of every member of the tile: mark where each non-empty record
+    // starts, then an inclusive max-scan carries the index forward
+    const int m = static_cast<int>(j1 - j0);
+    for (int e = tid; e < SC_TILE; e += SC_NT) sCl[cpad(e)] = 0;
+    __syncthreads();
+    for (int k = tid + 1; k < cnt; k += SC_NT) {
+      const int64_t s = sP[k] - j0;
+      if (s > 0 && s < m && sP[k + 1] > sP[k]) sCl[cpad(static_cast<int>(s))] = k;
+    }
+    __syncthreads();
+    int vals[SC_IT];
+    int run = 0;
+#pragma unroll
+    for (int i = 0; i < SC_IT; ++i) {
+      run = max(run, sCl[cpad(tid * SC_IT + i)]);
+      vals[i] = run;
+    }
+    int x = run;  // warp-inclusive max of the per-thread maxima
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) x = max(x, __shfl_up_sync(0xffffffffu, x, o));
+    if ((tid & 31) == 31) sWarpMax[tid >> 5] = x;
+    const int excl_lane = __shfl_up_sync(0xffffffffu, x, 1);
+    __syncthreads();
+    int carry = (tid & 31) ? excl_lane : 0;
+    for (int w = 0; w < (tid >> 5); ++w) carry = max(carry, sWarpMax[w]);
+#pragma unroll
+    for (int i = 0; i < SC_IT; ++i) sCl[cpad(tid * SC_IT + i)] = max(vals[i], carry);
+    __syncthreads();
+  }
   // resolve the source element of each of this thread's members first, then move
   int64_t src[SC_IT];
 #pragma unroll
@@ -263,12 +299,7 @@ __global__ void __launch_bounds__(SC_NT) scatter_kernel(const __grid_constant__ 
     if (j < j1) {
       int64_t c, pc, oc;
       if (staged) {
-        int a = 0, b = static_cast<int>(cnt);
-        while (b - a > 1) {
-          const int m = (a + b) >> 1;
-          if (sP[m] <= j) a = m;
-          else b = m;
-        }
+        const int a = sCl[cpad(i * SC_NT + tid)];
         pc = sP[a];
         oc = sOff[a];
       } else {

@@ -42,18 +42,47 @@ def _as_device(a, dtype, dev: int, keep: list) -> DeviceArray:
     return d
 
 
-def scan(lens: DeviceArray, prefix_ptr: int, prefix_code: str, dev: int, keep: list) -> int:
+class _Workspace:
+    """Per-device scan scratch (grown on demand), a device total slot and a
+    pinned host slot to read it back: no allocations on the per-call path."""
+
+    def __init__(self, dev: int) -> None:
+        self.dev = dev
+        self.scratch: DeviceArray | None = None
+        self.total = DeviceArray(1, np.int64, memctx.ContextInfo.cuda(dev))
+        self.host_total = memctx.allocate(memctx.ContextInfo.pinned(), 8)
+
+    def scratch_for(self, nbytes: int) -> DeviceArray:
+        if self.scratch is None or self.scratch.n < nbytes:
+            if self.scratch is not None:
+                self.scratch.free()
+            self.scratch = DeviceArray(max(nbytes, 4096), np.uint8, memctx.ContextInfo.cuda(self.dev))
+        return self.scratch
+
+
+_workspaces: dict[int, _Workspace] = {}
+
+
+def _workspace(dev: int) -> _Workspace:
+    ws = _workspaces.get(dev)
+    if ws is None:
+        ws = _workspaces[dev] = _Workspace(dev)
+    return ws
+
+
+def scan(lens: DeviceArray, prefix_ptr: int, prefix_code: str, dev: int, keep: list | None = None) -> int:
     """Exclusive scan of lens into prefix[0..n]; returns the int64 total."""
     n = lens.n
     need = C.c_size_t(0)
     nat.call("sk_jagged_scratch_bytes", n, C.byref(need))
-    scratch = DeviceArray(max(need.value, 16), np.uint8, memctx.ContextInfo.cuda(dev))
-    total = DeviceArray(1, np.int64, memctx.ContextInfo.cuda(dev))
-    keep += [scratch, total]
+    ws = _workspace(dev)
+    scratch = ws.scratch_for(need.value)
     lens_code = _NP_CODE[lens.dtype]
     nat.call("sk_jagged_scan", n, lens.ptr, nat.TYPE_CODES[lens_code], prefix_ptr, nat.TYPE_CODES[prefix_code],
-             scratch.ptr, need.value, total.ptr, nat.stream(dev))
-    return int(total.numpy()[0])
+             scratch.ptr, scratch.n, ws.total.ptr, nat.stream(dev))
+    nat.memcpy(ws.host_total.ptr, ws.total.ptr, 8, dev)
+    nat.sync(dev)
+    return int(ws.host_total._data.view(np.int64)[0])
 
 
 def pack(coll, path: str, lens, src_offsets, src_pool, member_stride: int | None = None,
