@@ -93,12 +93,24 @@ __device__ __forceinline__ float np_max0(float e) {
 // energy = A * f32(counts) + B ; noise = nA * sqrt(max(E, 0)) + nB, x2 if noisy
 // (detector/schemas.py:29-41)
 __device__ __forceinline__ float sensor_energy(uint64_t counts, float a, float b) {
-  return x86_add(x86_mul(a, __ull2float_rn(counts)), b);
+  const float c = __ull2float_rn(counts);
+  const float e = __fadd_rn(__fmul_rn(a, c), b);
+  return e == e ? e : x86_add(x86_mul(a, c), b);  // NaN: redo with the x86 propagation rule
 }
 
-__device__ __forceinline__ float sensor_noise(float e, float na, float nb, bool noisy) {
+__device__ __forceinline__ float sensor_noise_exact(float e, float na, float nb, bool noisy) {
   const float n = x86_add(x86_mul(na, x86_sqrt(np_max0(e))), nb);
   return noisy ? x86_mul(n, 2.0f) : n;
+}
+
+// Common path without the NaN bookkeeping; any NaN anywhere in the chain shows
+// up as a NaN result, and only then is the exact x86 path evaluated.
+__device__ __forceinline__ float sensor_noise(float e, float na, float nb, bool noisy) {
+  const float m = e > 0.0f ? e : 0.0f;
+  float n = __fadd_rn(__fmul_rn(na, __fsqrt_rn(m)), nb);
+  if (noisy) n = __fmul_rn(n, 2.0f);
+  if (n != n || e != e) return sensor_noise_exact(e, na, nb, noisy);
+  return n;
 }
 
 // ---- PTX wrappers -------------------------------------------------------------
