@@ -21,8 +21,10 @@
 #ifndef SOAKIT_B200_H
 #define SOAKIT_B200_H
 
+#ifndef __CUDACC_RTC__ /* the library also compiles its kernels at run time (NVRTC) */
 #include <stddef.h>
 #include <stdint.h>
+#endif
 
 #ifdef __cplusplus
 extern "C" {
@@ -81,6 +83,7 @@ typedef struct sk_conv_desc {
   sk_field fields[SK_MAX_FIELDS];
 } sk_conv_desc;
 
+#ifndef __CUDACC_RTC__
 /* ---- diagnostics ---------------------------------------------------------- */
 const char* sk_last_error(void);
 int sk_version(void);                     /* 0x00MMmmpp */
@@ -130,6 +133,12 @@ int sk_peer_enable(int device, int peer);
    `device` pulls the bytes over NVLink. Replaces _per_leaf_execute's
    per-leaf gather + staging (transfer.py:182-233). */
 int sk_convert(const sk_conv_desc* desc, int device, uintptr_t stream);
+/* Diagnostic: generate the record-signature-specialised transform the engine
+   would JIT (NVRTC) for `desc` (epi_fields: the 7 sensor field indices of the
+   fused case-study path, or NULL), copy its source to source_out, and compile
+   it for sm_100a without launching. SK_ERR_UNSUPPORTED: not eligible. */
+int sk_convert_specialize_check(const sk_conv_desc* desc, const int* epi_fields,
+                                char* source_out, size_t capacity, size_t* source_len);
 /* Dry run: validates `desc` and reports the tiling the engine would use. */
 int sk_convert_plan(const sk_conv_desc* desc, int device, int* records_per_tile,
                     int* stages, int* mode, size_t* smem_bytes, int* grid);
@@ -205,6 +214,7 @@ int sk_ipc_handle_size(size_t* nbytes);
 int sk_ipc_get_handle(void* dev_ptr, void* handle_out);
 int sk_ipc_open_handle(int device, const void* handle, void** dev_ptr);
 int sk_ipc_close_handle(int device, void* dev_ptr);
+#endif /* !__CUDACC_RTC__ */
 
 #ifdef __cplusplus
 }

@@ -1,6 +1,6 @@
-// Shared internals of libsoakit_b200: error state, device/stream registry,
-// dtype helpers and the PTX wrappers (mbarrier + bulk async copies) the
-// kernels use.
+// Host-side internals of libsoakit_b200: error state, device/stream registry,
+// dtype helpers. Device helpers (x86-exact float ops, PTX wrappers) live in
+// sk_device.cuh.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -8,6 +8,7 @@
 #include <cstdarg>
 
 #include "soakit_b200.h"
+#include "sk_device.cuh"
 
 namespace sk {
 
@@ -46,160 +47,6 @@ inline int dtype_size(int t) {
     case SK_U64: case SK_I64: case SK_F64: return 8;
     default: return 0;
   }
-}
-
-// ---- numpy-on-x86 float32 arithmetic ----------------------------------------------
-// The reference computes the case study with numpy on x86 (SSE/AVX). IEEE fixes
-// every finite and infinite result, but not NaN bits: x86 returns the first
-// NaN operand (quieted) and the "real indefinite" 0xFFC00000 for invalid
-// operations, where the GPU returns 0x7FFFFFFF. These wrappers restore the x86
-// rule so outputs are bit-exact, NaN payloads included. The _rn intrinsics
-// also keep ptxas from contracting a*b+c into an FMA.
-
-__device__ __forceinline__ float x86_quiet(float x) { return __uint_as_float(__float_as_uint(x) | 0x00400000u); }
-
-__device__ __forceinline__ float x86_nan_result(float a, float b) {
-  if (a != a) return x86_quiet(a);
-  if (b != b) return x86_quiet(b);
-  return __uint_as_float(0xffc00000u);
-}
-
-__device__ __forceinline__ float x86_mul(float a, float b) {
-  const float r = __fmul_rn(a, b);
-  return r == r ? r : x86_nan_result(a, b);
-}
-
-__device__ __forceinline__ float x86_add(float a, float b) {
-  const float r = __fadd_rn(a, b);
-  return r == r ? r : x86_nan_result(a, b);
-}
-
-__device__ __forceinline__ float x86_sqrt(float m) {
-  if (m != m) return x86_quiet(m);
-  const float r = __fsqrt_rn(m);
-  return r == r ? r : __uint_as_float(0xffc00000u);
-}
-
-// np.maximum(e, 0.0f) as numpy's vectorised loop computes it: NaN propagates
-// unchanged, and for two zeros vmaxps returns its second operand (+0.0).
-// Integer tests on purpose: a float select is rewritten by ptxas into
-// FMNMX.NAN, which returns the canonical NaN instead of the input bits.
-__device__ __forceinline__ float np_max0(float e) {
-  const uint32_t u = __float_as_uint(e);
-  if ((u & 0x7fffffffu) > 0x7f800000u) return e;           // NaN, bits unchanged
-  return ((u & 0x80000000u) || u == 0u) ? 0.0f : e;        // negatives and +-0 -> +0
-}
-
-// energy = A * f32(counts) + B ; noise = nA * sqrt(max(E, 0)) + nB, x2 if noisy
-// (detector/schemas.py:29-41)
-__device__ __forceinline__ float sensor_energy(uint64_t counts, float a, float b) {
-  const float c = __ull2float_rn(counts);
-  const float e = __fadd_rn(__fmul_rn(a, c), b);
-  return e == e ? e : x86_add(x86_mul(a, c), b);  // NaN: redo with the x86 propagation rule
-}
-
-__device__ __forceinline__ float sensor_noise_exact(float e, float na, float nb, bool noisy) {
-  const float n = x86_add(x86_mul(na, x86_sqrt(np_max0(e))), nb);
-  return noisy ? x86_mul(n, 2.0f) : n;
-}
-
-// Common path without the NaN bookkeeping; any NaN anywhere in the chain shows
-// up as a NaN result, and only then is the exact x86 path evaluated.
-__device__ __forceinline__ float sensor_noise(float e, float na, float nb, bool noisy) {
-  const float m = e > 0.0f ? e : 0.0f;
-  float n = __fadd_rn(__fmul_rn(na, __fsqrt_rn(m)), nb);
-  if (noisy) n = __fmul_rn(n, 2.0f);
-  if (n != n || e != e) return sensor_noise_exact(e, na, nb, noisy);
-  return n;
-}
-
-// ---- PTX wrappers -------------------------------------------------------------
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-
-__device__ __forceinline__ void fence_mbar_init() {
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  uint32_t done = 0;
-  const uint32_t addr = smem_u32(bar);
-  do {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(done)
-        : "r"(addr), "r"(parity)
-        : "memory");
-  } while (!done);
-}
-
-// global -> shared bulk copy (TMA engine, non-tensor); completes tx on `bar`.
-__device__ __forceinline__ void bulk_g2s(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar,
-                                         uint64_t policy) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
-          smem_u32(smem_dst)),
-      "l"(gsrc), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
-      : "memory");
-}
-
-__device__ __forceinline__ void bulk_g2s_plain(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   smem_u32(smem_dst)),
-               "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
-               : "memory");
-}
-
-__device__ __forceinline__ void bulk_s2g_plain(void* gdst, const void* smem_src, uint32_t bytes) {
-  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_u32(smem_src)),
-               "r"(bytes)
-               : "memory");
-}
-
-// shared -> global bulk copy, tracked by the issuing thread's bulk groups.
-__device__ __forceinline__ void bulk_s2g(void* gdst, const void* smem_src, uint32_t bytes, uint64_t policy) {
-  asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(gdst),
-               "r"(smem_u32(smem_src)), "r"(bytes), "l"(policy)
-               : "memory");
-}
-
-__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-
-template <int N>
-__device__ __forceinline__ void bulk_wait_read() {
-  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
-}
-
-__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
-
-// generic-proxy smem writes -> visible to the async proxy (bulk store source)
-__device__ __forceinline__ void fence_proxy_async() {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-
-__device__ __forceinline__ uint64_t policy_evict_first() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-
-__device__ __forceinline__ uint64_t policy_evict_normal() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 0.0;" : "=l"(p));
-  return p;
 }
 
 }  // namespace sk

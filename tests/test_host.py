@@ -184,6 +184,54 @@ def test_shard_ranges_cover_exactly():
     assert shard.exclusive_offsets([3, 0, 5, 2]) == [0, 3, 3, 8]
 
 
+# ---- record-signature specialisation (NVRTC, compiled here without a GPU) -------------------
+
+def _spec_check(desc, epi=None):
+    buf = ctypes.create_string_buffer(1 << 17)
+    ln = ctypes.c_size_t()
+    ep = (ctypes.c_int * 7)(*epi) if epi else None
+    st = nat.lib().sk_convert_specialize_check(ctypes.byref(desc), ep, buf, len(buf), ctypes.byref(ln))
+    return st, buf.value.decode(), nat.lib().sk_last_error().decode()
+
+
+def test_specialised_transforms_compile_for_sm100a():
+    a = sk.Collection(sensor.SENSOR_SCHEMA, ly.AOS)
+    p = sk.Collection(sensor.SENSOR_SCHEMA, ly.PER_FIELD)
+    for c in (a, p):
+        c.resize(777)
+    st, src, err = _spec_check(cv.plan_desc(p.layout, a.layout, 777))
+    assert st == nat.SK_OK, err
+    assert "const uint32_t W14 = w[14];" in src and "kFusedEpilogue = false" in src  # 2 x 30 B = 15 words
+    names = [lf.dotted for lf, _ in cv.main_slots(a.layout)]
+    epi = [names.index(k) for k in ("counts", "energy", "calibration_data.noisy", "calibration_data.parameter_A",
+                                    "calibration_data.parameter_B", "calibration_data.noise_A",
+                                    "calibration_data.noise_B")]
+    st, src, err = _spec_check(cv.plan_desc(p.layout, a.layout, 777), epi)
+    assert st == nat.SK_OK and "sensor_noise" in src, err
+    # planes -> AoS of the 64 B Particle record (u8 slots force the element path)
+    pa = sk.Collection(sensor.PARTICLE_SCHEMA, ly.AOS)
+    pp = sk.Collection(sensor.PARTICLE_SCHEMA, ly.PER_FIELD)
+    for c in (pa, pp):
+        c.resize(300)
+    st, src, err = _spec_check(cv.plan_desc(pa.layout, pp.layout, 300))
+    assert st == nat.SK_OK, err
+    # AoSoA with casts
+    t = sk.Collection(wl.TRACK_SCHEMA, ly.AOS)
+    t.resize(1000)
+    ao = cv.Aosoa.__new__(cv.Aosoa)  # geometry only: no device buffer needed for the check
+    ao.n, ao.lanes = 1000, 128
+    ao.fields = [cv.AosoaField("pz", "f32"), cv.AosoaField("px", "f32"), cv.AosoaField("charge", "i64")]
+    ao.block_off = [0, 512, 1024]
+    ao.tile_bytes = 2048
+
+    class _Buf:
+        ptr = 1 << 20  # never dereferenced: the check only plans and compiles
+
+    ao.buffer = _Buf()
+    st, src, err = _spec_check(cv._aosoa_desc(t.layout, ao, True))
+    assert st == nat.SK_OK and "cast_bits(" in src, err
+
+
 # ---- the C-ABI library ---------------------------------------------------------------------
 
 def _header_functions():
