@@ -165,6 +165,20 @@ int sk_jagged_scatter(int64_t n, const void* prefix, int prefix_type,
                       const int32_t* field_size, void* const* dst_pools,
                       int64_t total, uintptr_t stream);
 
+/* scan + gather in one call with no host round trip: the gather is
+   sized by the pools' `capacity` (members) and reads the true total from
+   *total_dev on the device, so it is complete iff *total_dev <= capacity; the
+   caller reads *total_dev afterwards and, on overflow, grows the pools and
+   gathers again with sk_jagged_scatter. Scratch: at least sk_jagged_scratch_bytes;
+   with (capacity / 2048 + 1) * 8 more bytes after it (256-aligned) the call
+   allocates nothing. */
+int sk_jagged_pack(int64_t n, const void* lens, int lens_type, void* prefix,
+                   int prefix_type, const int64_t* src_off, const void* src_pool,
+                   int64_t member_stride, int nfields, const int64_t* field_off,
+                   const int32_t* field_size, void* const* dst_pools, int64_t capacity,
+                   void* scratch, size_t scratch_bytes, int64_t* total_dev,
+                   uintptr_t stream);
+
 /* ---- behavior plugin: the case-study per-object kernel (detector/schemas.py) */
 /* energy = A * f32(counts) + B, two f32 roundings, no FMA
    (calibrate_collection, detector/schemas.py:29-33). */

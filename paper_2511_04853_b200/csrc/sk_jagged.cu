@@ -57,7 +57,8 @@ __device__ __forceinline__ int pad(int e) { return e + (e >> 4); }
 
 __global__ void __launch_bounds__(SCAN_NT) scan_kernel(int64_t n, const void* __restrict__ lens, int lens_type,
                                                        void* __restrict__ out, int out_type, uint64_t* status,
-                                                       unsigned int* ticket, int64_t* total_out) {
+                                                       unsigned int* ticket, int64_t* total_out,
+                                                       int64_t* __restrict__ out64) {
   __shared__ int64_t s[SCAN_TILE + SCAN_TILE / 16];
   __shared__ int64_t warp_tot[SCAN_NT / 32];
   __shared__ int64_t s_excl;
@@ -140,10 +141,14 @@ __global__ void __launch_bounds__(SCAN_NT) scan_kernel(int64_t n, const void* __
     if (idx < n) {
       const int64_t v = s[pad(e)];
       store_int(out, out_type, idx + 1, v);
+      if (out64) out64[idx + 1] = v;  // non-wrapped copy for the gather
       if (idx == n - 1 && total_out) *total_out = v;
     }
   }
-  if (tile == 0 && tid == 0) store_int(out, out_type, 0, 0);
+  if (tile == 0 && tid == 0) {
+    store_int(out, out_type, 0, 0);
+    if (out64) out64[0] = 0;
+  }
 }
 
 // ---- scatter ------------------------------------------------------------------------
@@ -161,7 +166,8 @@ struct ScatterArgs {
   const int64_t* src_off;
   const uint8_t* src_pool;
   int64_t member_stride;
-  int64_t total;
+  int64_t total;             // members to gather, or the capacity bound when total_dev is set
+  const int64_t* total_dev;  // device-resident total (fused pack): gather min(*total_dev, total)
   int nfields;
   int aligned;  // all member fields naturally aligned
   int64_t field_off[SC_MAXF];
@@ -224,6 +230,15 @@ __device__ __forceinline__ void store_member(uint8_t* p, uint64_t v, int isz) {
   }
 }
 
+// members to gather. Fused pack: the device total if it fits the capacity
+// bound, else nothing -- on overflow the (narrow) prefix may have wrapped and
+// the host redoes the pack with grown pools, so no search may run over it.
+__device__ __forceinline__ int64_t eff_total(const ScatterArgs& A) {
+  if (!A.total_dev) return A.total;
+  const int64_t t = *A.total_dev;
+  return t <= A.total ? t : 0;
+}
+
 // one padding word per 32 keeps both the consecutive-per-thread scan reads and
 // the strided member reads at <= 2-way bank conflicts
 __device__ __forceinline__ int cpad(int e) { return e + (e >> 5); }
@@ -235,7 +250,9 @@ __global__ void __launch_bounds__(256) tile_start_kernel(const __grid_constant__
                                                          int64_t ntiles) {
   const int64_t b = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
   if (b > ntiles) return;
-  const int64_t j = b < ntiles ? b * SC_TILE : A.total - 1;
+  const int64_t T = eff_total(A);
+  if (T <= 0) return;
+  const int64_t j = b * SC_TILE < T ? b * SC_TILE : T - 1;
   const int64_t c = search_warp(A, 0, A.n, j);
   if ((threadIdx.x & 31) == 0) starts[b] = c;
 }
@@ -248,7 +265,9 @@ __global__ void __launch_bounds__(SC_NT) scatter_kernel(const __grid_constant__ 
   __shared__ int32_t sWarpMax[SC_NT / 32];
   const int tid = threadIdx.x;
   const int64_t j0 = static_cast<int64_t>(blockIdx.x) * SC_TILE;
-  const int64_t j1 = min(j0 + SC_TILE, A.total);
+  const int64_t T = eff_total(A);
+  if (j0 >= T) return;
+  const int64_t j1 = min(j0 + SC_TILE, T);
   // the records covering [j0, j1) lie in [starts[b], starts[b+1]]
   const int64_t lo = starts[blockIdx.x];
   const int64_t cnt = starts[blockIdx.x + 1] - lo + 1;
@@ -368,14 +387,15 @@ int sk_jagged_scan(int64_t n, const void* lens, int lens_type, void* prefix, int
   unsigned int* ticket = static_cast<unsigned int*>(scratch);
   uint64_t* status = reinterpret_cast<uint64_t*>(static_cast<uint8_t*>(scratch) + 16);
   jag::scan_kernel<<<static_cast<unsigned>(tiles), jag::SCAN_NT, 0, s>>>(n, lens, lens_type, prefix, prefix_type,
-                                                                          status, ticket, total_dev);
+                                                                          status, ticket, total_dev, nullptr);
   SK_TRY(cudaGetLastError());
   return SK_OK;
 }
 
-int sk_jagged_scatter(int64_t n, const void* prefix, int prefix_type, const int64_t* src_off, const void* src_pool,
-                      int64_t member_stride, int nfields, const int64_t* field_off, const int32_t* field_size,
-                      void* const* dst_pools, int64_t total, uintptr_t stream) {
+static int scatter_impl(int64_t n, const void* prefix, int prefix_type, const int64_t* src_off, const void* src_pool,
+                        int64_t member_stride, int nfields, const int64_t* field_off, const int32_t* field_size,
+                        void* const* dst_pools, int64_t total, const int64_t* total_dev, uintptr_t stream,
+                        int64_t* starts_buf = nullptr) {
   if (n < 0 || total < 0) return set_error(SK_ERR_INVALID, "negative sizes");
   if (nfields < 1 || nfields > jag::SC_MAXF) return set_error(SK_ERR_INVALID, "nfields %d outside [1, 8]", nfields);
   if (!int_type(prefix_type)) return set_error(SK_ERR_INVALID, "prefix type must be an integer type");
@@ -388,6 +408,7 @@ int sk_jagged_scatter(int64_t n, const void* prefix, int prefix_type, const int6
   A.src_pool = static_cast<const uint8_t*>(src_pool);
   A.member_stride = member_stride;
   A.total = total;
+  A.total_dev = total_dev;
   A.nfields = nfields;
   bool aligned = true;
   for (int f = 0; f < nfields; ++f) {
@@ -407,14 +428,67 @@ int sk_jagged_scatter(int64_t n, const void* prefix, int prefix_type, const int6
   SK_TRY(cudaGetDevice(&dev));
   cudaStream_t s = resolve_stream(dev, stream);
   const int64_t blocks = (total + jag::SC_TILE - 1) / jag::SC_TILE;
-  int64_t* starts = nullptr;
-  SK_TRY(cudaMallocAsync(&starts, static_cast<size_t>(blocks + 1) * sizeof(int64_t), s));
+  int64_t* starts = starts_buf;
+  if (!starts) SK_TRY(cudaMallocAsync(&starts, static_cast<size_t>(blocks + 1) * sizeof(int64_t), s));
   jag::tile_start_kernel<<<static_cast<unsigned>((blocks + 1 + 7) / 8), 256, 0, s>>>(A, starts, blocks);
   SK_TRY(cudaGetLastError());
   jag::scatter_kernel<<<static_cast<unsigned>(blocks), jag::SC_NT, 0, s>>>(A, starts);
   SK_TRY(cudaGetLastError());
-  SK_TRY(cudaFreeAsync(starts, s));
+  if (!starts_buf) SK_TRY(cudaFreeAsync(starts, s));
   return SK_OK;
+}
+
+int sk_jagged_scatter(int64_t n, const void* prefix, int prefix_type, const int64_t* src_off, const void* src_pool,
+                      int64_t member_stride, int nfields, const int64_t* field_off, const int32_t* field_size,
+                      void* const* dst_pools, int64_t total, uintptr_t stream) {
+  return scatter_impl(n, prefix, prefix_type, src_off, src_pool, member_stride, nfields, field_off, field_size,
+                      dst_pools, total, nullptr, stream);
+}
+
+int sk_jagged_pack(int64_t n, const void* lens, int lens_type, void* prefix, int prefix_type, const int64_t* src_off,
+                   const void* src_pool, int64_t member_stride, int nfields, const int64_t* field_off,
+                   const int32_t* field_size, void* const* dst_pools, int64_t capacity, void* scratch,
+                   size_t scratch_bytes, int64_t* total_dev, uintptr_t stream) {
+  if (n < 0 || capacity < 0) return set_error(SK_ERR_INVALID, "negative sizes");
+  if (!total_dev) return set_error(SK_ERR_INVALID, "total_dev is required");
+  if (!int_type(lens_type) || !int_type(prefix_type) || lens_type == SK_BOOL || prefix_type == SK_BOOL)
+    return set_error(SK_ERR_INVALID, "jagged lengths and prefix need integer types");
+  size_t need = 0;
+  sk_jagged_scratch_bytes(n, &need);
+  if (scratch_bytes < need) return set_error(SK_ERR_INVALID, "scratch too small: %zu < %zu", scratch_bytes, need);
+  int dev = 0;
+  SK_TRY(cudaGetDevice(&dev));
+  cudaStream_t s = resolve_stream(dev, stream);
+  if (n == 0) {
+    SK_TRY(cudaMemsetAsync(prefix, 0, dtype_size(prefix_type), s));
+    SK_TRY(cudaMemsetAsync(total_dev, 0, 8, s));
+    return SK_OK;
+  }
+  // a prefix type that can wrap below the capacity needs an int64 copy for the gather
+  const int bits = 8 * dtype_size(prefix_type) - ((prefix_type == SK_I32 || prefix_type == SK_I64) ? 1 : 0);
+  const bool may_wrap = bits < 63 && capacity >= (int64_t(1) << bits);
+  int64_t* p64 = nullptr;
+  if (may_wrap) SK_TRY(cudaMallocAsync(&p64, static_cast<size_t>(n + 1) * sizeof(int64_t), s));
+  SK_TRY(cudaMemsetAsync(scratch, 0, need, s));
+  const int64_t tiles = (n + jag::SCAN_TILE - 1) / jag::SCAN_TILE;
+  unsigned int* ticket = static_cast<unsigned int*>(scratch);
+  uint64_t* status = reinterpret_cast<uint64_t*>(static_cast<uint8_t*>(scratch) + 16);
+  jag::scan_kernel<<<static_cast<unsigned>(tiles), jag::SCAN_NT, 0, s>>>(n, lens, lens_type, prefix, prefix_type,
+                                                                          status, ticket, total_dev, p64);
+  SK_TRY(cudaGetLastError());
+  // gather bounded by the pools' capacity; the kernels read the true total on the device
+  // the tile-start array lives in the caller's scratch when it is large enough
+  const size_t scan_part = (need + 255) & ~size_t(255);
+  const size_t starts_need = static_cast<size_t>((capacity + jag::SC_TILE - 1) / jag::SC_TILE + 1) * sizeof(int64_t);
+  int64_t* starts = scratch_bytes >= scan_part + starts_need
+                        ? reinterpret_cast<int64_t*>(static_cast<uint8_t*>(scratch) + scan_part)
+                        : nullptr;
+  int rc = capacity ? scatter_impl(n, p64 ? static_cast<const void*>(p64) : prefix, p64 ? SK_I64 : prefix_type,
+                                   src_off, src_pool, member_stride, nfields, field_off, field_size, dst_pools,
+                                   capacity, total_dev, stream, starts)
+                    : SK_OK;
+  if (p64) cudaFreeAsync(p64, s);
+  return rc;
 }
 
 }  // extern "C"

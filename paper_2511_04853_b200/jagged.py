@@ -128,6 +128,33 @@ def pack(coll, path: str, lens, src_offsets, src_pool, member_stride: int | None
         tmp_p = DeviceArray(n + 1, pleaf.value_type.np_dtype, memctx.ContextInfo.cuda(dev))
         keep.append(tmp_p)
         prefix_ptr = tmp_p.ptr
+    nf = len(leaves)
+    offs = (C.c_int64 * nf)(*[member_offsets[lf.dotted] for lf in leaves])
+    sizes = (C.c_int32 * nf)(*[lf.value_type.size_bytes for lf in leaves])
+    if device_resident and lay.capacity(path) > 0:
+        # fused scan + gather bounded by the current pool capacity: one sync
+        cap = lay.capacity(path)
+        ws = _workspace(dev)
+        need = C.c_size_t(0)
+        nat.call("sk_jagged_scratch_bytes", n, C.byref(need))
+        starts_bytes = ((cap + 2047) // 2048 + 1) * 8  # tile starts of the gather, kept in the scratch too
+        scratch = ws.scratch_for(-(-need.value // 256) * 256 + starts_bytes)
+        ptrs = (C.c_void_p * nf)(*[lay.plane_address(lf, 0) for lf in leaves])
+        nat.call("sk_jagged_pack", n, lens_d.ptr, nat.TYPE_CODES[_NP_CODE[lens_d.dtype]], prefix_ptr,
+                 nat.TYPE_CODES[pcode], off_d.ptr, pool_d.ptr, int(member_stride), nf, offs, sizes, ptrs, cap,
+                 scratch.ptr, scratch.n, ws.total.ptr, nat.stream(dev))
+        nat.memcpy(ws.host_total.ptr, ws.total.ptr, 8, dev)
+        nat.sync(dev)
+        total = int(ws.host_total._data.view(np.int64)[0])
+        if total <= cap:
+            coll._bump()
+            with lay.engine_ops():
+                lay._set_sizes_for_engine({path: total})
+            for t in keep:
+                t.free()
+            return total
+        # overflow: the pools must grow first -- redo as scan, resize, gather
+
     total = scan(lens_d, prefix_ptr, pcode, dev, keep)
 
     coll._bump()
@@ -143,9 +170,6 @@ def pack(coll, path: str, lens, src_offsets, src_pool, member_stride: int | None
         scan(lens_d, p64.ptr, "i64", dev, keep)
         scatter_ptr, scatter_code = p64.ptr, "i64"
 
-    nf = len(leaves)
-    offs = (C.c_int64 * nf)(*[member_offsets[lf.dotted] for lf in leaves])
-    sizes = (C.c_int32 * nf)(*[lf.value_type.size_bytes for lf in leaves])
     if device_resident:
         dsts = [lay.plane_address(lf, 0) for lf in leaves]
     else:

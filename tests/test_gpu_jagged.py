@@ -100,6 +100,23 @@ def test_long_and_empty_segments():
     assert p.tobytes() == p_want.tobytes() and m.tobytes() == m_want.tobytes()
 
 
+@pytest.mark.parametrize("itype,idx_dtype", [(sc.I32, np.int32), (sc.U8, np.uint8)])
+def test_fused_repack_and_overflow_fallback(itype, idx_dtype):
+    """Second and later packs run scan+gather in one call bounded by the pool
+    capacity; a pack that outgrows it falls back to scan / grow / gather."""
+    schema = sc.Schema("J", (sc.declare_per_item("seed", sc.U64), sc.declare_jagged("members", itype, sc.U64)))
+    c = sk.Collection(schema, ly.PER_FIELD, CUDA)
+    with mc.execution_scope(mc.CUDA):
+        c.resize(3000)
+    for seed, max_len in ((1, 10), (2, 10), (3, 4), (4, 30), (5, 30)):  # 4: overflow, 5: fused again
+        lens, offsets, pool = wl.cluster_inputs(3000, seed=seed, max_len=max_len)
+        total = jagged.pack(c, "members", lens, offsets, pool)
+        p_want, m_want = R.jagged_pack(lens, offsets, pool, idx_dtype)
+        p, m = _read(c, "members")
+        assert total == m_want.size and c.jagged_size("members") == total
+        assert p.tobytes() == p_want.tobytes() and m.tobytes() == m_want.tobytes(), seed
+
+
 def test_packed_collection_transfers_to_host_aos():
     lens, offsets, pool = wl.cluster_inputs(5000, seed=3)
     c = sk.Collection(wl.CLUSTER_SCHEMA, ly.PER_FIELD, CUDA)
