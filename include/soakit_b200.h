@@ -211,6 +211,27 @@ int sk_sensor_generate(int64_t w, int64_t h, const uint64_t* seeds, int nevents,
                        uint64_t* counts, uint8_t* noisy, float* a, float* b, float* na,
                        float* nb, float* energy, uintptr_t stream);
 
+/* Particle reconstruction (reconstruct_arrays, detector/reconstruct.py:53-136)
+   over nevents calibrated events of w x h cells (energy/noise/type/noisy
+   planes, event-major). Round-synchronous parallel greedy: same particles in
+   the same order as the reference's sequential seed walk. Returns an opaque
+   handle with the particles and per-event counts; sk_reco_write then writes
+   them in reference order into per-field planes (slot planes of the 4-wide
+   arrays as separate pointers), the per-particle contributor counts and
+   offsets into a contributor pool owned by the handle (*sensor_pool, u64
+   cell indices) for the jagged packer; sk_reco_free releases everything. */
+int sk_reco_run(int64_t w, int64_t h, int nevents, const float* energy,
+                const float* noise, const uint8_t* type, const uint8_t* noisy,
+                int device, uintptr_t stream, void** handle, int64_t* nparticles,
+                int* rounds);
+int sk_reco_event_counts(void* handle, int64_t* counts);
+int sk_reco_write(void* handle, float* energy, float* x, float* y, uint64_t* origin,
+                  float* x_variance, float* y_variance, float* const* significance,
+                  float* const* e_contribution, uint8_t* const* noisy_count,
+                  int32_t* sensor_lens, int64_t* sensor_offsets,
+                  const uint64_t** sensor_pool, uintptr_t stream);
+int sk_reco_free(void* handle, uintptr_t stream);
+
 /* ---- synthetic inputs ------------------------------------------------------- */
 /* Fill nbytes of device memory with splitmix64(seed, first_word + word index)
    bits (counter-based, so a shard starting at 8-byte word `first_word` of the

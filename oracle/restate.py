@@ -159,3 +159,71 @@ def sensor_aos(ev: dict[str, np.ndarray]) -> np.ndarray:
     for k in ("noisy", "parameter_A", "parameter_B", "noise_A", "noise_B"):
         cal[k] = ev[k]
     return s
+
+
+# ---- particle reconstruction (detector/reconstruct.py:53-136) -----------------------------
+
+def reconstruct(energy, noise, sensor_type, noisy, width: int, height: int) -> dict:
+    """Greedy seeded 5x5 clustering, restated from reconstruct.py:53-136: seeds
+    (ratio > 5) in descending energy / ascending index; each unconsumed seed
+    takes the unconsumed ratio > 2 cells of its grid-clipped window in
+    row-major order; per-type f64 sums rounded once to f32; energy-weighted
+    f64 centroid and two-pass variance."""
+    n = width * height
+    energy = np.asarray(energy, dtype=np.float32)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        ratio = energy / np.asarray(noise, dtype=np.float32)
+    cand = np.flatnonzero(ratio > np.float32(5.0))
+    seeds = cand[np.argsort(-energy[cand], kind="stable")]
+    consumed = np.zeros(n, dtype=bool)
+    out = {k: [] for k in ("energy", "x", "y", "origin", "x_variance", "y_variance", "significance",
+                           "E_contribution", "noisy_count", "sensors")}
+    for s in seeds:
+        s = int(s)
+        if consumed[s]:
+            continue
+        sy, sx = divmod(s, width)
+        contrib = []
+        for y in range(max(0, sy - 2), min(height - 1, sy + 2) + 1):
+            for x in range(max(0, sx - 2), min(width - 1, sx + 2) + 1):
+                f = y * width + x
+                if not consumed[f] and ratio[f] > np.float32(2.0):
+                    consumed[f] = True
+                    contrib.append(f)
+        e64, sig64, cnt = [0.0] * 4, [0.0] * 4, [0] * 4
+        sw = swx = swy = 0.0
+        for f in contrib:
+            e, t = float(energy[f]), int(sensor_type[f])
+            e64[t] += e
+            sig64[t] += float(ratio[f])
+            cnt[t] += bool(noisy[f])
+            sw += e
+            swx += e * (f % width)
+            swy += e * (f // width)
+        xbar, ybar = swx / sw, swy / sw
+        vx = vy = 0.0
+        for f in contrib:
+            e = float(energy[f])
+            vx += e * (f % width - xbar) ** 2
+            vy += e * (f // width - ybar) ** 2
+        e32 = [np.float32(v) for v in e64]
+        out["energy"].append(np.float32(float(e32[0]) + float(e32[1]) + float(e32[2]) + float(e32[3])))
+        out["x"].append(np.float32(xbar))
+        out["y"].append(np.float32(ybar))
+        out["origin"].append(s)
+        out["x_variance"].append(np.float32(vx / sw))
+        out["y_variance"].append(np.float32(vy / sw))
+        out["significance"].append([np.float32(v) for v in sig64])
+        out["E_contribution"].append(e32)
+        out["noisy_count"].append(cnt)
+        out["sensors"].append(np.array(contrib, dtype=np.uint64))
+    m = len(out["energy"])
+    res = {k: np.array(out[k], dtype=dt) for k, dt in (("energy", np.float32), ("x", np.float32), ("y", np.float32),
+                                                       ("origin", np.uint64), ("x_variance", np.float32),
+                                                       ("y_variance", np.float32))}
+    res["significance"] = np.array(out["significance"], np.float32).reshape(m, 4)
+    res["E_contribution"] = np.array(out["E_contribution"], np.float32).reshape(m, 4)
+    res["noisy_count"] = np.array(out["noisy_count"], np.uint8).reshape(m, 4)
+    res["sensor_lens"] = np.array([a.size for a in out["sensors"]], np.int32)
+    res["sensors"] = np.concatenate(out["sensors"]) if m else np.empty(0, np.uint64)
+    return res

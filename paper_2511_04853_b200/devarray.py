@@ -29,6 +29,15 @@ class DeviceArray:
                 nat.sync(out.device)
         return out
 
+    @classmethod
+    def wrap(cls, ptr: int, n: int, dtype, device: int) -> "DeviceArray":
+        """Non-owning view of device memory owned elsewhere (free() is a no-op)."""
+        out = cls.__new__(cls)
+        out.dtype, out.n, out.info = np.dtype(dtype), int(n), memctx.ContextInfo.cuda(device)
+        out.buffer = memctx.Buffer(0, out.info, out.n * out.dtype.itemsize, ptr, None, "view")
+        out.buffer._live = False  # not registered with the context: nothing to release
+        return out
+
     @property
     def ptr(self) -> int:
         return self.buffer.ptr

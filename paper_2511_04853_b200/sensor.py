@@ -137,6 +137,60 @@ def generate_events(coll, width: int, height: int, seeds, density: float = 0.0, 
         nat.sync(dev)
 
 
+def reconstruct_from_collection(sensors, width: int, height: int, out=None, events: int = 1, noise=None):
+    """Particle reconstruction on the GPU (detector/reconstruct.py:172-194 /
+    reconstruct_arrays 53-136) for `events` calibrated events stored event-major
+    in a device-resident Sensor collection. Returns a device per_field Particle
+    collection (or fills `out`) with the reference's particles in the
+    reference's order, events concatenated; out.event_counts holds the
+    per-event particle counts."""
+    from . import jagged
+    from .collection import Collection
+
+    dev, p = _device_planes(sensors)
+    n = width * height
+    if sensors.size() != n * events:
+        raise UnsupportedTransferError(f"collection holds {sensors.size()} cells, expected {events} x {n}")
+    if noise is None:
+        noise = noise_for_collection(sensors, sync=False)
+    ptype = sensors.layout.plane_address(sensors.plan.leaf("type"), 0)
+    handle = C.c_void_p(0)
+    np_ = C.c_int64(0)
+    rounds = C.c_int(0)
+    nat.call("sk_reco_run", width, height, events, p[_ENERGY], noise.ptr, ptype, p[_NOISY], dev, nat.stream(dev),
+             C.byref(handle), C.byref(np_), C.byref(rounds))
+    try:
+        m = np_.value
+        if out is None:
+            out = Collection(PARTICLE_SCHEMA, ly.PER_FIELD, memctx.ContextInfo.cuda(dev))
+        lay = out.layout
+        with lay.engine_ops():
+            out.clear()
+            lay.reserve(sc.MAIN_TAG, m)
+            lay._set_sizes_for_engine({sc.MAIN_TAG: m})
+        out._bump()
+        addr = lambda leaf, k=0: lay.plane_address(PARTICLE_PLAN.leaf(leaf), k)  # noqa: E731
+        lens = DeviceArray(m, np.int32, memctx.ContextInfo.cuda(dev))
+        offs = DeviceArray(m, np.int64, memctx.ContextInfo.cuda(dev))
+        pool = C.c_void_p(0)
+        planes4 = lambda leaf: (C.c_void_p * 4)(*[addr(leaf, k) for k in range(4)])  # noqa: E731
+        nat.call("sk_reco_write", handle, addr("energy"), addr("x"), addr("y"), addr("origin"), addr("x_variance"),
+                 addr("y_variance"), planes4("significance.value"), planes4("E_contribution.value"),
+                 planes4("noisy_count.value"), lens.ptr, offs.ptr, C.byref(pool), nat.stream(dev))
+        counts = (C.c_int64 * max(events, 1))()
+        nat.call("sk_reco_event_counts", handle, counts)
+        ncon = 25 * max(m, 1)
+        jagged.pack(out, "sensors", lens, offs, DeviceArray.wrap(pool.value or 0, ncon, np.uint64, dev))
+        lens.free()
+        offs.free()
+        out.event_counts = list(counts)[:events]
+        out.reco_rounds = rounds.value
+    finally:
+        nat.call("sk_reco_free", handle, nat.stream(dev))
+    nat.sync(dev)
+    return out
+
+
 def _calibrate_behavior(coll) -> None:
     calibrate_collection(coll)
 

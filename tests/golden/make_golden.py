@@ -188,6 +188,23 @@ def jagged() -> None:
     save("jagged.npz", **out)
 
 
+def particles() -> None:
+    """reconstruct_arrays (detector/reconstruct.py:53-136) on calibrated events,
+    including a dense event where deposit windows overlap heavily."""
+    for (w, h, seed, dens) in ((16, 16, 5, 0.01), (64, 64, 3, 0.002), (101, 37, 11, 0.004), (160, 120, 21, 0.02)):
+        ev = det.generate_event(det.EventSpec(w, h, seed=seed, particle_density=dens))
+        aos = det.HandwrittenAosPipeline()
+        aos.fill(ev)
+        aos.calibrate()
+        s = aos.sensors
+        p = det.reconstruct_arrays(s["energy"], aos.noise(), s["type"], s["calibration_data"]["noisy"], w, h)
+        save(f"particles_{w}x{h}_s{seed}.npz", w=np.int64(w), h=np.int64(h), seed=np.int64(seed),
+             density=np.float64(dens), energy=p.energy, x=p.x, y=p.y, origin=p.origin, x_variance=p.x_variance,
+             y_variance=p.y_variance, significance=p.significance, E_contribution=p.E_contribution,
+             noisy_count=p.noisy_count, sensor_lens=np.array([a.size for a in p.sensors], np.int32),
+             sensors=np.concatenate(p.sensors) if len(p.sensors) else np.empty(0, np.uint64))
+
+
 def splitmix() -> None:
     out = {}
     for seed in (0, 1, 0xDEADBEEF, (1 << 64) - 1):
@@ -202,4 +219,5 @@ if __name__ == "__main__":
     geometry()
     sensors()
     jagged()
+    particles()
     splitmix()

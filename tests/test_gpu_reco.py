@@ -1,0 +1,84 @@
+"""Particle reconstruction on the GPU vs the reference's reconstruct_arrays
+(golden particles, including a dense event with heavily overlapping deposit
+windows) and vs the oracle on batched full-size events."""
+
+import numpy as np
+import pytest
+
+import paper_2511_04853_b200 as sk
+from gpuhelp import CUDA, HOST, to_host_planes
+from oracle import restate as R
+from paper_2511_04853_b200 import layouts as ly, memctx as mc, sensor, transfer as tr
+from skhelp import golden
+
+pytestmark = pytest.mark.gpu
+
+FIELDS = ("energy", "x", "y", "origin", "x_variance", "y_variance")
+ARRAYS = ("significance", "E_contribution", "noisy_count")
+
+
+def _host_particles(coll):
+    h = sk.Collection(sensor.PARTICLE_SCHEMA, ly.PER_FIELD, HOST)
+    tr.copy_collection(h, coll)
+    out = {k: np.array(h.column(k).read()) for k in FIELDS}
+    for k in ARRAYS:
+        out[k] = np.ascontiguousarray(np.array(h.column(k).read()).T)
+    p = h.prefix_sums("sensors")
+    out["sensor_lens"] = np.diff(p.astype(np.int64)).astype(np.int32)
+    out["sensors"] = np.array(h.column("sensors").read())
+    return out
+
+
+def _compare(got, want, tag):
+    for k in FIELDS + ARRAYS + ("sensor_lens", "sensors"):
+        assert np.asarray(got[k]).tobytes() == np.asarray(want[k]).tobytes(), (tag, k)
+
+
+@pytest.mark.parametrize("name", ["particles_16x16_s5.npz", "particles_64x64_s3.npz", "particles_101x37_s11.npz",
+                                  "particles_160x120_s21.npz"])
+def test_reconstruction_matches_reference(name):
+    g = golden(name)
+    w, h = int(g["w"]), int(g["h"])
+    dev = sk.Collection(sensor.SENSOR_SCHEMA, ly.PER_FIELD, CUDA)
+    sensor.generate_events(dev, w, h, [int(g["seed"])], float(g["density"]))
+    with mc.execution_scope(mc.CUDA):
+        dev.funcs.calibrate_energy()
+    parts = sensor.reconstruct_from_collection(dev, w, h)
+    assert len(parts) == g["energy"].size and parts.event_counts == [g["energy"].size]
+    _compare(_host_particles(parts), g, name)
+
+
+def test_batched_full_size_events_vs_oracle():
+    seeds, w, h = [0, 7, 0xDEADBEEF], 436, 436
+    dev = sk.Collection(sensor.SENSOR_SCHEMA, ly.PER_FIELD, CUDA)
+    sensor.generate_events(dev, w, h, seeds, 0.002)
+    with mc.execution_scope(mc.CUDA):
+        dev.funcs.calibrate_energy()
+        e = dev.column("energy").read()
+    noise = sensor.noise_for_collection(dev).numpy()
+    planes = to_host_planes(dev)
+    typ = np.frombuffer(planes["type#0"], np.uint8)
+    noisy = np.frombuffer(planes["calibration_data.noisy#0"], np.uint8).astype(bool)
+    parts = sensor.reconstruct_from_collection(dev, w, h, events=len(seeds))
+    got = _host_particles(parts)
+    n = w * h
+    lo = 0
+    for i, _ in enumerate(seeds):
+        want = R.reconstruct(e[i * n:(i + 1) * n], noise[i * n:(i + 1) * n], typ[i * n:(i + 1) * n],
+                             noisy[i * n:(i + 1) * n], w, h)
+        m = parts.event_counts[i]
+        assert m == want["energy"].size
+        sl = {k: got[k][lo:lo + m] for k in FIELDS + ARRAYS + ("sensor_lens",)}
+        starts = np.concatenate([[0], np.cumsum(got["sensor_lens"].astype(np.int64))])
+        sl["sensors"] = got["sensors"][starts[lo]:starts[lo + m]]
+        _compare(sl, want, i)
+        lo += m
+
+
+def test_event_without_deposits_has_no_particles():
+    dev = sk.Collection(sensor.SENSOR_SCHEMA, ly.PER_FIELD, CUDA)
+    sensor.generate_events(dev, 32, 32, [3], 0.0)
+    with mc.execution_scope(mc.CUDA):
+        dev.funcs.calibrate_energy()
+    parts = sensor.reconstruct_from_collection(dev, 32, 32)
+    assert len(parts) == 0 and parts.jagged_size("sensors") == 0

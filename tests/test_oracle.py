@@ -100,3 +100,17 @@ def test_aosoa_restatement_layout():
     assert t0[16:].view(np.float32)[0] == np.float32(1.5)
     t1 = img[32:]
     assert np.array_equal(t1[:16].view(np.int32), [5, 0, 0, 0])  # tail lanes zero
+
+
+@pytest.mark.parametrize("name", ["particles_16x16_s5.npz", "particles_64x64_s3.npz", "particles_101x37_s11.npz",
+                                  "particles_160x120_s21.npz"])
+def test_reconstruction_restatement_matches_reference(name):
+    g = golden(name)
+    w, h = int(g["w"]), int(g["h"])
+    ev = R.generate_event(w, h, int(g["seed"]), float(g["density"]))
+    e = R.calibrate(ev["counts"], ev["parameter_A"], ev["parameter_B"])
+    nz = R.noise(e, ev["noise_A"], ev["noise_B"], ev["noisy"])
+    got = R.reconstruct(e, nz, ev["type"], ev["noisy"], w, h)
+    for k in ("energy", "x", "y", "origin", "x_variance", "y_variance", "significance", "E_contribution",
+              "noisy_count", "sensor_lens", "sensors"):
+        assert got[k].tobytes() == g[k].tobytes(), k
