@@ -457,7 +457,21 @@ def run_extras(args, dev: int) -> dict:
         "event_generation_ms": round(ms_gen, 3), "event_generation_cells_per_s": round(cells / ms_gen * 1e3),
         "data": "64 events 436x436, seeds 0..63, density 0.002, generated on-device (bit-exact with "
                 "detector/events.py:85-133)"}
-    for c in (a2, p2, h2, gen):
+    # the reference's second phase on the same events: reconstruct + transfer back (bench.py:180-184)
+    from paper_2511_04853_b200 import sensor as sn
+
+    sn.calibrate_collection(p2)
+    parts = sk.Collection(sensor.PARTICLE_SCHEMA, ly.PER_FIELD, cuda)
+    ms_r = timed(lambda: sn.reconstruct_from_collection(p2, 436, 436, out=parts, events=64, noise=noise),
+                 steps=3, warmup=1)
+    host_parts = sk.Collection(sensor.PARTICLE_SCHEMA, ly.PER_FIELD, mc.ContextInfo.pinned())
+    ms_rt = timed(lambda: (sn.reconstruct_from_collection(p2, 436, 436, out=parts, events=64, noise=noise),
+                           tr.copy_collection(host_parts, parts)), steps=3, warmup=1)
+    out["config2_reconstruct_64_events"] = {
+        "ms": round(ms_r, 3), "events_per_s": round(64 / ms_r * 1e3), "particles": len(parts),
+        "rounds": parts.reco_rounds, "with_transfer_back_ms": round(ms_rt, 3),
+        "note": "round-synchronous parallel greedy, same particles/order as reconstruct_arrays"}
+    for c in (a2, p2, h2, gen, parts, host_parts):
         c.free()
     noise.free()
 
