@@ -133,6 +133,15 @@ int sk_peer_enable(int device, int peer);
    `device` pulls the bytes over NVLink. Replaces _per_leaf_execute's
    per-leaf gather + staging (transfer.py:182-233). */
 int sk_convert(const sk_conv_desc* desc, int device, uintptr_t stream);
+/* CUDA-graph capture of the device's library stream: everything enqueued on
+   it (and on the pipeline's helper streams) between begin and end -- e.g. a
+   whole transfer with its chunked copies and conversion launches -- becomes
+   one executable graph replayed with a single launch. Operations that cannot
+   be captured (pageable-host copies, synchronisation) make end fail. */
+int sk_capture_begin(int device);
+int sk_capture_end(int device, void** graph_exec);
+int sk_graph_launch(void* graph_exec, int device);
+int sk_graph_destroy(void* graph_exec);
 /* Diagnostic: generate the record-signature-specialised transform the engine
    would JIT (NVRTC) for `desc` (epi_fields: the 7 sensor field indices of the
    fused case-study path, or NULL), copy its source to source_out, and compile

@@ -58,11 +58,13 @@ from .schema import (
 )
 from .transfer import (
     ExternalBinding,
+    PreparedTransfer,
     TransferPriority,
     copy_collection,
     export_external,
     import_external,
     move_collection,
+    prepare,
     register_transfer,
 )
 

@@ -93,6 +93,10 @@ _SIGNATURES = {
     "sk_convert_plan": [C.POINTER(ConvDesc), _I, C.POINTER(_I), C.POINTER(_I), C.POINTER(_I), C.POINTER(_SZ),
                         C.POINTER(_I)],
     "sk_convert_specialize_check": [C.POINTER(ConvDesc), C.POINTER(_I), C.c_char_p, _SZ, C.POINTER(_SZ)],
+    "sk_capture_begin": [_I],
+    "sk_capture_end": [_I, C.POINTER(_P)],
+    "sk_graph_launch": [_P, _I],
+    "sk_graph_destroy": [_P],
     "sk_jagged_scratch_bytes": [_I64, C.POINTER(_SZ)],
     "sk_jagged_scan": [_I64, _P, _I, _P, _I, _P, _SZ, _P, _U],
     "sk_jagged_scatter": [_I64, _P, _I, _P, _P, _I64, _I, C.POINTER(_I64), C.POINTER(C.c_int32), C.POINTER(_P),

@@ -576,8 +576,10 @@ int run(const sk_conv_desc& d, int device, cudaStream_t s, int epi, float* extra
   }
   // the helper streams start after everything already queued on s
   SK_TRY(cudaEventRecord(start, s));
-  SK_TRY(cudaStreamWaitEvent(ds->copy_in, start, 0));
-  SK_TRY(cudaStreamWaitEvent(ds->copy_out, start, 0));
+  // fork only the helper streams that get work (an idle fork would be an
+  // unjoined stream inside a CUDA-graph capture)
+  if (sh) SK_TRY(cudaStreamWaitEvent(ds->copy_in, start, 0));
+  if (dh) SK_TRY(cudaStreamWaitEvent(ds->copy_out, start, 0));
   const int64_t nchunks = (d.n + C - 1) / C;
   for (int64_t k = 0; k < nchunks; ++k) {
     const int slot = static_cast<int>(k % NSLOT);

@@ -394,3 +394,48 @@ extern "C" int sk_fill_random(void* dst, size_t nbytes, uint64_t seed, uint64_t 
   SK_TRY(cudaGetLastError());
   return SK_OK;
 }
+
+// ---- CUDA graphs: capture the library stream, replay with one launch -------------------
+
+extern "C" {
+
+int sk_capture_begin(int device) {
+  DeviceState* d = nullptr;
+  int rc = device_state(device, &d);
+  if (rc) return rc;
+  SK_TRY(cudaStreamBeginCapture(d->stream, cudaStreamCaptureModeThreadLocal));
+  return SK_OK;
+}
+
+int sk_capture_end(int device, void** graph_exec) {
+  DeviceState* d = nullptr;
+  int rc = device_state(device, &d);
+  if (rc) return rc;
+  cudaGraph_t g = nullptr;
+  cudaError_t e = cudaStreamEndCapture(d->stream, &g);
+  if (e != cudaSuccess) {
+    if (g) cudaGraphDestroy(g);
+    return cuda_fail(e, "cudaStreamEndCapture (an operation in the region cannot be captured)");
+  }
+  cudaGraphExec_t x = nullptr;
+  e = cudaGraphInstantiate(&x, g, 0);
+  cudaGraphDestroy(g);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate");
+  *graph_exec = x;
+  return SK_OK;
+}
+
+int sk_graph_launch(void* graph_exec, int device) {
+  DeviceState* d = nullptr;
+  int rc = device_state(device, &d);
+  if (rc) return rc;
+  SK_TRY(cudaGraphLaunch(static_cast<cudaGraphExec_t>(graph_exec), d->stream));
+  return SK_OK;
+}
+
+int sk_graph_destroy(void* graph_exec) {
+  if (graph_exec) SK_TRY(cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(graph_exec)));
+  return SK_OK;
+}
+
+}  // extern "C"

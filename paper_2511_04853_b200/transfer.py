@@ -25,6 +25,7 @@ There is no CPU conversion path: a conversion without a usable B200 raises.
 
 from __future__ import annotations
 
+import ctypes as C
 import itertools
 from dataclasses import dataclass, field
 from enum import IntEnum
@@ -227,6 +228,71 @@ def _planes_execute(dst: Collection, src: Collection, opts: Mapping[str, Any] | 
     _match_sizes(dst, src)
     _copy_planes(dst, src, src.plan.leaves, {"async": True})
     _sync(dst, src, opts)
+
+
+# ---- prepared transfers: one CUDA-graph launch per repeat ---------------------------------------
+
+class PreparedTransfer:
+    """copy_collection(dst, src) captured once into a CUDA graph.
+
+    For transfers repeated between the same two collections (a serving loop,
+    per-event staging), the host-side work (spec resolution, descriptor and
+    plan, per-chunk copy calls of the host pipeline) is paid once. run()
+    replays the whole transfer with one graph launch. The capture runs the
+    transfer once eagerly first (allocations, NVRTC, staging), so the graph
+    holds only stream work. Valid while neither collection changes size or
+    storage; pageable-host endpoints cannot be captured (use pinned)."""
+
+    def __init__(self, dst: Collection, src: Collection) -> None:
+        self.dst, self.src = dst, src
+        self.spec = copy_collection(dst, src)  # eager warm-up; also resolves the spec
+        self.device = _engine_device(dst, src)
+        for dev in {dst.device, src.device, self.device} - {None}:
+            nat.sync(dev)
+        spec = _specs[self.spec]
+        nat.call("sk_capture_begin", self.device)
+        graph = C.c_void_p(0)
+        try:
+            spec.execute(dst, src, {"async": True})
+        finally:
+            nat.check(nat.lib().sk_capture_end(self.device, C.byref(graph)), "sk_capture_end")
+        self.graph = graph.value
+        self._geometry = (_geometry(dst), _geometry(src))
+
+    def run(self, sync: bool = True) -> str:
+        if self.graph is None:
+            raise TransferError("prepared transfer is closed")
+        if (_geometry(self.dst), _geometry(self.src)) != self._geometry:
+            raise TransferError("prepared transfer is stale: a collection changed size or storage")
+        nat.call("sk_graph_launch", self.graph, self.device)
+        self.dst._bump()
+        if sync:
+            nat.sync(self.device)
+        return self.spec
+
+    def close(self) -> None:
+        if self.graph:
+            nat.call("sk_graph_destroy", self.graph)
+            self.graph = None
+
+    def __del__(self) -> None:  # pragma: no cover - interpreter teardown order
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _geometry(c: Collection) -> tuple:
+    """What a captured graph bakes in: sizes, buffer addresses, capacities."""
+    lay = c.layout
+    return (tuple(lay._sizes.items()),
+            tuple((b.ptr, b.length_bytes) for b in lay.buffers()),
+            tuple(lay._caps.values()))
+
+
+def prepare(dst: Collection, src: Collection) -> PreparedTransfer:
+    """Capture copy_collection(dst, src) as a CUDA graph for cheap repeats."""
+    return PreparedTransfer(dst, src)
 
 
 # ---- external record import/export (transfer.py:246-346) ---------------------------------------
