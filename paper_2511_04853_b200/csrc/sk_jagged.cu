@@ -1,12 +1,28 @@
-// Jagged-collection packer (K4): single-pass exclusive prefix sum with
-// decoupled look-back, then a load-balanced gather of variable-length member
-// lists into packed per-field pools.
+// Jagged-collection packer (K4): exclusive prefix sum of the lengths, then a
+// load-balanced gather of variable-length member lists into packed per-field
+// pools.
 //
 // Reference: Collection.jagged_fill (collection.py:537-556) computes
 // pv[1:] = np.cumsum(lengths, int64).astype(index dtype) and
 // np.concatenate(segments); import_external (transfer.py:297-320) does the same
 // for multi-leaf members. Both walk the segments in a Python loop.
+//
+// Scan: tiles of 4096 lengths. Up to SCAN_DIRECT_TILES tiles it is
+// reduce-then-scan (tile sums, then every tile adds up its predecessors' sums
+// in parallel: no inter-CTA waiting at all); beyond that a single-pass
+// decoupled look-back. In pack mode the scan also emits the gather's work
+// split: starts[w] = the record holding member w*W, and 1 + the last non-empty
+// record.
+//
+// Gather: one warp per W = 256 consecutive output members, no block barriers.
+// The warp loads its record window (<= 32 records per batch, one per lane),
+// ranks the non-empty ones with ballot/popc and marks where each starts with
+// redux.or bitmasks; member j's record is then a popc away and its source is
+// j + (src_off[c] - P[c]). The next window's loads are in flight while this
+// window's members are.
 #include <algorithm>
+#include <cstdlib>
+#include <utility>
 
 #include "sk_internal.cuh"
 
@@ -16,6 +32,12 @@ namespace jag {
 constexpr int SCAN_NT = 256;
 constexpr int SCAN_IT = 16;
 constexpr int SCAN_TILE = SCAN_NT * SCAN_IT;  // 4096 lengths per CTA
+constexpr int64_t SCAN_DIRECT_TILES = 4096;   // reduce-then-scan up to 16.7M records
+
+constexpr int W = 256;          // output members per warp task (= the boundary pitch)
+constexpr int W_CH = W / 32;    // 32-member chunks per task
+constexpr int G_NT = 256;       // gather threads per CTA
+constexpr int G_MAXF = 8;
 
 constexpr uint64_t FLAG_A = 1ull << 62;  // tile aggregate published
 constexpr uint64_t FLAG_P = 2ull << 62;  // inclusive prefix published
@@ -55,20 +77,32 @@ __device__ __forceinline__ void st_release(uint64_t* p, uint64_t v) {
 // consecutive reads at a 2-way (64-bit) bank pattern
 __device__ __forceinline__ int pad(int e) { return e + (e >> 4); }
 
-__global__ void __launch_bounds__(SCAN_NT) scan_kernel(int64_t n, const void* __restrict__ lens, int lens_type,
-                                                       void* __restrict__ out, int out_type, uint64_t* status,
-                                                       unsigned int* ticket, int64_t* total_out,
-                                                       int64_t* __restrict__ out64) {
-  __shared__ int64_t s[SCAN_TILE + SCAN_TILE / 16];
-  __shared__ int64_t warp_tot[SCAN_NT / 32];
-  __shared__ int64_t s_excl;
-  __shared__ unsigned int s_tile;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid == 0) s_tile = atomicAdd(ticket, 1u);  // dynamic tile order: look-back never waits on an unscheduled CTA
-  __syncthreads();
-  const int64_t tile = s_tile;
-  const int64_t base = tile * SCAN_TILE;
+// programmatic dependent launch: the next kernel of the chain may be scheduled
+// now (its CTAs park in pdl_wait until this grid has completed and flushed)
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
+struct ScanOut {
+  void* out;                 // prefix, index dtype, n + 1 entries
+  int out_type;
+  int64_t* total;            // device total (optional)
+  int64_t* out64;            // non-wrapped int64 copy of the prefix (optional)
+  int64_t* starts;           // pack mode: starts[w] = record holding member w*W
+  int64_t nstarts;
+  unsigned long long* last;  // pack mode: atomicMax of 1 + non-empty record index
+};
+
+struct TileScan {
+  int64_t loc[SCAN_IT];  // inclusive scan of this thread's 16 consecutive lengths
+  int64_t thread_excl;   // exclusive prefix of this thread within the tile
+  int64_t agg;           // tile total
+};
+
+// lengths of tile `tile` -> smem, per-thread and block-wide scans
+__device__ __forceinline__ void tile_scan(int64_t n, const void* lens, int lens_type, int64_t tile, int64_t* s,
+                                          int64_t* warp_tot, TileScan& ts) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t base = tile * SCAN_TILE;
 #pragma unroll
   for (int i = 0; i < SCAN_IT; ++i) {
     const int e = i * SCAN_NT + tid;
@@ -76,14 +110,12 @@ __global__ void __launch_bounds__(SCAN_NT) scan_kernel(int64_t n, const void* __
     s[pad(e)] = idx < n ? load_int(lens, lens_type, idx) : 0;
   }
   __syncthreads();
-  int64_t loc[SCAN_IT];
   int64_t acc = 0;
 #pragma unroll
   for (int i = 0; i < SCAN_IT; ++i) {
     acc += s[pad(tid * SCAN_IT + i)];
-    loc[i] = acc;
+    ts.loc[i] = acc;
   }
-  // block-wide exclusive scan of the per-thread totals
   int64_t x = acc;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -98,14 +130,121 @@ __global__ void __launch_bounds__(SCAN_NT) scan_kernel(int64_t n, const void* __
     if (w < warp) warp_off += warp_tot[w];
     agg += warp_tot[w];
   }
-  const int64_t thread_excl = warp_off + x - acc;
+  ts.thread_excl = warp_off + x - acc;
+  ts.agg = agg;
+}
 
-  if (warp == 0) {
+// tile exclusive prefix known: write P[base+1 .. base+4096], the boundaries and the last non-empty record
+__device__ __forceinline__ void tile_write(int64_t n, int64_t tile, int64_t tile_excl, const TileScan& ts, int64_t* s,
+                                           const ScanOut& O) {
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int64_t base = tile * SCAN_TILE;
+  const int64_t off = tile_excl + ts.thread_excl;
+  __syncthreads();  // everyone has read the lengths out of s
+#pragma unroll
+  for (int i = 0; i < SCAN_IT; ++i) s[pad(tid * SCAN_IT + i)] = off + ts.loc[i];
+  __syncthreads();
+  int64_t last = -1;
+#pragma unroll
+  for (int i = 0; i < SCAN_IT; ++i) {
+    const int e = i * SCAN_NT + tid;
+    const int64_t idx = base + e;
+    if (idx < n) {
+      const int64_t v = s[pad(e)];
+      store_int(O.out, O.out_type, idx + 1, v);
+      if (O.out64) O.out64[idx + 1] = v;
+      if (idx == n - 1 && O.total) *O.total = v;
+      if (O.starts) {
+        const int64_t pv = e ? s[pad(e - 1)] : tile_excl;
+        if (v > pv) {
+          last = idx;
+          const int64_t w1 = min((v - 1) / W, O.nstarts - 1);
+          for (int64_t w = (pv + W - 1) / W; w <= w1; ++w) O.starts[w] = idx;
+        }
+      }
+    }
+  }
+  if (O.starts) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) last = max(last, __shfl_xor_sync(0xffffffffu, last, o));
+    if (lane == 0 && last >= 0) atomicMax(O.last, static_cast<unsigned long long>(last + 1));
+  }
+  if (tile == 0 && tid == 0) {
+    store_int(O.out, O.out_type, 0, 0);
+    if (O.out64) O.out64[0] = 0;
+  }
+}
+
+// reduce-then-scan, pass 1: tile sums
+__global__ void __launch_bounds__(SCAN_NT) tile_sum_kernel(int64_t n, const void* __restrict__ lens, int lens_type,
+                                                           int64_t* __restrict__ agg, unsigned long long* last) {
+  __shared__ int64_t red[SCAN_NT / 32];
+  pdl_trigger();
+  const int tid = threadIdx.x;
+  const int64_t base = static_cast<int64_t>(blockIdx.x) * SCAN_TILE;
+  int64_t acc = 0;
+#pragma unroll
+  for (int i = 0; i < SCAN_IT; ++i) {
+    const int64_t idx = base + i * SCAN_NT + tid;
+    if (idx < n) acc += load_int(lens, lens_type, idx);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((tid & 31) == 0) red[tid >> 5] = acc;
+  __syncthreads();
+  if (tid == 0) {
+    int64_t t = 0;
+#pragma unroll
+    for (int w = 0; w < SCAN_NT / 32; ++w) t += red[w];
+    agg[blockIdx.x] = t;
+    if (blockIdx.x == 0 && last) *last = 0;
+  }
+}
+
+// reduce-then-scan, pass 2: each tile sums its predecessors' totals in parallel, then scans itself
+__global__ void __launch_bounds__(SCAN_NT) tile_apply_kernel(int64_t n, const void* __restrict__ lens, int lens_type,
+                                                             const int64_t* __restrict__ agg, const ScanOut O) {
+  __shared__ int64_t s[SCAN_TILE + SCAN_TILE / 16];
+  __shared__ int64_t warp_tot[SCAN_NT / 32];
+  __shared__ int64_t red[SCAN_NT / 32];
+  const int tid = threadIdx.x;
+  const int64_t tile = blockIdx.x;
+  pdl_wait();
+  pdl_trigger();
+  int64_t pre = 0;
+  for (int64_t k = tid; k < tile; k += SCAN_NT) pre += agg[k];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) pre += __shfl_xor_sync(0xffffffffu, pre, o);
+  if ((tid & 31) == 0) red[tid >> 5] = pre;
+  TileScan ts;
+  tile_scan(n, lens, lens_type, tile, s, warp_tot, ts);  // its barriers also publish red[]
+  int64_t excl = 0;
+#pragma unroll
+  for (int w = 0; w < SCAN_NT / 32; ++w) excl += red[w];
+  tile_write(n, tile, excl, ts, s, O);
+}
+
+// single pass with decoupled look-back (large n): tiles in ticket order, warp 0
+// looks back over 32 predecessors per round
+__global__ void __launch_bounds__(SCAN_NT) scan_lookback_kernel(int64_t n, const void* __restrict__ lens,
+                                                                int lens_type, uint64_t* status, unsigned int* ticket,
+                                                                const ScanOut O) {
+  __shared__ int64_t s[SCAN_TILE + SCAN_TILE / 16];
+  __shared__ int64_t warp_tot[SCAN_NT / 32];
+  __shared__ int64_t s_excl;
+  __shared__ unsigned int s_tile;
+  const int tid = threadIdx.x, lane = tid & 31;
+  if (tid == 0) s_tile = atomicAdd(ticket, 1u);  // dynamic tile order: look-back never waits on an unscheduled CTA
+  __syncthreads();
+  const int64_t tile = s_tile;
+  TileScan ts;
+  tile_scan(n, lens, lens_type, tile, s, warp_tot, ts);
+  if (tid < 32) {
     int64_t excl = 0;
     if (tile == 0) {
-      if (lane == 0) st_release(&status[0], FLAG_P | (static_cast<uint64_t>(agg) & VAL_MASK));
+      if (lane == 0) st_release(&status[0], FLAG_P | (static_cast<uint64_t>(ts.agg) & VAL_MASK));
     } else {
-      if (lane == 0) st_release(&status[tile], FLAG_A | (static_cast<uint64_t>(agg) & VAL_MASK));
+      if (lane == 0) st_release(&status[tile], FLAG_A | (static_cast<uint64_t>(ts.agg) & VAL_MASK));
       int64_t end = tile - 1;  // look back over [end-31, end]
       while (true) {
         const int64_t idx = end - lane;
@@ -125,39 +264,15 @@ __global__ void __launch_bounds__(SCAN_NT) scan_kernel(int64_t n, const void* __
         if (pmask) break;
         end -= 32;
       }
-      if (lane == 0) st_release(&status[tile], FLAG_P | (static_cast<uint64_t>(excl + agg) & VAL_MASK));
+      if (lane == 0) st_release(&status[tile], FLAG_P | (static_cast<uint64_t>(excl + ts.agg) & VAL_MASK));
     }
     if (lane == 0) s_excl = excl;
   }
   __syncthreads();
-  const int64_t off = s_excl + thread_excl;
-#pragma unroll
-  for (int i = 0; i < SCAN_IT; ++i) s[pad(tid * SCAN_IT + i)] = off + loc[i];
-  __syncthreads();
-#pragma unroll
-  for (int i = 0; i < SCAN_IT; ++i) {
-    const int e = i * SCAN_NT + tid;
-    const int64_t idx = base + e;
-    if (idx < n) {
-      const int64_t v = s[pad(e)];
-      store_int(out, out_type, idx + 1, v);
-      if (out64) out64[idx + 1] = v;  // non-wrapped copy for the gather
-      if (idx == n - 1 && total_out) *total_out = v;
-    }
-  }
-  if (tile == 0 && tid == 0) {
-    store_int(out, out_type, 0, 0);
-    if (out64) out64[0] = 0;
-  }
+  tile_write(n, tile, s_excl, ts, s, O);
 }
 
-// ---- scatter ------------------------------------------------------------------------
-
-constexpr int SC_NT = 256;
-constexpr int SC_IT = 8;
-constexpr int SC_TILE = SC_NT * SC_IT;  // output members per CTA
-constexpr int SC_CMAX = 1024;           // records staged in smem per CTA
-constexpr int SC_MAXF = 8;
+// ---- gather -------------------------------------------------------------------------
 
 struct ScatterArgs {
   int64_t n;
@@ -168,27 +283,19 @@ struct ScatterArgs {
   int64_t member_stride;
   int64_t total;             // members to gather, or the capacity bound when total_dev is set
   const int64_t* total_dev;  // device-resident total (fused pack): gather min(*total_dev, total)
+  const int64_t* starts;     // starts[w] = record holding member w*W
+  const unsigned long long* last_rec;  // 1 + last non-empty record
   int nfields;
-  int aligned;  // all member fields naturally aligned
-  int64_t field_off[SC_MAXF];
-  int32_t field_size[SC_MAXF];
-  uint8_t* dst[SC_MAXF];
+  int64_t field_off[G_MAXF];
+  int32_t field_size[G_MAXF];
+  int32_t aligned[G_MAXF];   // naturally aligned source field: one load per member
+  uint8_t* dst[G_MAXF];
 };
 
-// last record c in [lo, hi) with prefix[c] <= j
-__device__ __forceinline__ int64_t search_global(const ScatterArgs& A, int64_t lo, int64_t hi, int64_t j) {
-  while (hi - lo > 1) {
-    const int64_t mid = (lo + hi) >> 1;
-    if (load_int(A.prefix, A.prefix_type, mid) <= j) lo = mid;
-    else hi = mid;
-  }
-  return lo;
-}
-
-// Same answer as search_global, found by a whole warp: each round the 32
-// lanes probe 32 evenly spaced records and keep the sub-range after the last
-// probe that is <= j, so 1M records need 4 rounds of parallel loads instead
-// of 20 dependent ones. All lanes return the result.
+// Same answer as a binary search for the last record c in [lo, hi) with
+// prefix[c] <= j, found by a whole warp: each round the 32 lanes probe 32
+// evenly spaced records and keep the sub-range after the last probe that is
+// <= j (4 rounds of parallel loads for 1M records). All lanes return it.
 __device__ __forceinline__ int64_t search_warp(const ScatterArgs& A, int64_t lo, int64_t hi, int64_t j) {
   const int lane = threadIdx.x & 31;
   while (hi - lo > 32) {
@@ -239,117 +346,294 @@ __device__ __forceinline__ int64_t eff_total(const ScatterArgs& A) {
   return t <= A.total ? t : 0;
 }
 
-// one padding word per 32 keeps both the consecutive-per-thread scan reads and
-// the strided member reads at <= 2-way bank conflicts
-__device__ __forceinline__ int cpad(int e) { return e + (e >> 5); }
-
-// first record of every member tile: starts[b] = last record c with
-// prefix[c] <= b * SC_TILE (one warp per tile, all tiles in parallel), and
-// starts[ntiles] = the last record holding a member.
-__global__ void __launch_bounds__(256) tile_start_kernel(const __grid_constant__ ScatterArgs A, int64_t* starts,
-                                                         int64_t ntiles) {
-  const int64_t b = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
-  if (b > ntiles) return;
+// work split for a prefix computed elsewhere (sk_jagged_scatter):
+// starts[w] = last record c with prefix[c] <= w*W (one warp per task), and
+// starts[ntasks] = 1 + the record holding the last member (last_rec form).
+__global__ void __launch_bounds__(256) task_start_kernel(const __grid_constant__ ScatterArgs A, int64_t* starts,
+                                                         int64_t ntasks) {
+  pdl_trigger();
+  const int64_t w = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+  if (w > ntasks) return;
   const int64_t T = eff_total(A);
   if (T <= 0) return;
-  const int64_t j = b * SC_TILE < T ? b * SC_TILE : T - 1;
+  const int64_t j = w < ntasks ? w * W : T - 1;
   const int64_t c = search_warp(A, 0, A.n, j);
-  if ((threadIdx.x & 31) == 0) starts[b] = c;
+  if ((threadIdx.x & 31) == 0) starts[w] = w < ntasks ? c : c + 1;
 }
 
-__global__ void __launch_bounds__(SC_NT) scatter_kernel(const __grid_constant__ ScatterArgs A,
-                                                        const int64_t* __restrict__ starts) {
-  __shared__ int64_t sP[SC_CMAX + 1];
-  __shared__ int64_t sOff[SC_CMAX];
-  __shared__ int32_t sCl[SC_TILE + SC_TILE / 32];  // member -> record (relative), padded
-  __shared__ int32_t sWarpMax[SC_NT / 32];
-  const int tid = threadIdx.x;
-  const int64_t j0 = static_cast<int64_t>(blockIdx.x) * SC_TILE;
+// one lane per record of a window batch: P[c], P[c+1], src_off[c], loaded
+// unconditionally from a clamped (always valid) index and kept in the raw
+// prefix type, so nothing consumes them before rank time (a predicated load
+// merged with defaults would make the compiler wait for it right away)
+template <class PT>
+struct RecBatch {
+  PT p, pn;
+  int64_t off;
+  int64_t c;  // unclamped record index: valid when c <= hi
+};
+
+template <class PT>
+__device__ __forceinline__ RecBatch<PT> load_batch(const ScatterArgs& A, int64_t c, int64_t hi) {
+  const PT* P = static_cast<const PT*>(A.prefix);
+  const int64_t cc = max(min(c, hi), static_cast<int64_t>(0));
+  RecBatch<PT> r;
+  r.p = P[cc];
+  r.pn = P[cc + 1];
+  r.off = A.src_off[cc];
+  r.c = c;
+  return r;
+}
+
+__device__ __forceinline__ void task_window(const ScatterArgs& A, int64_t t, int64_t T, int64_t& lo, int64_t& hi) {
+  lo = A.starts[t];
+  hi = (t + 1) * W < T ? A.starts[t + 1] : static_cast<int64_t>(*A.last_rec) - 1;
+}
+
+// rank the batch's non-empty records (sD[rank] = src_off - P) and mark where each starts
+template <class PT>
+__device__ __forceinline__ void rank_batch(const RecBatch<PT>& r, int64_t hi, int64_t j0, int64_t j1, int64_t* sD,
+                                           int& nr, unsigned (&masks)[W_CH]) {
+  const int lane = threadIdx.x & 31;
+  const int64_t p = static_cast<int64_t>(r.p), pn = static_cast<int64_t>(r.pn);
+  const bool ne = r.c <= hi && pn > p && p < j1;
+  const unsigned bal = __ballot_sync(0xffffffffu, ne);
+  const int rank = nr + __popc(bal & ((1u << lane) - 1u));
+  nr += __popc(bal);
+  const int s = ne ? static_cast<int>(max(p - j0, static_cast<int64_t>(0))) : -1;
+  if (ne) sD[rank] = r.off - p;
+#pragma unroll
+  for (int k = 0; k < W_CH; ++k)
+    masks[k] |= __reduce_or_sync(0xffffffffu, (s >> 5) == k ? 1u << (s & 31) : 0u);
+}
+
+template <int MS>
+struct MemberWord;
+template <>
+struct MemberWord<4> {
+  using T = uint32_t;
+};
+template <>
+struct MemberWord<8> {
+  using T = uint64_t;
+};
+
+// PT: prefix element type. MS: 4 or 8 = one naturally aligned member field of
+// that size (straight-line loads/stores); 0 = the generic field table.
+template <class PT, int MS>
+__global__ void __launch_bounds__(G_NT) gather_kernel(const __grid_constant__ ScatterArgs A) {
+  __shared__ int64_t sD_all[G_NT / 32][W];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int64_t* sD = sD_all[warp];
+  pdl_wait();
   const int64_t T = eff_total(A);
-  if (j0 >= T) return;
-  const int64_t j1 = min(j0 + SC_TILE, T);
-  // the records covering [j0, j1) lie in [starts[b], starts[b+1]]
-  const int64_t lo = starts[blockIdx.x];
-  const int64_t cnt = starts[blockIdx.x + 1] - lo + 1;
-  const bool staged = cnt <= SC_CMAX;
-  if (staged) {
-    for (int k = tid; k <= cnt; k += SC_NT) {
-      sP[k] = load_int(A.prefix, A.prefix_type, lo + k);
-      if (k < cnt) sOff[k] = A.src_off[lo + k];
+  const int64_t ntasks = (T + W - 1) / W;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * (G_NT / 32);
+  int64_t t = static_cast<int64_t>(blockIdx.x) * (G_NT / 32) + warp;
+  if (t >= ntasks) return;
+  const unsigned le_mask = 0xffffffffu >> (31 - lane);
+
+  int64_t lo, hi;
+  task_window(A, t, T, lo, hi);
+  RecBatch<PT> cur = load_batch<PT>(A, lo + lane, hi);
+  int64_t nlo, nhi;
+  task_window(A, min(t + stride, ntasks - 1), T, nlo, nhi);
+
+  while (true) {
+    const int64_t j0 = t * W;
+    const int64_t j1 = min(j0 + W, T);
+    unsigned masks[W_CH];
+#pragma unroll
+    for (int k = 0; k < W_CH; ++k) masks[k] = 0;
+    int nr = 0;
+    rank_batch(cur, hi, j0, j1, sD, nr, masks);
+    for (int64_t c0 = lo + 32; c0 <= hi; c0 += 32)
+      rank_batch(load_batch<PT>(A, c0 + lane, hi), hi, j0, j1, sD, nr, masks);
+    __syncwarp();
+    // next task's window first: its loads fly together with this task's members
+    const int64_t tn = t + stride;
+    const bool more = tn < ntasks;
+    // unconditional (clamped) prefetches: nothing waits on them before the next task
+    const RecBatch<PT> nxt = load_batch<PT>(A, nlo + lane, nhi);
+    int64_t nnlo, nnhi;
+    task_window(A, min(tn + stride, ntasks - 1), T, nnlo, nnhi);
+    // source element of each of this lane's members (chunk k: member j0 + 32k + lane)
+    int64_t src[W_CH];
+    int cum = 0;
+#pragma unroll
+    for (int k = 0; k < W_CH; ++k) {
+      const int64_t j = j0 + 32 * k + lane;
+      const int r = cum + __popc(masks[k] & le_mask) - 1;
+      src[k] = j < j1 ? j + sD[r] : -1;
+      cum += __popc(masks[k]);
     }
-  }
-  __syncthreads();
-  if (staged) {
-    // record of every member of the tile: mark where each non-empty record
-    // starts, then an inclusive max-scan carries the index forward
-    const int m = static_cast<int>(j1 - j0);
-    for (int e = tid; e < SC_TILE; e += SC_NT) sCl[cpad(e)] = 0;
-    __syncthreads();
-    for (int k = tid + 1; k < cnt; k += SC_NT) {
-      const int64_t s = sP[k] - j0;
-      if (s > 0 && s < m && sP[k + 1] > sP[k]) sCl[cpad(static_cast<int>(s))] = k;
-    }
-    __syncthreads();
-    int vals[SC_IT];
-    int run = 0;
+    if constexpr (MS != 0) {
+      using V = typename MemberWord<MS>::T;
+      const uint8_t* sp = A.src_pool + A.field_off[0];
+      V* dp = reinterpret_cast<V*>(A.dst[0]);
+      V v[W_CH];
 #pragma unroll
-    for (int i = 0; i < SC_IT; ++i) {
-      run = max(run, sCl[cpad(tid * SC_IT + i)]);
-      vals[i] = run;
-    }
-    int x = run;  // warp-inclusive max of the per-thread maxima
+      for (int k = 0; k < W_CH; ++k)
+        v[k] = src[k] >= 0 ? *reinterpret_cast<const V*>(sp + src[k] * A.member_stride) : V(0);
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) x = max(x, __shfl_up_sync(0xffffffffu, x, o));
-    if ((tid & 31) == 31) sWarpMax[tid >> 5] = x;
-    const int excl_lane = __shfl_up_sync(0xffffffffu, x, 1);
-    __syncthreads();
-    int carry = (tid & 31) ? excl_lane : 0;
-    for (int w = 0; w < (tid >> 5); ++w) carry = max(carry, sWarpMax[w]);
+      for (int k = 0; k < W_CH; ++k)
+        if (src[k] >= 0) dp[j0 + 32 * k + lane] = v[k];
+    } else {
+      for (int f = 0; f < A.nfields; ++f) {
+        const int isz = A.field_size[f];
+        const bool al = A.aligned[f];
+        const uint8_t* sp = A.src_pool + A.field_off[f];
+        uint8_t* dp = A.dst[f];
+        uint64_t v[W_CH];
 #pragma unroll
-    for (int i = 0; i < SC_IT; ++i) sCl[cpad(tid * SC_IT + i)] = max(vals[i], carry);
-    __syncthreads();
-  }
-  // resolve the source element of each of this thread's members first, then move
-  int64_t src[SC_IT];
+        for (int k = 0; k < W_CH; ++k)
+          v[k] = src[k] >= 0 ? load_member(sp + src[k] * A.member_stride, isz, al) : 0;
 #pragma unroll
-  for (int i = 0; i < SC_IT; ++i) {
-    const int64_t j = j0 + i * SC_NT + tid;
-    src[i] = -1;
-    if (j < j1) {
-      int64_t c, pc, oc;
-      if (staged) {
-        const int a = sCl[cpad(i * SC_NT + tid)];
-        pc = sP[a];
-        oc = sOff[a];
-      } else {
-        c = search_global(A, lo, lo + cnt, j);
-        pc = load_int(A.prefix, A.prefix_type, c);
-        oc = A.src_off[c];
+        for (int k = 0; k < W_CH; ++k)
+          if (src[k] >= 0) store_member(dp + (j0 + 32 * k + lane) * isz, v[k], isz);
       }
-      src[i] = oc + (j - pc);
     }
+    if (!more) break;
+    __syncwarp();  // sD is rewritten for the next task
+    t = tn;
+    lo = nlo;
+    hi = nhi;
+    cur = nxt;
+    nlo = nnlo;
+    nhi = nnhi;
   }
-  const bool al = A.aligned;
-  for (int f = 0; f < A.nfields; ++f) {
-    const int isz = A.field_size[f];
-    const uint8_t* sp = A.src_pool + A.field_off[f];
-    uint8_t* dp = A.dst[f];
-    uint64_t v[SC_IT];
-#pragma unroll
-    for (int i = 0; i < SC_IT; ++i)
-      v[i] = src[i] >= 0 ? load_member(sp + src[i] * A.member_stride, isz, al) : 0;
-#pragma unroll
-    for (int i = 0; i < SC_IT; ++i) {
-      const int64_t j = j0 + i * SC_NT + tid;
-      if (src[i] >= 0) store_member(dp + j * isz, v[i], isz);
+}
+
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+template <int MS>
+__device__ __forceinline__ void cp_async_member(void* s, const void* g) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(smem_u32(s)), "l"(g), "n"(MS) : "memory");
+}
+
+constexpr int GA_WARPS = 8;  // warps per CTA of the async gather
+
+// Async gather for one naturally aligned 4/8-byte member field with a
+// 16-byte aligned destination pool. Members go global -> shared with cp.async
+// (no registers held per load in flight) into a per-warp double buffer, and
+// each task's 256 contiguous output members leave in ONE bulk (TMA) store, so
+// every warp keeps two tasks of loads in flight while the previous task drains.
+template <class PT, int MS>
+__global__ void __launch_bounds__(GA_WARPS * 32) gather_async_kernel(const __grid_constant__ ScatterArgs A) {
+  __shared__ __align__(128) uint8_t stage_all[GA_WARPS][2][W * MS];
+  __shared__ int64_t sD_all[GA_WARPS][W];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int64_t* sD = sD_all[warp];
+  pdl_wait();
+  const int64_t T = eff_total(A);
+  const int64_t ntasks = (T + W - 1) / W;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * GA_WARPS;
+  int64_t t = static_cast<int64_t>(blockIdx.x) * GA_WARPS + warp;
+  if (t >= ntasks) return;
+  const unsigned le_mask = 0xffffffffu >> (31 - lane);
+  const uint8_t* sp = A.src_pool + A.field_off[0];
+  uint8_t* dp = A.dst[0];
+
+  // record windows run two tasks ahead of the member loads: (lo0, hi0, b0) is
+  // this task, (lo1, hi1, b1) the next one (batch in flight), (lo2, hi2) the
+  // one after (starts only)
+  // (prefetches past the last task read clamped, valid entries and are never used)
+  int64_t lo0, hi0, lo1, hi1, lo2, hi2;
+  task_window(A, t, T, lo0, hi0);
+  RecBatch<PT> b0 = load_batch<PT>(A, lo0 + lane, hi0);
+  task_window(A, min(t + stride, ntasks - 1), T, lo1, hi1);
+  RecBatch<PT> b1 = load_batch<PT>(A, lo1 + lane, hi1);
+  task_window(A, min(t + 2 * stride, ntasks - 1), T, lo2, hi2);
+
+  // drains task `pt` from buffer `pb`: bulk store of the 16-byte body, lanes store the tail
+  auto drain = [&](int64_t pt, int pb) {
+    const int64_t pj0 = pt * W;
+    const int m = static_cast<int>(min(static_cast<int64_t>(W), T - pj0));
+    const int body = (m * MS) & ~15;
+    const uint8_t* buf = stage_all[warp][pb];
+    fence_proxy_async();
+    __syncwarp();
+    if (lane == 0 && body) {
+      bulk_s2g_plain(dp + pj0 * MS, buf, body);
+      bulk_commit();
     }
+    for (int e = body / MS + lane; e < m; e += 32)
+      *reinterpret_cast<typename MemberWord<MS>::T*>(dp + (pj0 + e) * MS) =
+          *reinterpret_cast<const typename MemberWord<MS>::T*>(buf + e * MS);
+  };
+
+  int it = 0;
+  int64_t prev_t = -1;
+  while (true) {
+    const int64_t j0 = t * W;
+    const int64_t j1 = min(j0 + W, T);
+    unsigned masks[W_CH];
+#pragma unroll
+    for (int k = 0; k < W_CH; ++k) masks[k] = 0;
+    int nr = 0;
+    rank_batch(b0, hi0, j0, j1, sD, nr, masks);
+    for (int64_t c0 = lo0 + 32; c0 <= hi0; c0 += 32)
+      rank_batch(load_batch<PT>(A, c0 + lane, hi0), hi0, j0, j1, sD, nr, masks);
+    __syncwarp();
+    const int b = it & 1;
+    uint8_t* buf = stage_all[warp][b];
+    // the bulk store that last read this buffer (two tasks ago) must have finished reading it
+    if (lane == 0) bulk_wait_read<1>();
+    __syncwarp();
+    int cum = 0;
+#pragma unroll
+    for (int k = 0; k < W_CH; ++k) {
+      const int64_t j = j0 + 32 * k + lane;
+      const int r = cum + __popc(masks[k] & le_mask) - 1;
+      if (j < j1) cp_async_member<MS>(buf + (32 * k + lane) * MS, sp + (j + sD[r]) * A.member_stride);
+      cum += __popc(masks[k]);
+    }
+    cp_async_commit();
+    // window two tasks ahead
+    const RecBatch<PT> b2 = load_batch<PT>(A, lo2 + lane, hi2);
+    int64_t lo3, hi3;
+    task_window(A, min(t + 3 * stride, ntasks - 1), T, lo3, hi3);
+    if (prev_t >= 0) {
+      cp_async_wait<1>();  // the previous task's members have landed
+      drain(prev_t, b ^ 1);
+    }
+    prev_t = t;
+    ++it;
+    if (t + stride >= ntasks) break;
+    __syncwarp();  // sD is rewritten for the next task
+    t += stride;
+    lo0 = lo1; hi0 = hi1; b0 = b1;
+    lo1 = lo2; hi1 = hi2; b1 = b2;
+    lo2 = lo3; hi2 = hi3;
   }
+  cp_async_wait<0>();
+  drain(prev_t, (it - 1) & 1);
+  if (lane == 0) bulk_wait_read<0>();  // shared memory stays valid until the last bulk store has read it
 }
 
 }  // namespace jag
 }  // namespace sk
 
 using namespace sk;
+
+// launch with programmatic stream serialization (the kernel pdl_wait()s before
+// touching its predecessor's output)
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 extern "C" {
 
@@ -362,6 +646,27 @@ int sk_jagged_scratch_bytes(int64_t n, size_t* nbytes) {
 
 static bool int_type(int t) {
   return t == SK_U8 || t == SK_U16 || t == SK_U32 || t == SK_U64 || t == SK_I32 || t == SK_I64 || t == SK_BOOL;
+}
+
+// scratch layout: [0] look-back ticket (u32), [8] 1 + last non-empty record, [16..] per-tile status / sums
+static int launch_scan(int64_t n, const void* lens, int lens_type, void* scratch, size_t need, const jag::ScanOut& O,
+                       cudaStream_t s) {
+  const int64_t tiles = (n + jag::SCAN_TILE - 1) / jag::SCAN_TILE;
+  uint8_t* sc = static_cast<uint8_t*>(scratch);
+  if (tiles <= jag::SCAN_DIRECT_TILES) {
+    int64_t* agg = reinterpret_cast<int64_t*>(sc + 16);
+    jag::tile_sum_kernel<<<static_cast<unsigned>(tiles), jag::SCAN_NT, 0, s>>>(
+        n, lens, lens_type, agg, O.starts ? O.last : nullptr);
+    SK_TRY(cudaGetLastError());
+    SK_TRY(launch_pdl(jag::tile_apply_kernel, dim3(static_cast<unsigned>(tiles)), dim3(jag::SCAN_NT), s, n, lens,
+                      lens_type, static_cast<const int64_t*>(agg), O));
+  } else {
+    SK_TRY(cudaMemsetAsync(scratch, 0, need, s));
+    jag::scan_lookback_kernel<<<static_cast<unsigned>(tiles), jag::SCAN_NT, 0, s>>>(
+        n, lens, lens_type, reinterpret_cast<uint64_t*>(sc + 16), reinterpret_cast<unsigned int*>(sc), O);
+  }
+  SK_TRY(cudaGetLastError());
+  return SK_OK;
 }
 
 int sk_jagged_scan(int64_t n, const void* lens, int lens_type, void* prefix, int prefix_type, void* scratch,
@@ -382,67 +687,131 @@ int sk_jagged_scan(int64_t n, const void* lens, int lens_type, void* prefix, int
     if (total_dev) SK_TRY(cudaMemsetAsync(total_dev, 0, 8, s));
     return SK_OK;
   }
-  SK_TRY(cudaMemsetAsync(scratch, 0, need, s));
-  const int64_t tiles = (n + jag::SCAN_TILE - 1) / jag::SCAN_TILE;
-  unsigned int* ticket = static_cast<unsigned int*>(scratch);
-  uint64_t* status = reinterpret_cast<uint64_t*>(static_cast<uint8_t*>(scratch) + 16);
-  jag::scan_kernel<<<static_cast<unsigned>(tiles), jag::SCAN_NT, 0, s>>>(n, lens, lens_type, prefix, prefix_type,
-                                                                          status, ticket, total_dev, nullptr);
-  SK_TRY(cudaGetLastError());
-  return SK_OK;
+  jag::ScanOut O{prefix, prefix_type, total_dev, nullptr, nullptr, 0, nullptr};
+  return launch_scan(n, lens, lens_type, scratch, need, O, s);
 }
 
-static int scatter_impl(int64_t n, const void* prefix, int prefix_type, const int64_t* src_off, const void* src_pool,
-                        int64_t member_stride, int nfields, const int64_t* field_off, const int32_t* field_size,
-                        void* const* dst_pools, int64_t total, const int64_t* total_dev, uintptr_t stream,
-                        int64_t* starts_buf = nullptr) {
+// member-field table of the gather
+static int gather_args(jag::ScatterArgs* A, int64_t n, const void* prefix, int prefix_type, const int64_t* src_off,
+                       const void* src_pool, int64_t member_stride, int nfields, const int64_t* field_off,
+                       const int32_t* field_size, void* const* dst_pools, int64_t total, const int64_t* total_dev) {
   if (n < 0 || total < 0) return set_error(SK_ERR_INVALID, "negative sizes");
-  if (nfields < 1 || nfields > jag::SC_MAXF) return set_error(SK_ERR_INVALID, "nfields %d outside [1, 8]", nfields);
+  if (nfields < 1 || nfields > jag::G_MAXF) return set_error(SK_ERR_INVALID, "nfields %d outside [1, 8]", nfields);
   if (!int_type(prefix_type)) return set_error(SK_ERR_INVALID, "prefix type must be an integer type");
-  jag::ScatterArgs A;
-  memset(&A, 0, sizeof(A));
-  A.n = n;
-  A.prefix = prefix;
-  A.prefix_type = prefix_type;
-  A.src_off = src_off;
-  A.src_pool = static_cast<const uint8_t*>(src_pool);
-  A.member_stride = member_stride;
-  A.total = total;
-  A.total_dev = total_dev;
-  A.nfields = nfields;
-  bool aligned = true;
+  memset(A, 0, sizeof(*A));
+  A->n = n;
+  A->prefix = prefix;
+  A->prefix_type = prefix_type;
+  A->src_off = src_off;
+  A->src_pool = static_cast<const uint8_t*>(src_pool);
+  A->member_stride = member_stride;
+  A->total = total;
+  A->total_dev = total_dev;
+  A->nfields = nfields;
   for (int f = 0; f < nfields; ++f) {
     const int isz = field_size[f];
     if (isz != 1 && isz != 2 && isz != 4 && isz != 8) return set_error(SK_ERR_INVALID, "member field size %d", isz);
     if (field_off[f] < 0 || field_off[f] + isz > member_stride)
       return set_error(SK_ERR_RANGE, "member field %d outside the member stride", f);
-    A.field_off[f] = field_off[f];
-    A.field_size[f] = isz;
-    A.dst[f] = static_cast<uint8_t*>(dst_pools[f]);
-    aligned = aligned && (field_off[f] % isz == 0) && (member_stride % isz == 0) &&
-              (reinterpret_cast<uintptr_t>(src_pool) % isz == 0);
+    A->field_off[f] = field_off[f];
+    A->field_size[f] = isz;
+    A->dst[f] = static_cast<uint8_t*>(dst_pools[f]);
+    A->aligned[f] = (field_off[f] % isz == 0) && (member_stride % isz == 0) &&
+                    (reinterpret_cast<uintptr_t>(src_pool) % isz == 0);
   }
-  A.aligned = aligned;
-  if (total == 0 || n == 0) return SK_OK;
-  int dev = 0;
-  SK_TRY(cudaGetDevice(&dev));
-  cudaStream_t s = resolve_stream(dev, stream);
-  const int64_t blocks = (total + jag::SC_TILE - 1) / jag::SC_TILE;
-  int64_t* starts = starts_buf;
-  if (!starts) SK_TRY(cudaMallocAsync(&starts, static_cast<size_t>(blocks + 1) * sizeof(int64_t), s));
-  jag::tile_start_kernel<<<static_cast<unsigned>((blocks + 1 + 7) / 8), 256, 0, s>>>(A, starts, blocks);
-  SK_TRY(cudaGetLastError());
-  jag::scatter_kernel<<<static_cast<unsigned>(blocks), jag::SC_NT, 0, s>>>(A, starts);
-  SK_TRY(cudaGetLastError());
-  if (!starts_buf) SK_TRY(cudaFreeAsync(starts, s));
   return SK_OK;
 }
+
+}  // extern "C"
+
+template <class PT, int MS>
+static int launch_gather_t(const jag::ScatterArgs& A, int64_t ntasks, cudaStream_t s, const DeviceState* ds) {
+  static int occ = 0;
+  if (!occ) {
+    SK_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, jag::gather_kernel<PT, MS>, jag::G_NT, 0));
+    occ = std::max(occ, 1);
+  }
+  const int64_t wpb = jag::G_NT / 32;
+  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((ntasks + wpb - 1) / wpb,
+                                                              static_cast<int64_t>(ds->sm_count) * occ));
+  SK_TRY(launch_pdl(jag::gather_kernel<PT, MS>, dim3(static_cast<unsigned>(grid)), dim3(jag::G_NT), s, A));
+  SK_TRY(cudaGetLastError());
+  return SK_OK;
+}
+
+template <class PT, int MS>
+static int launch_gather_async(const jag::ScatterArgs& A, int64_t ntasks, cudaStream_t s, const DeviceState* ds) {
+  static int occ = 0;
+  if (!occ) {
+    SK_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, jag::gather_async_kernel<PT, MS>,
+                                                         jag::GA_WARPS * 32, 0));
+    occ = std::max(occ, 1);
+  }
+  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((ntasks + jag::GA_WARPS - 1) / jag::GA_WARPS,
+                                                              static_cast<int64_t>(ds->sm_count) * occ));
+  SK_TRY(launch_pdl(jag::gather_async_kernel<PT, MS>, dim3(static_cast<unsigned>(grid)), dim3(jag::GA_WARPS * 32), s,
+                    A));
+  SK_TRY(cudaGetLastError());
+  return SK_OK;
+}
+
+static bool async_gather_ok() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SK_JAGGED_ASYNC");
+    v = e ? atoi(e) : 1;
+  }
+  return v != 0;
+}
+
+template <class PT>
+static int launch_gather_p(const jag::ScatterArgs& A, int64_t ntasks, cudaStream_t s, const DeviceState* ds) {
+  const bool dst16 = reinterpret_cast<uintptr_t>(A.dst[0]) % 16 == 0;
+  if (async_gather_ok() && A.nfields == 1 && A.aligned[0] && dst16) {
+    if (A.field_size[0] == 8) return launch_gather_async<PT, 8>(A, ntasks, s, ds);
+    if (A.field_size[0] == 4) return launch_gather_async<PT, 4>(A, ntasks, s, ds);
+  }
+  if (A.nfields == 1 && A.aligned[0] && A.field_size[0] == 8) return launch_gather_t<PT, 8>(A, ntasks, s, ds);
+  if (A.nfields == 1 && A.aligned[0] && A.field_size[0] == 4) return launch_gather_t<PT, 4>(A, ntasks, s, ds);
+  return launch_gather_t<PT, 0>(A, ntasks, s, ds);
+}
+
+static int launch_gather(const jag::ScatterArgs& A, int64_t ntasks, cudaStream_t s, int dev) {
+  DeviceState* ds = nullptr;
+  if (int rc = device_state(dev, &ds)) return rc;
+  switch (A.prefix_type) {
+    case SK_U8: case SK_BOOL: return launch_gather_p<uint8_t>(A, ntasks, s, ds);
+    case SK_U16: return launch_gather_p<uint16_t>(A, ntasks, s, ds);
+    case SK_U32: return launch_gather_p<uint32_t>(A, ntasks, s, ds);
+    case SK_I32: return launch_gather_p<int32_t>(A, ntasks, s, ds);
+    default: return launch_gather_p<int64_t>(A, ntasks, s, ds);
+  }
+}
+
+extern "C" {
 
 int sk_jagged_scatter(int64_t n, const void* prefix, int prefix_type, const int64_t* src_off, const void* src_pool,
                       int64_t member_stride, int nfields, const int64_t* field_off, const int32_t* field_size,
                       void* const* dst_pools, int64_t total, uintptr_t stream) {
-  return scatter_impl(n, prefix, prefix_type, src_off, src_pool, member_stride, nfields, field_off, field_size,
-                      dst_pools, total, nullptr, stream);
+  jag::ScatterArgs A;
+  if (int rc = gather_args(&A, n, prefix, prefix_type, src_off, src_pool, member_stride, nfields, field_off,
+                           field_size, dst_pools, total, nullptr))
+    return rc;
+  if (total == 0 || n == 0) return SK_OK;
+  int dev = 0;
+  SK_TRY(cudaGetDevice(&dev));
+  cudaStream_t s = resolve_stream(dev, stream);
+  const int64_t ntasks = (total + jag::W - 1) / jag::W;
+  // starts[0..ntasks) from a search over the given prefix, starts[ntasks] = 1 + last non-empty record
+  int64_t* starts = nullptr;
+  SK_TRY(cudaMallocAsync(&starts, static_cast<size_t>(ntasks + 1) * sizeof(int64_t), s));
+  jag::task_start_kernel<<<static_cast<unsigned>((ntasks + 1 + 7) / 8), 256, 0, s>>>(A, starts, ntasks);
+  SK_TRY(cudaGetLastError());
+  A.starts = starts;
+  A.last_rec = reinterpret_cast<const unsigned long long*>(starts + ntasks);
+  const int rc = launch_gather(A, ntasks, s, dev);
+  SK_TRY(cudaFreeAsync(starts, s));
+  return rc;
 }
 
 int sk_jagged_pack(int64_t n, const void* lens, int lens_type, void* prefix, int prefix_type, const int64_t* src_off,
@@ -456,6 +825,10 @@ int sk_jagged_pack(int64_t n, const void* lens, int lens_type, void* prefix, int
   size_t need = 0;
   sk_jagged_scratch_bytes(n, &need);
   if (scratch_bytes < need) return set_error(SK_ERR_INVALID, "scratch too small: %zu < %zu", scratch_bytes, need);
+  jag::ScatterArgs A;
+  if (int rc = gather_args(&A, n, nullptr, prefix_type, src_off, src_pool, member_stride, nfields, field_off,
+                           field_size, dst_pools, capacity, total_dev))
+    return rc;
   int dev = 0;
   SK_TRY(cudaGetDevice(&dev));
   cudaStream_t s = resolve_stream(dev, stream);
@@ -469,24 +842,27 @@ int sk_jagged_pack(int64_t n, const void* lens, int lens_type, void* prefix, int
   const bool may_wrap = bits < 63 && capacity >= (int64_t(1) << bits);
   int64_t* p64 = nullptr;
   if (may_wrap) SK_TRY(cudaMallocAsync(&p64, static_cast<size_t>(n + 1) * sizeof(int64_t), s));
-  SK_TRY(cudaMemsetAsync(scratch, 0, need, s));
-  const int64_t tiles = (n + jag::SCAN_TILE - 1) / jag::SCAN_TILE;
-  unsigned int* ticket = static_cast<unsigned int*>(scratch);
-  uint64_t* status = reinterpret_cast<uint64_t*>(static_cast<uint8_t*>(scratch) + 16);
-  jag::scan_kernel<<<static_cast<unsigned>(tiles), jag::SCAN_NT, 0, s>>>(n, lens, lens_type, prefix, prefix_type,
-                                                                          status, ticket, total_dev, p64);
-  SK_TRY(cudaGetLastError());
-  // gather bounded by the pools' capacity; the kernels read the true total on the device
-  // the tile-start array lives in the caller's scratch when it is large enough
+  // the gather's work split: in the caller's scratch when it is large enough
+  const int64_t ntasks = capacity ? (capacity + jag::W - 1) / jag::W : 0;
   const size_t scan_part = (need + 255) & ~size_t(255);
-  const size_t starts_need = static_cast<size_t>((capacity + jag::SC_TILE - 1) / jag::SC_TILE + 1) * sizeof(int64_t);
+  const size_t starts_need = static_cast<size_t>(ntasks + 1) * sizeof(int64_t);
   int64_t* starts = scratch_bytes >= scan_part + starts_need
                         ? reinterpret_cast<int64_t*>(static_cast<uint8_t*>(scratch) + scan_part)
                         : nullptr;
-  int rc = capacity ? scatter_impl(n, p64 ? static_cast<const void*>(p64) : prefix, p64 ? SK_I64 : prefix_type,
-                                   src_off, src_pool, member_stride, nfields, field_off, field_size, dst_pools,
-                                   capacity, total_dev, stream, starts)
-                    : SK_OK;
+  const bool own_starts = ntasks && !starts;
+  if (own_starts) SK_TRY(cudaMallocAsync(&starts, starts_need, s));
+  unsigned long long* last_rec = reinterpret_cast<unsigned long long*>(static_cast<uint8_t*>(scratch) + 8);
+  jag::ScanOut O{prefix, prefix_type, total_dev, p64, ntasks ? starts : nullptr, ntasks, last_rec};
+  int rc = launch_scan(n, lens, lens_type, scratch, need, O, s);
+  // gather bounded by the pools' capacity; the kernel reads the true total on the device
+  if (rc == SK_OK && ntasks) {
+    A.prefix = p64 ? static_cast<const void*>(p64) : prefix;
+    A.prefix_type = p64 ? SK_I64 : prefix_type;
+    A.starts = starts;
+    A.last_rec = last_rec;
+    rc = launch_gather(A, ntasks, s, dev);
+  }
+  if (own_starts) cudaFreeAsync(starts, s);
   if (p64) cudaFreeAsync(p64, s);
   return rc;
 }

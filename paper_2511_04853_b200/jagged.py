@@ -137,7 +137,7 @@ def pack(coll, path: str, lens, src_offsets, src_pool, member_stride: int | None
         ws = _workspace(dev)
         need = C.c_size_t(0)
         nat.call("sk_jagged_scratch_bytes", n, C.byref(need))
-        starts_bytes = ((cap + 2047) // 2048 + 1) * 8  # tile starts of the gather, kept in the scratch too
+        starts_bytes = ((cap + 255) // 256 + 1) * 8  # the gather's work split (one entry per 256 members)
         scratch = ws.scratch_for(-(-need.value // 256) * 256 + starts_bytes)
         ptrs = (C.c_void_p * nf)(*[lay.plane_address(lf, 0) for lf in leaves])
         nat.call("sk_jagged_pack", n, lens_d.ptr, nat.TYPE_CODES[_NP_CODE[lens_d.dtype]], prefix_ptr,

@@ -1,0 +1,155 @@
+"""K4 kernel paths through the C-ABI: reduce-then-scan and look-back scans,
+the async (cp.async + bulk store) gather for 4/8-byte members, the register
+gather (misaligned destination), the generic multi-field table, wrapping
+narrow prefixes and sk_jagged_scatter over a caller-provided prefix.
+
+Oracle: prefix = cumsum(lens) cast to the index dtype (collection.py:553-554),
+members = the concatenated segments (collection.py:555-556), restated with
+numpy (np.repeat) so multi-million-record cases check in seconds."""
+
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from paper_2511_04853_b200 import _native as nat
+from paper_2511_04853_b200 import memctx as mc
+from paper_2511_04853_b200.devarray import DeviceArray
+
+pytestmark = pytest.mark.gpu
+
+CUDA = mc.ContextInfo.cuda(0)
+TC = nat.TYPE_CODES
+
+
+def _inputs(n, max_len, seed, slack=3):
+    rng = np.random.default_rng(seed)
+    lens = rng.integers(0, max_len + 1, n).astype(np.int32)
+    order = rng.permutation(n)
+    gaps = lens[order].astype(np.int64) + rng.integers(0, slack + 1, n)
+    offs = np.empty(n, np.int64)
+    offs[order] = np.concatenate([[0], np.cumsum(gaps)[:-1]]) if n else gaps
+    return lens, offs, int(gaps.sum()) if n else 0
+
+
+def _gather_index(lens, offs):
+    """source member index of every output member"""
+    P = np.concatenate([[0], np.cumsum(lens.astype(np.int64))])
+    T = int(P[-1])
+    return np.repeat(offs - P[:-1], lens.astype(np.int64)) + np.arange(T, dtype=np.int64), P
+
+
+def _pack(lens, offs, pool_bytes, stride, fields, ptype, cap_extra=0, dst_shift=0):
+    """run sk_jagged_pack; fields = [(offset, size)]; returns (prefix, [field arrays as bytes], total)"""
+    n = lens.size
+    T = int(lens.astype(np.int64).sum())
+    cap = T + cap_extra
+    d_lens = DeviceArray.from_numpy(lens, CUDA)
+    d_offs = DeviceArray.from_numpy(offs, CUDA)
+    d_pool = DeviceArray.from_numpy(pool_bytes, CUDA)
+    pnp = np.dtype({"i32": np.int32, "u16": np.uint16, "u8": np.uint8, "i64": np.int64, "u32": np.uint32}[ptype])
+    prefix = DeviceArray(n + 1, pnp, CUDA)
+    outs = [DeviceArray(max(cap, 1) * sz + 64, np.uint8, CUDA) for _, sz in fields]
+    need = C.c_size_t(0)
+    nat.call("sk_jagged_scratch_bytes", n, C.byref(need))
+    sbytes = -(-need.value // 256) * 256 + ((cap + 255) // 256 + 1) * 8
+    scratch = DeviceArray(sbytes, np.uint8, CUDA)
+    total = DeviceArray(1, np.int64, CUDA)
+    nf = len(fields)
+    foff = (C.c_int64 * nf)(*[o for o, _ in fields])
+    fsz = (C.c_int32 * nf)(*[sz for _, sz in fields])
+    dst = (C.c_void_p * nf)(*[o.ptr + dst_shift for o in outs])
+    nat.call("sk_jagged_pack", n, d_lens.ptr, TC["i32"], prefix.ptr, TC[ptype], d_offs.ptr, d_pool.ptr, stride, nf,
+             foff, fsz, dst, cap, scratch.ptr, scratch.n, total.ptr, nat.stream(0))
+    nat.sync(0)
+    t = int(total.numpy()[0])
+    res = [o.numpy()[dst_shift:dst_shift + t * sz].tobytes() for o, (_, sz) in zip(outs, fields)]
+    p = prefix.numpy()
+    for a in (d_lens, d_offs, d_pool, prefix, scratch, total, *outs):
+        a.free()
+    return p, res, t
+
+
+def _expect(lens, offs, pool_bytes, stride, fields, ptype):
+    idx, P = _gather_index(lens, offs)
+    rec = pool_bytes.reshape(-1, stride)
+    want = [rec[idx, o:o + sz].tobytes() for o, sz in fields]
+    return P.astype(np.dtype({"i32": np.int32, "u16": np.uint16, "u8": np.uint8, "i64": np.int64,
+                              "u32": np.uint32}[ptype])), want, int(P[-1])
+
+
+@pytest.mark.parametrize("n,max_len,msize", [(1, 5, 8), (300, 20, 8), (1_000_000, 20, 8), (1_000_000, 20, 4),
+                                             (200_000, 0, 8), (50_000, 3000, 8)])
+def test_async_gather_single_field(n, max_len, msize):
+    lens, offs, plen = _inputs(n, max_len, seed=n + max_len)
+    pool = np.random.default_rng(1).integers(0, 256, plen * msize + 8, dtype=np.uint8)
+    fields = [(0, msize)]
+    p, got, t = _pack(lens, offs, pool, msize, fields, "i32", cap_extra=777)
+    pw, want, tw = _expect(lens, offs, pool[:plen * msize], msize, fields, "i32")
+    assert t == tw
+    assert p.tobytes() == pw.tobytes()
+    assert got == want
+
+
+def test_register_gather_misaligned_destination():
+    lens, offs, plen = _inputs(400_000, 20, seed=3)
+    pool = np.random.default_rng(2).integers(0, 256, plen * 8, dtype=np.uint8)
+    p, got, t = _pack(lens, offs, pool, 8, [(0, 8)], "i32", dst_shift=8)  # dst % 16 == 8 -> register path
+    pw, want, _ = _expect(lens, offs, pool, 8, [(0, 8)], "i32")
+    assert p.tobytes() == pw.tobytes() and got == want
+
+
+def test_generic_field_table_unaligned_stride():
+    lens, offs, plen = _inputs(100_000, 12, seed=4)
+    stride = 15
+    fields = [(0, 4), (4, 8), (12, 2), (14, 1)]
+    pool = np.random.default_rng(3).integers(0, 256, plen * stride, dtype=np.uint8)
+    p, got, t = _pack(lens, offs, pool, stride, fields, "i64")
+    pw, want, _ = _expect(lens, offs, pool, stride, fields, "i64")
+    assert p.tobytes() == pw.tobytes() and got == want
+
+
+def test_wrapping_u16_prefix_uses_wide_gather():
+    lens, offs, plen = _inputs(30_000, 9, seed=5)  # ~135k members: the u16 prefix wraps
+    pool = np.random.default_rng(4).integers(0, 256, plen * 8, dtype=np.uint8)
+    p, got, t = _pack(lens, offs, pool, 8, [(0, 8)], "u16")
+    pw, want, tw = _expect(lens, offs, pool, 8, [(0, 8)], "u16")
+    assert tw > 65535 and t == tw
+    assert p.tobytes() == pw.tobytes() and got == want
+
+
+def test_lookback_scan_beyond_direct_grid():
+    # > 4096 scan tiles of 4096 lengths: the single-pass look-back scan
+    n = 4096 * 4096 + 12345
+    lens = (np.random.default_rng(6).integers(0, 4, n)).astype(np.int32)
+    d_lens = DeviceArray.from_numpy(lens, CUDA)
+    prefix = DeviceArray(n + 1, np.int64, CUDA)
+    need = C.c_size_t(0)
+    nat.call("sk_jagged_scratch_bytes", n, C.byref(need))
+    scratch = DeviceArray(need.value, np.uint8, CUDA)
+    total = DeviceArray(1, np.int64, CUDA)
+    nat.call("sk_jagged_scan", n, d_lens.ptr, TC["i32"], prefix.ptr, TC["i64"], scratch.ptr, scratch.n, total.ptr,
+             nat.stream(0))
+    nat.sync(0)
+    want = np.concatenate([[0], np.cumsum(lens.astype(np.int64))])
+    assert int(total.numpy()[0]) == int(want[-1])
+    assert np.array_equal(prefix.numpy(), want)
+    for a in (d_lens, prefix, scratch, total):
+        a.free()
+
+
+def test_scatter_over_given_prefix():
+    lens, offs, plen = _inputs(250_000, 20, seed=7)
+    pool = np.random.default_rng(8).integers(0, 256, plen * 8, dtype=np.uint8)
+    P = np.concatenate([[0], np.cumsum(lens.astype(np.int64))]).astype(np.int32)
+    T = int(P[-1])
+    d_p, d_o, d_pool = (DeviceArray.from_numpy(x, CUDA) for x in (P, offs, pool))
+    out = DeviceArray(T * 8, np.uint8, CUDA)
+    foff, fsz, dst = (C.c_int64 * 1)(0), (C.c_int32 * 1)(8), (C.c_void_p * 1)(out.ptr)
+    nat.call("sk_jagged_scatter", lens.size, d_p.ptr, TC["i32"], d_o.ptr, d_pool.ptr, 8, 1, foff, fsz, dst, T,
+             nat.stream(0))
+    nat.sync(0)
+    _, want, _ = _expect(lens, offs, pool, 8, [(0, 8)], "i32")
+    assert out.numpy().tobytes() == want[0]
+    for a in (d_p, d_o, d_pool, out):
+        a.free()
