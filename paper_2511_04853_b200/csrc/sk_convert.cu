@@ -206,6 +206,19 @@ int make_plan(const sk_conv_desc& d, const DeviceState& ds, bool in_bulk_ok, boo
   int64_t R = (static_cast<int64_t>(tun.tile_bytes) * 1000 / rec_sum) / g * g;
   R = std::max<int64_t>(R, g);
   R = std::min<int64_t>(R, std::max<int64_t>(g, 4096));
+  // small problems: shrink the tile so the tiles fill whole rounds of the
+  // persistent grid (1M Obj8 records = 2.25 target tiles per CTA would
+  // otherwise run 3 rounds with the last one a quarter full)
+  if (d.n > 0) {
+    const int64_t est_grid = static_cast<int64_t>(ds.sm_count) * std::max(tun.ctas_per_sm, 1);
+    const int64_t tiles0 = (d.n + R - 1) / R;
+    const int64_t rounds = (tiles0 + est_grid - 1) / est_grid;
+    if (rounds <= 16 && tiles0 > est_grid) {
+      int64_t Rb = (d.n + est_grid * rounds - 1) / (est_grid * rounds);
+      Rb = (Rb + g - 1) / g * g;
+      if (Rb >= std::min<int64_t>(R, 256)) R = std::min(R, Rb);
+    }
+  }
   P.R = static_cast<int32_t>(R);
   P.ntiles = d.n ? (d.n + R - 1) / R : 0;
 
