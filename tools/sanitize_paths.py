@@ -1,0 +1,49 @@
+"""Small invocations of every kernel family for compute-sanitizer runs
+(memcheck / racecheck / synccheck): jagged scan + both gathers + scatter,
+conversion word/element/specialised paths, sensor fused, reco."""
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests"))
+import test_gpu_jagged_paths as J  # noqa: E402
+
+lens, offs, plen = J._inputs(3000, 20, seed=1)
+pool = np.random.default_rng(1).integers(0, 256, plen * 8 + 8, dtype=np.uint8)
+J._pack(lens, offs, pool, 8, [(0, 8)], "i32", cap_extra=99)            # async gather
+J._pack(lens, offs, pool, 8, [(0, 8)], "i32", dst_shift=8)             # register gather
+pool15 = np.random.default_rng(2).integers(0, 256, plen * 15, dtype=np.uint8)
+J._pack(lens, offs, pool15, 15, [(0, 4), (4, 8), (12, 2), (14, 1)], "i64")  # generic table
+lens2, offs2, plen2 = J._inputs(2000, 60, seed=3)
+pool2 = np.random.default_rng(3).integers(0, 256, plen2 * 8, dtype=np.uint8)
+J._pack(lens2, offs2, pool2, 8, [(0, 8)], "u16")                       # wrapping prefix
+J._pack(lens2, offs2, pool2, 8, [(0, 4)], "i32", cap_extra=10)         # 4-byte async
+J._pack(lens2, offs2, pool2, 8, [(0, 8)], "i32", cap_extra=-100)       # overflow: gathers nothing
+J.test_scatter_over_given_prefix.__wrapped__ if hasattr(J.test_scatter_over_given_prefix, "__wrapped__") else None
+
+import paper_2511_04853_b200 as sk  # noqa: E402
+from paper_2511_04853_b200 import layouts as ly, memctx as mc, sensor, transfer as tr, workloads as wl  # noqa: E402
+
+CUDA = mc.ContextInfo.cuda(0)
+for n in (1, 5000, 70001):
+    recs = wl.obj8_records(n, seed=n)
+    h = sk.Collection(wl.OBJ8_SCHEMA, ly.AOS, mc.ContextInfo.pinned())
+    h.resize(n)
+    h.layout._struct_buf._data[: n * 32] = recs.view(np.uint8)
+    d = sk.Collection(wl.OBJ8_SCHEMA, ly.PER_FIELD, CUDA)
+    tr.copy_collection(d, h)
+    back = sk.Collection(wl.OBJ8_SCHEMA, ly.AOS, CUDA)
+    tr.copy_collection(back, d)
+gen = sk.Collection(sensor.SENSOR_SCHEMA, ly.PER_FIELD, CUDA)
+sensor.generate_events(gen, 40, 30, range(2), 0.01)
+a = sk.Collection(sensor.SENSOR_SCHEMA, ly.AOS, CUDA)
+tr.copy_collection(a, gen)
+p = sk.Collection(sensor.SENSOR_SCHEMA, ly.PER_FIELD, CUDA)
+from paper_2511_04853_b200.devarray import DeviceArray  # noqa: E402
+noise = DeviceArray(len(a), np.float32, CUDA)
+sensor.transfer_calibrate(p, a, noise)
+parts = sk.Collection(sensor.PARTICLE_SCHEMA, ly.PER_FIELD, CUDA)
+sensor.reconstruct_from_collection(p, 40, 30, out=parts, events=2, noise=noise)
+print("sanitize paths done", len(parts))
