@@ -572,7 +572,7 @@ int run(const sk_conv_desc& d, int device, cudaStream_t s, int epi, float* extra
     SK_TRY(cudaStreamSynchronize(ds->stream));
     SK_TRY(cudaStreamSynchronize(ds->copy_in));
     SK_TRY(cudaStreamSynchronize(ds->copy_out));
-    if (ds->staging) SK_TRY(cudaFree(ds->staging));
+    if (ds->staging) retire_or_free_staging(device, ds->staging);
     ds->staging = nullptr;
     ds->staging_bytes = 0;
     SK_TRY(cudaMalloc(&ds->staging, need));

@@ -35,6 +35,14 @@ struct DeviceState {
   size_t staging_bytes = 0;
 };
 
+// Captured graphs bake in device addresses, the pipeline's staging buffer
+// included. While any graph is alive, a staging buffer that has to grow is
+// retired (kept allocated) instead of freed; the last sk_graph_destroy frees
+// the retired buffers.
+void retire_or_free_staging(int device, void* p);
+void graph_created();
+void graph_destroyed();
+
 int device_state(int device, DeviceState** out);
 // resolves stream 0 to the device's library stream
 cudaStream_t resolve_stream(int device, uintptr_t s);

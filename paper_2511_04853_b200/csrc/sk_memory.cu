@@ -5,6 +5,8 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <utility>
+#include <vector>
 
 #include "sk_internal.cuh"
 
@@ -399,6 +401,43 @@ extern "C" int sk_fill_random(void* dst, size_t nbytes, uint64_t seed, uint64_t 
 
 extern "C" {
 
+}  // extern "C"
+
+namespace sk {
+
+static std::mutex g_graph_mu;
+static int g_graphs_alive = 0;
+static std::vector<std::pair<int, void*>> g_retired;
+
+void retire_or_free_staging(int device, void* p) {
+  std::lock_guard<std::mutex> lk(g_graph_mu);
+  if (g_graphs_alive > 0) g_retired.push_back({device, p});
+  else cudaFree(p);
+}
+
+void graph_created() {
+  std::lock_guard<std::mutex> lk(g_graph_mu);
+  ++g_graphs_alive;
+}
+
+void graph_destroyed() {
+  std::lock_guard<std::mutex> lk(g_graph_mu);
+  if (--g_graphs_alive > 0) return;
+  g_graphs_alive = 0;
+  int cur = 0;
+  cudaGetDevice(&cur);
+  for (const auto& r : g_retired) {
+    cudaSetDevice(r.first);
+    cudaFree(r.second);
+  }
+  g_retired.clear();
+  cudaSetDevice(cur);
+}
+
+}  // namespace sk
+
+extern "C" {
+
 int sk_capture_begin(int device) {
   DeviceState* d = nullptr;
   int rc = device_state(device, &d);
@@ -422,6 +461,7 @@ int sk_capture_end(int device, void** graph_exec) {
   cudaGraphDestroy(g);
   if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate");
   *graph_exec = x;
+  graph_created();
   return SK_OK;
 }
 
@@ -434,7 +474,10 @@ int sk_graph_launch(void* graph_exec, int device) {
 }
 
 int sk_graph_destroy(void* graph_exec) {
-  if (graph_exec) SK_TRY(cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(graph_exec)));
+  if (!graph_exec) return SK_OK;
+  const cudaError_t e = cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(graph_exec));
+  graph_destroyed();
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGraphExecDestroy");
   return SK_OK;
 }
 

@@ -51,3 +51,28 @@ def test_prepared_transfer_with_jagged_side_leaves_and_staleness():
     src.resize(10)
     with pytest.raises(sk.TransferError):
         prep.run()
+
+
+def test_prepared_transfer_survives_staging_growth():
+    """a captured host pipeline references the device staging buffer; a later,
+    larger transfer that grows the staging must not free it under the graph"""
+    n = 50_000
+    recs = wl.obj8_records(n, seed=9)
+    small = aos_collection(wl.OBJ8_SCHEMA, recs, n, PINNED)
+    dst = sk.Collection(wl.OBJ8_SCHEMA, ly.PER_FIELD, CUDA)
+    prep = tr.prepare(dst, small)
+    big_n = 40_000_000  # 1.28 GB: several full pipeline chunks, grows the staging
+    big = sk.Collection(wl.OBJ8_SCHEMA, ly.AOS, PINNED)
+    big.resize(big_n)
+    big_dst = sk.Collection(wl.OBJ8_SCHEMA, ly.PER_FIELD, CUDA)
+    tr.copy_collection(big_dst, big)
+    big.free()
+    big_dst.free()
+    recs2 = wl.obj8_records(n, seed=10)
+    small.layout._struct_buf._data[: n * 32] = recs2.view(np.uint8)
+    prep.run()
+    planes = to_host_planes(dst)
+    want = R.aos_to_planes(recs2)
+    for i in range(8):
+        assert planes[f"f{i}#0"] == want[f"f{i}"][0].tobytes()
+    prep.close()
