@@ -363,6 +363,19 @@ def run_ours(args) -> None:
                "sample": f"{args.cpu_objects} Obj8 objects, reference per-leaf numpy path "
                          f"(transfer.py:196-228) restated in oracle/cpu_baseline.py, mean of fastest of "
                          f"{cb['reps']} reps; host: {os.cpu_count()} x {_cpu_info()}"}
+        if extra:
+            # the reference's CPU path beside each extra config (one core, bounded samples)
+            pc = cpu_baseline.per_config(budget_s=1.5)
+            pairs = {"config1_obj8_1M": ("config1_obj8", "device_gbs"),
+                     "config2_sensor_64x190096": ("config2_sensor", "device_gbs"),
+                     "config3_jagged_1M": ("config3_jagged", "gbs"),
+                     "config4_aosoa_100M": ("config4_aosoa", "gbs")}
+            for key, (ck, gkey) in pairs.items():
+                if key in extra and ck in pc:
+                    c = pc[ck]
+                    extra[key]["cpu_port_1core"] = {k: (round(v, 3) if isinstance(v, float) else v)
+                                                    for k, v in c.items()}
+                    extra[key]["gpu_over_cpu_1core"] = round(extra[key][gkey] / c["gbs"], 1)
 
     if rank != 0:
         if world > 1:

@@ -94,3 +94,85 @@ def multi_core(n: int, steps: int, warmup: int, procs: int | None = None, seed: 
         del rec, base
         a.close()
         p.close()
+
+
+# ---- per-config single-core legs (bench extras) ------------------------------------------
+
+def _rate(fn, budget_s: float) -> float:
+    """seconds per call: warm-up, then the mean of the fastest third (bench.py:214-215)"""
+    fn()
+    samples = []
+    t_end = time.perf_counter() + budget_s
+    while time.perf_counter() < t_end or len(samples) < 3:
+        t0 = time.perf_counter()
+        fn()
+        samples.append(time.perf_counter() - t0)
+    return mean_of_fastest(samples, max(1, min(10, len(samples) // 3)))
+
+
+def per_config(budget_s: float = 2.0, seed: int = 3) -> dict:
+    """The reference's CPU path for configs 1-4 on one core, on bounded samples
+    of each workload (rates scale linearly in the sample size):
+    1: per-leaf AoS->planes of 1M Obj8 (transfer.py:196-228);
+    2: one 436x436 event, per-leaf AoS->planes of the 30 B Sensor record, then
+       calibrate + noise (detector/schemas.py:29-41);
+    3: jagged_fill of 100K clusters from a shuffled pool: per-segment
+       np.asarray + concatenate + cumsum (collection.py:537-556);
+    4: 1M Track records -> AoSoA T=128 of [pz, px, x, charge] with numpy casts."""
+    from . import restate as R
+
+    rng = np.random.default_rng(seed)
+    out = {}
+    n1 = 1_000_000
+    rec = np.frombuffer(rng.integers(0, 256, n1 * 32, dtype=np.uint8).tobytes(), OBJ8)
+    planes = [np.empty(n1, OBJ8[i]) for i in range(8)]
+    t = _rate(lambda: per_leaf_convert(rec, planes), budget_s)
+    out["config1_obj8"] = {"sample": f"{n1} objects", "objects_per_s": n1 / t, "gbs": n1 * 64 / t / 1e9}
+
+    ev = R.generate_event(436, 436, seed=0, density=0.002)
+    aos = R.sensor_aos(ev)
+    cal = aos["calibration_data"]
+    cols = {"type": aos["type"], "counts": aos["counts"], "energy": aos["energy"],
+            **{k: cal[k] for k in cal.dtype.names}}  # the 8 leaves, plan order
+    cells = aos.size
+    splanes = {k: np.empty(cells, v.dtype) for k, v in cols.items()}
+
+    def case_study():
+        for k, v in cols.items():
+            splanes[k][:] = np.ascontiguousarray(v)
+        e = R.calibrate(splanes["counts"], splanes["parameter_A"], splanes["parameter_B"])
+        R.noise(e, splanes["noise_A"], splanes["noise_B"], splanes["noisy"])
+
+    t = _rate(case_study, budget_s)
+    out["config2_sensor"] = {"sample": f"1 event, {cells} cells", "cells_per_s": cells / t,
+                             "gbs": cells * 64 / t / 1e9}
+
+    n3 = 100_000
+    lens = rng.integers(0, 21, n3).astype(np.int32)
+    order = rng.permutation(n3)
+    gaps = lens[order].astype(np.int64) + rng.integers(0, 4, n3)
+    offs = np.empty(n3, np.int64)
+    offs[order] = np.concatenate([[0], np.cumsum(gaps)[:-1]])
+    pool = rng.integers(0, 1 << 62, int(gaps.sum()), dtype=np.uint64)
+    segments = [pool[o:o + n] for o, n in zip(offs.tolist(), lens.tolist())]  # the caller's per-object vectors
+    members = int(lens.sum())
+
+    def jagged_fill():
+        arrs = [np.asarray(s, dtype=np.uint64) for s in segments]
+        pv = np.zeros(n3 + 1, np.int32)
+        pv[1:] = np.cumsum(np.array([a.size for a in arrs], np.int64)).astype(np.int32)
+        np.concatenate(arrs)
+
+    t = _rate(jagged_fill, budget_s)
+    out["config3_jagged"] = {"sample": f"{n3} clusters, {members} members", "members_per_s": members / t,
+                             "gbs": (n3 * 16 + members * 16) / t / 1e9}
+
+    n4 = 1_000_000
+    track = np.dtype([("x", "<f8"), ("y", "<f8"), ("z", "<f8"), ("px", "<f8"), ("py", "<f8"), ("pz", "<f8"),
+                      ("charge", "<i4"), ("id", "<u8")])
+    trk = np.frombuffer(rng.integers(0, 256, n4 * 60, dtype=np.uint8).tobytes(), track)
+    fields = [("pz", "f32"), ("px", "f32"), ("x", "f32"), ("charge", "i32")]
+    with np.errstate(all="ignore"):
+        t = _rate(lambda: R.to_aosoa(trk, fields, 128), budget_s)
+    out["config4_aosoa"] = {"sample": f"{n4} tracks", "objects_per_s": n4 / t, "gbs": n4 * 76 / t / 1e9}
+    return out
