@@ -155,7 +155,7 @@ struct Tunables {
   int tile_bytes = TILE_TARGET;
   int max_stages = MAX_STAGES;
   int ctas_per_sm = 4;
-  int cache_hint = 1;
+  int cache_hint = 0;  // evict_first hints: neutral at 1e9 records, costly when the data could stay in L2
 };
 
 static int env_int(const char* name, int dflt, int lo, int hi) {
