@@ -653,7 +653,11 @@ static int launch_scan(int64_t n, const void* lens, int lens_type, void* scratch
                        cudaStream_t s) {
   const int64_t tiles = (n + jag::SCAN_TILE - 1) / jag::SCAN_TILE;
   uint8_t* sc = static_cast<uint8_t*>(scratch);
-  if (tiles <= jag::SCAN_DIRECT_TILES) {
+  static const int64_t direct_max = [] {
+    const char* e = getenv("SK_SCAN_DIRECT_TILES");
+    return e ? static_cast<int64_t>(atoll(e)) : jag::SCAN_DIRECT_TILES;
+  }();
+  if (tiles <= direct_max) {
     int64_t* agg = reinterpret_cast<int64_t*>(sc + 16);
     jag::tile_sum_kernel<<<static_cast<unsigned>(tiles), jag::SCAN_NT, 0, s>>>(
         n, lens, lens_type, agg, O.starts ? O.last : nullptr);
