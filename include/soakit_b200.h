@@ -179,14 +179,22 @@ int sk_jagged_scatter(int64_t n, const void* prefix, int prefix_type,
    *total_dev on the device, so it is complete iff *total_dev <= capacity; the
    caller reads *total_dev afterwards and, on overflow, grows the pools and
    gathers again with sk_jagged_scatter. Scratch: at least sk_jagged_scratch_bytes;
-   with (capacity / 2048 + 1) * 8 more bytes after it (256-aligned) the call
-   allocates nothing. */
+   with (ceil(capacity / 256) + 1) * 8 more bytes after it (256-aligned) the
+   call allocates nothing (the scan writes the gather's work split there). */
 int sk_jagged_pack(int64_t n, const void* lens, int lens_type, void* prefix,
                    int prefix_type, const int64_t* src_off, const void* src_pool,
                    int64_t member_stride, int nfields, const int64_t* field_off,
                    const int32_t* field_size, void* const* dst_pools, int64_t capacity,
                    void* scratch, size_t scratch_bytes, int64_t* total_dev,
                    uintptr_t stream);
+/* Sharded jagged collections (no reference counterpart -- the
+   reference has no sharding): after each shard packed locally and the shard
+   totals were exclusive-scanned across ranks, prefix[0..count) += offset in
+   the index dtype's modular arithmetic, which makes the shard's prefix the
+   exact slice of the unsharded np.cumsum(...).astype(idx)
+   (collection.py:553-554). */
+int sk_jagged_rebase(int64_t count, void* prefix, int prefix_type, int64_t offset,
+                     uintptr_t stream);
 
 /* ---- behavior plugin: the case-study per-object kernel (detector/schemas.py) */
 /* energy = A * f32(counts) + B, two f32 roundings, no FMA

@@ -613,6 +613,17 @@ __global__ void __launch_bounds__(GA_WARPS * 32) gather_async_kernel(const __gri
   if (lane == 0) bulk_wait_read<0>();  // shared memory stays valid until the last bulk store has read it
 }
 
+// shard rebase: P[i] += offset in the index dtype's modular
+// arithmetic -- the truncation of (local cumsum + offset) equals the
+// truncation of the global cumsum, so a rebased shard prefix is exactly the
+// slice of the unsharded one
+template <class PT>
+__global__ void __launch_bounds__(256) rebase_kernel(int64_t count, PT* __restrict__ p, uint64_t offset) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < count; i += stride)
+    p[i] = static_cast<PT>(static_cast<uint64_t>(p[i]) + offset);
+}
+
 }  // namespace jag
 }  // namespace sk
 
@@ -725,6 +736,7 @@ static int gather_args(jag::ScatterArgs* A, int64_t n, const void* prefix, int p
   }
   return SK_OK;
 }
+
 
 }  // extern "C"
 
@@ -872,3 +884,30 @@ int sk_jagged_pack(int64_t n, const void* lens, int lens_type, void* prefix, int
 }
 
 }  // extern "C"
+
+template <class PT>
+static int launch_rebase(int64_t count, void* p, int64_t offset, cudaStream_t s, const DeviceState* ds) {
+  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((count + 255) / 256, ds->sm_count * 8ll));
+  jag::rebase_kernel<PT><<<static_cast<unsigned>(blocks), 256, 0, s>>>(count, static_cast<PT*>(p),
+                                                                        static_cast<uint64_t>(offset));
+  SK_TRY(cudaGetLastError());
+  return SK_OK;
+}
+
+extern "C" int sk_jagged_rebase(int64_t count, void* prefix, int prefix_type, int64_t offset, uintptr_t stream) {
+  if (count < 0) return set_error(SK_ERR_INVALID, "negative count");
+  if (!int_type(prefix_type) || prefix_type == SK_BOOL) return set_error(SK_ERR_INVALID, "prefix needs an integer type");
+  if (count == 0 || offset == 0) return SK_OK;
+  if (!prefix) return set_error(SK_ERR_INVALID, "null prefix");
+  int dev = 0;
+  SK_TRY(cudaGetDevice(&dev));
+  DeviceState* ds = nullptr;
+  if (int rc = device_state(dev, &ds)) return rc;
+  cudaStream_t s = resolve_stream(dev, stream);
+  switch (prefix_type) {
+    case SK_U8: return launch_rebase<uint8_t>(count, prefix, offset, s, ds);
+    case SK_U16: return launch_rebase<uint16_t>(count, prefix, offset, s, ds);
+    case SK_U32: case SK_I32: return launch_rebase<uint32_t>(count, prefix, offset, s, ds);
+    default: return launch_rebase<uint64_t>(count, prefix, offset, s, ds);
+  }
+}

@@ -55,8 +55,51 @@ def jagged_shard_offset(local_total: int, group=None) -> tuple[int, int]:
 
 def rebase_prefix(prefix, offset: int):
     """A shard's local prefix [0, l1, ..] shifted to global positions; its first
-    entry equals the previous shard's last (numpy/int64 semantics)."""
+    entry equals the previous shard's last. Host arrays: numpy, in the index
+    dtype's modular arithmetic (the truncation of local cumsum + offset equals
+    the truncation of the global cumsum, collection.py:553-554)."""
+    import numpy as np
+
+    prefix = np.asarray(prefix)
+    if prefix.dtype.kind in "iu":
+        with np.errstate(over="ignore"):
+            return (prefix.astype(np.uint64) + np.uint64(offset % (1 << 64))).astype(prefix.dtype)
     return prefix + offset
+
+
+def global_prefix(coll, path: str, offset: int):
+    """The shard's prefix sums of jagged vector `path` rebased by `offset` (from
+    jagged_shard_offset): a new array, the collection itself keeps P[0] = 0.
+    Device-resident collections get a DeviceArray rebased on the device
+    (sk_jagged_rebase); host collections a numpy array."""
+    import numpy as np
+
+    from . import memctx
+    from .devarray import DeviceArray
+
+    pleaf = coll.plan.leaf(path + ".prefix_sum")
+    vt = pleaf.value_type
+    n = coll.size()
+    lay = coll.layout
+    if lay.host_visible:
+        return rebase_prefix(np.array(coll.prefix_sums(path), copy=True), offset)
+    dev = lay.device
+    out = DeviceArray(n + 1, vt.np_dtype, memctx.ContextInfo.cuda(dev))
+    nat.memcpy(out.ptr, lay.plane_address(pleaf, 0), (n + 1) * vt.size_bytes, dev)
+    nat.call("sk_jagged_rebase", n + 1, out.ptr, nat.TYPE_CODES[vt.storage_code], int(offset), nat.stream(dev))
+    nat.sync(dev)
+    return out
+
+
+def pack_sharded(coll, path: str, lens, src_offsets, src_pool, group=None, **member_layout):
+    """SURVEY 8e for jagged collections: pack this rank's shard locally (K4),
+    one all-gather of the shard totals, then the shard's global prefix.
+    Returns (global prefix of this shard, member offset, global total)."""
+    from . import jagged
+
+    local = jagged.pack(coll, path, lens, src_offsets, src_pool, **member_layout)
+    offset, total = jagged_shard_offset(local, group)
+    return global_prefix(coll, path, offset), offset, total
 
 
 # ---- whole collections across processes (layout-changing peer pulls) ----------------------

@@ -44,3 +44,14 @@ def test_jagged_shards_rebase_to_the_unsharded_prefix():
         assert total == int(lens.sum())
         assert np.array_equal(prefix, full[lo : hi + 1])  # first entry = previous shard's last
     assert res[0][1] == res[1][0]
+
+
+def test_rebase_wraps_like_the_unsharded_cast():
+    # u16 index: the global prefix passes 65535; each shard's rebased prefix must
+    # equal the slice of cumsum(int64).astype(u16) (collection.py:553-554)
+    lens = np.random.default_rng(5).integers(0, 200, 1500)
+    full = np.concatenate([[0], np.cumsum(lens)]).astype(np.uint16)
+    cut = 700
+    p1 = np.concatenate([[0], np.cumsum(lens[cut:])]).astype(np.uint16)  # shard 1's local prefix, wrapped
+    off = int(lens[:cut].sum())
+    assert np.array_equal(shard.rebase_prefix(p1, off), full[cut:])
