@@ -13,6 +13,7 @@ constexpr int NT = 256;
 constexpr int MAX_WORDS = 256;     // word table -> AoS strides up to 1 KiB use word moves
 constexpr int TILE_TARGET = 49152; // in+out bytes per tile (sweep: profiles/r01_sweep.md)
 constexpr int MAX_STAGES = 4;
+constexpr int MAX_SUBWORD = 16;    // AoS words made of 1-/2-byte fields the word path splits / assembles
 
 enum { MODE_ELEM = 0, MODE_WORD_A2P = 1, MODE_WORD_P2A = 2 };
 enum { EPI_NONE = 0, EPI_SENSOR = 1 };
@@ -59,7 +60,13 @@ struct Plan {
   uint8_t elem_idx[SK_MAX_FIELDS];
   int32_t cache_hint;       // 0 none, 1 evict_first on loads and stores, 2 loads only
   FieldPlan f[SK_MAX_FIELDS];
-  int32_t wtab[MAX_WORDS];  // (segment byte base << 4) | element size ; -1 = not a word-moved word
+  int32_t wtab[MAX_WORDS];  // (segment byte base << 4) | element size ; -1 = not a word-moved word;
+                            // -2 - k = sub-word slot k of btab
+  // sub-word slots: a word of the AoS record holding 1-/2-byte fields, moved as
+  // one word and split (A2P) / assembled (P2A); parts (base << 4) | (size << 2) | byte, -1 unused
+  int32_t btab[MAX_SUBWORD][4];
+  int32_t nsub;                  // sub-word slots in use and the record word each one is
+  int32_t bword[MAX_SUBWORD];
 };
 
 static_assert(sizeof(Plan) < 4000, "kernel parameter block must stay under 4 KB");
@@ -350,74 +357,160 @@ __device__ __forceinline__ void elem_field(const Plan& P, const FieldPlan& F, co
 }
 
 // ---------------------------------------------------------------------------------
+// sub-word slots of the word path
+
+// plane-side byte address of element r of a field at `base`: a planes segment
+// (GEO false) or an AoSoA tile block (GEO true)
+template <bool GEO>
+__device__ __forceinline__ int paddr(int base, int r, int isz, int lsh, int A, int msk) {
+  if (GEO) return base + ((r >> lsh) * A) + ((r & msk) * isz);
+  return base + r * isz;
+}
+
+template <bool GEO>
+__device__ __forceinline__ void subword_put(uint32_t v, uint8_t* out, int r, int32_t p, int lsh, int A, int msk) {
+  if (p < 0) return;
+  const int base = p >> 4, sz = (p >> 2) & 3, sh = (p & 3) * 8;
+  if (sz == 1) out[paddr<GEO>(base, r, 1, lsh, A, msk)] = static_cast<uint8_t>(v >> sh);
+  else *reinterpret_cast<uint16_t*>(out + paddr<GEO>(base, r, 2, lsh, A, msk)) = static_cast<uint16_t>(v >> sh);
+}
+
+template <bool GEO>
+__device__ __forceinline__ uint32_t subword_get(const uint8_t* in, int r, int32_t p, int lsh, int A, int msk) {
+  if (p < 0) return 0u;
+  const int base = p >> 4, sz = (p >> 2) & 3, sh = (p & 3) * 8;
+  const uint32_t x =
+      sz == 1 ? static_cast<uint32_t>(in[paddr<GEO>(base, r, 1, lsh, A, msk)])
+              : static_cast<uint32_t>(*reinterpret_cast<const uint16_t*>(in + paddr<GEO>(base, r, 2, lsh, A, msk)));
+  return x << sh;
+}
+
+// A2P: AoS words -> planes / AoSoA; P2A: planes / AoSoA -> AoS words.
+template <bool A2P, bool GEO>
+__device__ __forceinline__ void word_moves(const Plan& P, const uint8_t* __restrict__ in, uint8_t* __restrict__ out,
+                                           int rows, const int32_t* __restrict__ wtab) {
+  const int tid = threadIdx.x;
+  const int lsh = A2P ? P.dst_lshift : P.src_lshift;
+  const int A = A2P ? P.dst_A : P.src_A;
+  const int msk = A2P ? P.dst_msk : P.src_msk;
+  const int wpr = P.words_per_rec;
+  const int total = rows * wpr;
+  const int per = NT / wpr;   // records per pass when every active thread owns one word slot
+  const int nta = per * wpr;  // active threads in that mode
+  if (per >= 1 && 4 * nta >= 3 * NT) {
+    // fixed word slot per thread (all NT threads when NT is a multiple of the
+    // record's word count, else the largest multiple): every word this thread
+    // touches sits at the same record slot q, so the table entry is loop
+    // invariant and the loop is a pure, unrolled LDS->STS stream (4 loads in
+    // flight per thread). Sub-word slots are left to their own pass.
+    if (tid >= nta) return;
+    int r = tid / wpr;
+    const int q = tid - r * wpr;
+    const int e = wtab[q];
+    if (e < 0) return;
+    const int base = e >> 4, isz = e & 15;
+    int w = tid;
+    if (A2P) {
+      const uint32_t* in32 = reinterpret_cast<const uint32_t*>(in);
+      for (; w + 3 * nta < total; w += 4 * nta, r += 4 * per) {
+        const uint32_t v0 = in32[w], v1 = in32[w + nta], v2 = in32[w + 2 * nta], v3 = in32[w + 3 * nta];
+        *reinterpret_cast<uint32_t*>(out + paddr<GEO>(base, r, isz, lsh, A, msk)) = v0;
+        *reinterpret_cast<uint32_t*>(out + paddr<GEO>(base, r + per, isz, lsh, A, msk)) = v1;
+        *reinterpret_cast<uint32_t*>(out + paddr<GEO>(base, r + 2 * per, isz, lsh, A, msk)) = v2;
+        *reinterpret_cast<uint32_t*>(out + paddr<GEO>(base, r + 3 * per, isz, lsh, A, msk)) = v3;
+      }
+      for (; w < total; w += nta, r += per)
+        *reinterpret_cast<uint32_t*>(out + paddr<GEO>(base, r, isz, lsh, A, msk)) = in32[w];
+    } else {
+      uint32_t* out32 = reinterpret_cast<uint32_t*>(out);
+      for (; w + 3 * nta < total; w += 4 * nta, r += 4 * per) {
+        const uint32_t v0 = *reinterpret_cast<const uint32_t*>(in + paddr<GEO>(base, r, isz, lsh, A, msk));
+        const uint32_t v1 = *reinterpret_cast<const uint32_t*>(in + paddr<GEO>(base, r + per, isz, lsh, A, msk));
+        const uint32_t v2 = *reinterpret_cast<const uint32_t*>(in + paddr<GEO>(base, r + 2 * per, isz, lsh, A, msk));
+        const uint32_t v3 = *reinterpret_cast<const uint32_t*>(in + paddr<GEO>(base, r + 3 * per, isz, lsh, A, msk));
+        out32[w] = v0;
+        out32[w + nta] = v1;
+        out32[w + 2 * nta] = v2;
+        out32[w + 3 * nta] = v3;
+      }
+      for (; w < total; w += nta, r += per)
+        out32[w] = *reinterpret_cast<const uint32_t*>(in + paddr<GEO>(base, r, isz, lsh, A, msk));
+    }
+    return;
+  }
+  int r = tid / wpr;
+  int q = tid - r * wpr;
+  const int dr = NT / wpr;
+  const int dq = NT - dr * wpr;
+  for (int w = tid; w < total; w += NT) {
+    const int e = wtab[q];
+    if (e >= 0) {
+      const int a = paddr<GEO>(e >> 4, r, e & 15, lsh, A, msk);
+      if (A2P) *reinterpret_cast<uint32_t*>(out + a) = reinterpret_cast<const uint32_t*>(in)[w];
+      else reinterpret_cast<uint32_t*>(out)[w] = *reinterpret_cast<const uint32_t*>(in + a);
+    }
+    q += dq;
+    r += dr;
+    if (q >= wpr) { q -= wpr; ++r; }
+  }
+}
+
+// sub-word slots as their own pass over (record, slot) pairs on all threads
+// (inside the fixed-slot loop only a few lanes per warp would own such a slot
+// and every warp would run both loops back to back); uncovered bytes of an
+// assembled word come out zero (the zero_out contract)
+template <bool A2P, bool GEO>
+__device__ __forceinline__ void subword_moves(const Plan& P, const uint8_t* __restrict__ in,
+                                              uint8_t* __restrict__ out, int rows) {
+  const int lsh = A2P ? P.dst_lshift : P.src_lshift;
+  const int A = A2P ? P.dst_A : P.src_A;
+  const int msk = A2P ? P.dst_msk : P.src_msk;
+  const int wpr = P.words_per_rec, ns = P.nsub;
+  const int pairs = rows * ns;
+  for (int i = threadIdx.x; i < pairs; i += NT) {
+    const int r = i / ns, k = i - r * ns;
+    const int32_t* pt = P.btab[k];
+    if (A2P) {
+      const uint32_t v = reinterpret_cast<const uint32_t*>(in)[r * wpr + P.bword[k]];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) subword_put<GEO>(v, out, r, pt[j], lsh, A, msk);
+    } else {
+      uint32_t v = 0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) v |= subword_get<GEO>(in, r, pt[j], lsh, A, msk);
+      reinterpret_cast<uint32_t*>(out)[r * wpr + P.bword[k]] = v;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------
 // in-smem transposition
 
 __device__ __forceinline__ void transform(const Plan& P, const uint8_t* __restrict__ in, uint8_t* __restrict__ out,
                                           int rows, const int32_t* __restrict__ wtab) {
   const int tid = threadIdx.x;
   if (P.mode != MODE_ELEM) {
-    // word moves: iterate over the words of the AoS side (conflict-free there);
-    // the planes side is staggered 16 B per segment so 8 lanes x 4 records hit
-    // distinct banks.
-    const int wpr = P.words_per_rec;
-    const int total = rows * wpr;
-    int r = tid / wpr;
-    int q = tid - r * wpr;
-    const int dr = NT / wpr;
-    const int dq = NT - dr * wpr;
-    if (dq == 0) {
-      // NT is a multiple of the record's word count: every word this thread
-      // touches sits at the same record slot q, so the table entry is loop
-      // invariant and the loop is a pure, unrolled LDS->STS stream (4 loads in
-      // flight per thread).
-      const int e = wtab[q];
-      if (e >= 0) {
-        const int base = e >> 4, isz = e & 15;
-        if (P.mode == MODE_WORD_A2P) {
-          const uint32_t* in32 = reinterpret_cast<const uint32_t*>(in);
-          int w = tid;
-          for (; w + 3 * NT < total; w += 4 * NT, r += 4 * dr) {
-            const uint32_t v0 = in32[w], v1 = in32[w + NT], v2 = in32[w + 2 * NT], v3 = in32[w + 3 * NT];
-            *reinterpret_cast<uint32_t*>(out + base + r * isz) = v0;
-            *reinterpret_cast<uint32_t*>(out + base + (r + dr) * isz) = v1;
-            *reinterpret_cast<uint32_t*>(out + base + (r + 2 * dr) * isz) = v2;
-            *reinterpret_cast<uint32_t*>(out + base + (r + 3 * dr) * isz) = v3;
-          }
-          for (; w < total; w += NT, r += dr) *reinterpret_cast<uint32_t*>(out + base + r * isz) = in32[w];
-        } else {
-          uint32_t* out32 = reinterpret_cast<uint32_t*>(out);
-          int w = tid;
-          for (; w + 3 * NT < total; w += 4 * NT, r += 4 * dr) {
-            const uint32_t v0 = *reinterpret_cast<const uint32_t*>(in + base + r * isz);
-            const uint32_t v1 = *reinterpret_cast<const uint32_t*>(in + base + (r + dr) * isz);
-            const uint32_t v2 = *reinterpret_cast<const uint32_t*>(in + base + (r + 2 * dr) * isz);
-            const uint32_t v3 = *reinterpret_cast<const uint32_t*>(in + base + (r + 3 * dr) * isz);
-            out32[w] = v0;
-            out32[w + NT] = v1;
-            out32[w + 2 * NT] = v2;
-            out32[w + 3 * NT] = v3;
-          }
-          for (; w < total; w += NT, r += dr) out32[w] = *reinterpret_cast<const uint32_t*>(in + base + r * isz);
-        }
-      }
-    } else if (P.mode == MODE_WORD_A2P) {
-      const uint32_t* in32 = reinterpret_cast<const uint32_t*>(in);
-      for (int w = tid; w < total; w += NT) {
-        const int e = wtab[q];
-        if (e >= 0) *reinterpret_cast<uint32_t*>(out + (e >> 4) + r * (e & 15)) = in32[w];
-        q += dq;
-        r += dr;
-        if (q >= wpr) { q -= wpr; ++r; }
-      }
+    // word moves; the non-AoS side is planes (segment + r * size) or AoSoA
+    // tiles ((r >> lshift) * tile + (r & lanes-1) * size + block)
+    const bool a2p = P.mode == MODE_WORD_A2P;
+    const bool geo = a2p ? P.dst_kind == SK_KIND_AOSOA : P.src_kind == SK_KIND_AOSOA;
+    if (a2p) {
+      if (geo) word_moves<true, true>(P, in, out, rows, wtab);
+      else word_moves<true, false>(P, in, out, rows, wtab);
     } else {
-      uint32_t* out32 = reinterpret_cast<uint32_t*>(out);
-      for (int w = tid; w < total; w += NT) {
-        const int e = wtab[q];
-        if (e >= 0) out32[w] = *reinterpret_cast<const uint32_t*>(in + (e >> 4) + r * (e & 15));
-        q += dq;
-        r += dr;
-        if (q >= wpr) { q -= wpr; ++r; }
-      }
+      if (geo) word_moves<false, true>(P, in, out, rows, wtab);
+      else word_moves<false, false>(P, in, out, rows, wtab);
+    }
+  }
+  if (P.nsub) {
+    const bool a2p = P.mode == MODE_WORD_A2P;
+    const bool geo = a2p ? P.dst_kind == SK_KIND_AOSOA : P.src_kind == SK_KIND_AOSOA;
+    if (a2p) {
+      if (geo) subword_moves<true, true>(P, in, out, rows);
+      else subword_moves<true, false>(P, in, out, rows);
+    } else {
+      if (geo) subword_moves<false, true>(P, in, out, rows);
+      else subword_moves<false, false>(P, in, out, rows);
     }
   }
   if (!P.n_elem) return;
