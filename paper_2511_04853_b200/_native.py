@@ -13,7 +13,8 @@ import threading
 
 from . import errors as E
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libsoakit_b200.so")
+LIB_PATH = os.environ.get("SK_LIB_PATH") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib",
+                                                          "libsoakit_b200.so")  # override: A/B builds
 
 # status codes (soakit_b200.h)
 SK_OK = 0

@@ -65,6 +65,7 @@ struct Plan {
   // sub-word slots: a word of the AoS record holding 1-/2-byte fields, moved as
   // one word and split (A2P) / assembled (P2A); parts (base << 4) | (size << 2) | byte, -1 unused
   int32_t btab[MAX_SUBWORD][4];
+  int32_t issue_lanes;           // 32: warp 0 issues the bulk segment copies in parallel; 1: thread 0 alone
   int32_t nsub;                  // sub-word slots in use and the record word each one is
   int32_t bword[MAX_SUBWORD];
 };
@@ -216,15 +217,22 @@ __device__ __forceinline__ void s2g(const Plan& P, void* g, const void* s, uint3
   else bulk_s2g_plain(g, s, bytes);
 }
 
-static __device__ void issue_bulk_load(const Plan& P, int64_t t, uint8_t* in, uint64_t* bar, uint64_t pol) {
+// issued by P.issue_lanes threads (thread 0 alone, or the 32 lanes of warp 0):
+// lane 0 arms the barrier, then every lane sends its share of the segments
+template <int NL>
+static __device__ __forceinline__ void issue_bulk_load(const Plan& P, int64_t t, uint8_t* in, uint64_t* bar,
+                                                       uint64_t pol) {
+  const int lane = NL > 1 ? (threadIdx.x & 31) : 0;
+  constexpr int nl = NL;
   const int64_t r0 = t * P.R;
-  mbar_expect_tx(bar, static_cast<uint32_t>(P.in_tile_bytes));
+  if (lane == 0) mbar_expect_tx(bar, static_cast<uint32_t>(P.in_tile_bytes));
+  if (nl > 1) __syncwarp();
   if (P.src_kind == SK_KIND_PLANES) {
-    for (int i = 0; i < P.nfields; ++i) {
+    for (int i = lane; i < P.nfields; i += nl) {
       const FieldPlan& F = P.f[i];
       g2s(P, in + F.sloc, F.splane + r0 * F.sisz, static_cast<uint32_t>(P.R * F.sisz), bar, pol);
     }
-  } else {
+  } else if (lane == 0) {
     const int64_t off = P.src_kind == SK_KIND_AOS ? r0 * P.src_stride : (r0 >> P.src_lshift) * P.src_stride;
     g2s(P, in, P.src + off, static_cast<uint32_t>(P.in_tile_bytes), bar, pol);
   }
@@ -243,18 +251,24 @@ static __device__ void coop_load(const Plan& P, int64_t t, int rows, uint8_t* in
   }
 }
 
-static __device__ void issue_bulk_store(const Plan& P, int64_t t, const uint8_t* out, uint64_t pol) {
+// same issuing threads; each commits its own bulk group
+template <int NL>
+static __device__ __forceinline__ void issue_bulk_store(const Plan& P, int64_t t, const uint8_t* out, uint64_t pol) {
+  const int lane = NL > 1 ? (threadIdx.x & 31) : 0;
+  constexpr int nl = NL;
   const int64_t r0 = t * P.R;
   if (P.dst_kind == SK_KIND_PLANES) {
-    for (int i = 0; i < P.nfields; ++i) {
+    for (int i = lane; i < P.nfields; i += nl) {
       const FieldPlan& F = P.f[i];
       s2g(P, F.dplane + r0 * F.disz, out + F.dloc, static_cast<uint32_t>(P.R * F.disz), pol);
     }
-  } else {
+  } else if (lane == 0) {
     const int64_t off = P.dst_kind == SK_KIND_AOS ? r0 * P.dst_stride : (r0 >> P.dst_lshift) * P.dst_stride;
     s2g(P, P.dst + off, out, static_cast<uint32_t>(P.out_tile_bytes), pol);
   }
-  if (P.extra_plane) s2g(P, P.extra_plane + r0 * 4, out + P.extra_loc, static_cast<uint32_t>(P.R * 4), pol);
+  if (P.extra_plane && lane == nl - 1)
+    s2g(P, P.extra_plane + r0 * 4, out + P.extra_loc, static_cast<uint32_t>(P.R * 4), pol);
+  bulk_commit();
 }
 
 static __device__ void coop_store(const Plan& P, int64_t t, int rows, const uint8_t* out) {
@@ -556,8 +570,10 @@ struct GenericTransform {
   }
 };
 
-template <class T>
-__global__ void __launch_bounds__(NT) convert_kernel_t(const __grid_constant__ Plan P) {
+// NL: threads that issue the bulk segment copies (1: thread 0; 32: warp 0), a
+// compile-time choice so the single-issuer loop stays exactly a plain loop
+template <class T, int NL>
+__device__ __forceinline__ void convert_body(const Plan& P) {
   extern __shared__ __align__(128) uint8_t smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + P.smem_bar_off);
   int32_t* wtab = reinterpret_cast<int32_t*>(smem + P.smem_tab_off);
@@ -583,10 +599,11 @@ __global__ void __launch_bounds__(NT) convert_kernel_t(const __grid_constant__ P
 
   auto tile_bulk_in = [&](int64_t t) { return P.bulk_in && (t != last_tile || last_rows == P.R); };
 
-  if (tid == 0) {
+  const bool issuer = tid < NL;
+  if (issuer) {
     for (int s = 0; s < S && s < my_tiles; ++s) {
       const int64_t t = first + s * step;
-      if (tile_bulk_in(t)) issue_bulk_load(P, t, in0 + s * P.in_stage_stride, &bars[s], pol_in);
+      if (tile_bulk_in(t)) issue_bulk_load<NL>(P, t, in0 + s * P.in_stage_stride, &bars[s], pol_in);
     }
   }
 
@@ -604,7 +621,7 @@ __global__ void __launch_bounds__(NT) convert_kernel_t(const __grid_constant__ P
     } else {
       coop_load(P, t, rows, in);
     }
-    if (tid == 0) bulk_wait_read<1>();  // out[it&1] no longer read by the store of tile it-2
+    if (issuer) bulk_wait_read<1>();  // out[it&1] no longer read by the store of tile it-2 (every issuer)
     __syncthreads();
     if (P.zero_out || (rows < P.R && P.dst_kind == SK_KIND_AOSOA)) {
       uint32_t* o32 = reinterpret_cast<uint32_t*>(out);
@@ -620,20 +637,23 @@ __global__ void __launch_bounds__(NT) convert_kernel_t(const __grid_constant__ P
     if (bout) fence_proxy_async();
     __syncthreads();
     if (bout) {
-      if (tid == 0) {
-        issue_bulk_store(P, t, out, pol_out);
-        bulk_commit();
-      }
+      if (issuer) issue_bulk_store<NL>(P, t, out, pol_out);
     } else {
       coop_store(P, t, rows, out);
     }
-    if (tid == 0 && it + S < my_tiles) {
+    if (issuer && it + S < my_tiles) {
       const int64_t tn = first + (it + S) * step;
-      if (tile_bulk_in(tn)) issue_bulk_load(P, tn, in, &bars[slot], pol_in);
+      if (tile_bulk_in(tn)) issue_bulk_load<NL>(P, tn, in, &bars[slot], pol_in);
     }
     if (++slot == S) slot = 0;
   }
-  if (tid == 0) bulk_wait_all();
+  if (issuer) bulk_wait_all();
+}
+
+template <class T>
+__global__ void __launch_bounds__(NT) convert_kernel_t(const __grid_constant__ Plan P) {
+  if (P.issue_lanes == 32) convert_body<T, 32>(P);
+  else convert_body<T, 1>(P);
 }
 
 }  // namespace conv

@@ -391,6 +391,17 @@ int make_plan(const sk_conv_desc& d, const DeviceState& ds, bool in_bulk_ok, boo
   }
   P.bulk_in = bin;
   P.bulk_out = bout;
+  // who issues the per-segment bulk copies, measured per path on B200
+  // (profiles/r01_path_survey.md): the 32 lanes of warp 0 in parallel for
+  // word-mode AoS <-> planes (Obj8 0.97 -> 0.99, Track/Particle planes->AoS
+  // +3-5%); thread 0 alone for element-mode and AoSoA-side plans (Sensor
+  // planes->AoS 0.94 -> 1.00, AoSoA->AoS 0.78 -> 0.84)
+  {
+    const bool word_planes = (P.mode == MODE_WORD_A2P && d.dst_kind == SK_KIND_PLANES) ||
+                             (P.mode == MODE_WORD_P2A && d.src_kind == SK_KIND_PLANES);
+    P.issue_lanes = word_planes ? 32 : 1;
+    if (const char* e = getenv("SK_ISSUE_LANES")) P.issue_lanes = atoi(e) == 32 ? 32 : 1;
+  }
   P.in_tile_bytes = in_exact;  // bytes a full tile brings in (tx count)
   // in-tile allocation span (segments incl. stagger)
   int32_t in_span = in_exact;
