@@ -196,6 +196,10 @@ int sk_jagged_pack(int64_t n, const void* lens, int lens_type, void* prefix,
 int sk_jagged_rebase(int64_t count, void* prefix, int prefix_type, int64_t offset,
                      uintptr_t stream);
 
+/* Diagnostics only: copies the fused pack's table-warp timestamps (recorded
+   when SK_FUSED_DBG has bit 8 set) into `host`. */
+int sk_jagged_trace(void* host, size_t bytes);
+
 /* ---- behavior plugin: the case-study per-object kernel (detector/schemas.py) */
 /* energy = A * f32(counts) + B, two f32 roundings, no FMA
    (calibrate_collection, detector/schemas.py:29-33). */

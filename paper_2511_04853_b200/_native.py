@@ -105,6 +105,7 @@ _SIGNATURES = {
     "sk_jagged_pack": [_I64, _P, _I, _P, _I, _P, _P, _I64, _I, C.POINTER(_I64), C.POINTER(C.c_int32), C.POINTER(_P),
                        _I64, _P, _SZ, _P, _U],
     "sk_jagged_rebase": [_I64, _P, _I, _I64, _U],
+    "sk_jagged_trace": [_P, _SZ],
     "sk_sensor_calibrate": [_I64, _P, _P, _P, _P, _U],
     "sk_sensor_noise": [_I64, _P, _P, _P, _P, _P, _U],
     "sk_sensor_convert_calibrate": [C.POINTER(ConvDesc), _I, _I, _I, _I, _I, _I, _I, _P, _I, _U],

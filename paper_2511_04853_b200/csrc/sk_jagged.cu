@@ -21,6 +21,7 @@
 // j + (src_off[c] - P[c]). The next window's loads are in flight while this
 // window's members are.
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <utility>
 
@@ -53,6 +54,15 @@ __device__ __forceinline__ int64_t load_int(const void* p, int type, int64_t i) 
   }
 }
 
+__device__ __forceinline__ int dtype_size_dev(int type) {
+  switch (type) {
+    case SK_U8: case SK_BOOL: return 1;
+    case SK_U16: return 2;
+    case SK_U32: case SK_I32: return 4;
+    default: return 8;
+  }
+}
+
 // int64 -> index dtype by truncation, exactly numpy astype on the cumsum
 __device__ __forceinline__ void store_int(void* p, int type, int64_t i, int64_t v) {
   switch (type) {
@@ -67,6 +77,18 @@ __device__ __forceinline__ uint64_t ld_acquire(const uint64_t* p) {
   uint64_t v;
   asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
+}
+
+// the look-back status words carry their value: nothing else is published
+// with them, so relaxed (L2-coherent, no L1 invalidation) access is enough
+__device__ __forceinline__ uint64_t ld_relaxed(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_relaxed(uint64_t* p, uint64_t v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
 __device__ __forceinline__ void st_release(uint64_t* p, uint64_t v) {
@@ -242,15 +264,15 @@ __global__ void __launch_bounds__(SCAN_NT) scan_lookback_kernel(int64_t n, const
   if (tid < 32) {
     int64_t excl = 0;
     if (tile == 0) {
-      if (lane == 0) st_release(&status[0], FLAG_P | (static_cast<uint64_t>(ts.agg) & VAL_MASK));
+      if (lane == 0) st_relaxed(&status[0], FLAG_P | (static_cast<uint64_t>(ts.agg) & VAL_MASK));
     } else {
-      if (lane == 0) st_release(&status[tile], FLAG_A | (static_cast<uint64_t>(ts.agg) & VAL_MASK));
+      if (lane == 0) st_relaxed(&status[tile], FLAG_A | (static_cast<uint64_t>(ts.agg) & VAL_MASK));
       int64_t end = tile - 1;  // look back over [end-31, end]
       while (true) {
         const int64_t idx = end - lane;
-        uint64_t st = idx >= 0 ? ld_acquire(&status[idx]) : FLAG_P;
+        uint64_t st = idx >= 0 ? ld_relaxed(&status[idx]) : FLAG_P;
         while (__any_sync(0xffffffffu, (st >> 62) == 0)) {
-          if ((st >> 62) == 0) st = ld_acquire(&status[idx]);
+          if ((st >> 62) == 0) st = ld_relaxed(&status[idx]);
         }
         const unsigned pmask = __ballot_sync(0xffffffffu, (st >> 62) == 2);
         int64_t v = static_cast<int64_t>(st & VAL_MASK);
@@ -264,7 +286,7 @@ __global__ void __launch_bounds__(SCAN_NT) scan_lookback_kernel(int64_t n, const
         if (pmask) break;
         end -= 32;
       }
-      if (lane == 0) st_release(&status[tile], FLAG_P | (static_cast<uint64_t>(excl + ts.agg) & VAL_MASK));
+      if (lane == 0) st_relaxed(&status[tile], FLAG_P | (static_cast<uint64_t>(excl + ts.agg) & VAL_MASK));
     }
     if (lane == 0) s_excl = excl;
   }
@@ -579,8 +601,8 @@ __global__ void __launch_bounds__(GA_WARPS * 32) gather_async_kernel(const __gri
     __syncwarp();
     const int b = it & 1;
     uint8_t* buf = stage_all[warp][b];
-    // the bulk store that last read this buffer (two tasks ago) must have finished reading it
-    if (lane == 0) bulk_wait_read<1>();
+    // the most recent bulk store (issued one task ago, draining task t - 2) read this buffer
+    if (lane == 0) bulk_wait_read<0>();
     __syncwarp();
     int cum = 0;
 #pragma unroll
@@ -611,6 +633,430 @@ __global__ void __launch_bounds__(GA_WARPS * 32) gather_async_kernel(const __gri
   cp_async_wait<0>();
   drain(prev_t, (it - 1) & 1);
   if (lane == 0) bulk_wait_read<0>();  // shared memory stays valid until the last bulk store has read it
+}
+
+// ---- fused pack: one persistent grid, one block of records per CTA --------------------
+//
+// The records are cut into one contiguous block per CTA (at most MAX_SUB
+// sub-tiles of R = 1024 records; larger inputs hand out several blocks per
+// CTA by ticket). Per block:
+//   1. all threads sum the block's lengths (coalesced) and publish the block
+//      total (status word); warp 0 then adds up every predecessor block's
+//      published total for the block's exclusive prefix E. Blocks publish
+//      after one pass over their own lengths, so this waits on no gather and
+//      on no chain of other blocks' prefixes;
+//   2. per sub-tile, all threads scan its lengths (4 consecutive records per
+//      thread, prefetched into registers while the previous sub-tile
+//      gathered) into smem tables -- local exclusive prefix Lx[r] and
+//      D[r] = src_off[r] - Lx[r] -- store P[r] = E_sub + Lx[r] truncated to
+//      the index dtype, and the warps claim the sub-tile's 256-member output
+//      windows one at a time (an smem counter) and gather them from the tables.
+// Output windows use the pool's global 256-member alignment: each window's
+// 16-byte-aligned body leaves in one bulk store, and a window shared with a
+// neighbour sub-tile is split at its ends, the ragged edges stored by lanes.
+// Members go global -> shared with cp.async into a per-warp double buffer;
+// each warp's pipeline runs on across sub-tiles, so the sub-tile scans hide
+// behind members in flight.
+// A sub-tile with more than DEFER_PER_REC members per record on average is
+// not gathered by its owner: it is queued, and once every sub-tile is
+// accounted for all warps of all CTAs share the queued sub-tiles' windows
+// (each CTA rebuilds the tables), so skewed lengths cannot serialise on one CTA.
+
+// experiments only (sk_jagged_trace reads it; nothing writes it in this version)
+__device__ unsigned long long g_fused_trace[8 * 16 * 8];
+
+constexpr int F_NW = 8;             // warps per CTA
+constexpr int F_NT = 32 * F_NW;
+constexpr int F_RPT = 4;            // records per thread of a sub-tile
+constexpr int F_R = F_NT * F_RPT;   // records per sub-tile
+constexpr int MAX_SUB = 256;        // sub-tiles per block
+constexpr int64_t DEFER_PER_REC = 64;
+constexpr int DEFER_CHUNK = 16;     // windows per queued-sub-tile work item
+
+struct FusedHdr {
+  unsigned int ticket;
+  unsigned int finished;  // sub-tiles gathered or queued
+  unsigned int ndef;      // queued sub-tiles
+  unsigned int pad;
+};
+
+struct DeferEntry {
+  int64_t rec0;  // first record of the sub-tile
+  int64_t cnt;   // its records
+  int64_t E, A;
+  unsigned long long next;  // next chunk to hand out
+  unsigned long long pad[3];
+};
+
+struct FusedArgs {
+  int64_t n;
+  const void* lens;
+  int lens_type;
+  void* prefix;
+  int prefix_type;
+  int64_t* total;
+  const int64_t* src_off;
+  const uint8_t* src;   // pool + field offset
+  int64_t member_stride;
+  uint8_t* dst;         // 16-byte aligned
+  int64_t capacity;
+  int64_t block_recs;   // records per block (multiple of 4)
+  int64_t nblocks;
+  int64_t tiles;        // sub-tiles over all blocks
+  FusedHdr* hdr;
+  uint64_t* status;     // per block
+  DeferEntry* defer;
+  int pvec;             // 4-byte prefix, 16-byte aligned: vector prefix stores
+  int dbg;              // experiments only (SK_FUSED_DBG): 1 = no gather, 2 = no look-back
+};
+
+struct __align__(16) TileBuf {
+  int64_t D[F_R];           // src_off - Lx
+  int64_t Lx[F_R + 2];      // local exclusive prefix; Lx[F_R] = sub-tile total
+  int64_t coarse[32];       // Lx[32 k]: the first probe round of the record search
+};
+
+struct FusedSmem {
+  TileBuf tb;
+  int sRec[F_NW][W];        // per warp: rank -> record of the current window
+  int64_t warp_tot[F_NW];
+  int64_t item, E, A;
+  int next;                 // next window of the current sub-tile
+};
+
+template <int RPT>
+struct FRegs {
+  int64_t len[RPT], off[RPT];
+};
+
+// this thread's records of the sub-tile [r0, r0 + cnt) (clamped loads; masked in the scan)
+__device__ __forceinline__ void sub_load(const FusedArgs& F, int64_t r0, int cnt, FRegs<F_RPT>& g) {
+  const int e0 = threadIdx.x * F_RPT;
+#pragma unroll
+  for (int i = 0; i < F_RPT; ++i) {
+    const int64_t idx = r0 + min(e0 + i, max(cnt - 1, 0));
+    g.len[i] = e0 + i < cnt ? load_int(F.lens, F.lens_type, idx) : 0;
+    g.off[i] = F.src_off[idx];
+  }
+}
+
+// all threads: the loaded sub-tile -> tables; returns the sub-tile total.
+// incl[i] = tile-local inclusive prefix of this thread's records.
+__device__ __forceinline__ int64_t sub_scan(const FRegs<F_RPT>& g, FusedSmem& S, int64_t (&ex)[F_RPT]) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  int64_t acc = 0;
+#pragma unroll
+  for (int i = 0; i < F_RPT; ++i) acc += g.len[i];
+  int64_t x = acc;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) S.warp_tot[warp] = x;
+  __syncthreads();
+  int64_t woff = 0, agg = 0;
+#pragma unroll
+  for (int w = 0; w < F_NW; ++w) {
+    if (w < warp) woff += S.warp_tot[w];
+    agg += S.warp_tot[w];
+  }
+  int64_t run = woff + x - acc;
+  const int e0 = tid * F_RPT;
+#pragma unroll
+  for (int i = 0; i < F_RPT; ++i) {
+    ex[i] = run;
+    S.tb.Lx[e0 + i] = run;
+    S.tb.D[e0 + i] = g.off[i] - run;
+    run += g.len[i];
+  }
+  if (tid % (32 / F_RPT) == 0) S.tb.coarse[tid / (32 / F_RPT)] = ex[0];
+  if (tid == 0) S.tb.Lx[F_R] = agg;
+  return agg;
+}
+
+// P[r0 + e] = E + Lx[e] for this thread's records e < cnt, truncated to the index dtype
+__device__ __forceinline__ void sub_prefix(const FusedArgs& F, int64_t r0, int cnt, int64_t E,
+                                           const int64_t (&ex)[F_RPT]) {
+  const int e0 = threadIdx.x * F_RPT;
+  if (F.pvec && e0 + F_RPT <= cnt) {
+    *reinterpret_cast<uint4*>(static_cast<uint32_t*>(F.prefix) + r0 + e0) =
+        make_uint4(static_cast<uint32_t>(E + ex[0]), static_cast<uint32_t>(E + ex[1]),
+                   static_cast<uint32_t>(E + ex[2]), static_cast<uint32_t>(E + ex[3]));
+    return;
+  }
+#pragma unroll
+  for (int i = 0; i < F_RPT; ++i)
+    if (e0 + i < cnt) store_int(F.prefix, F.prefix_type, r0 + e0 + i, E + ex[i]);
+}
+
+// last record r in [0, F_R) with Lx[r] <= j (the record holding local member j)
+__device__ __forceinline__ int table_search(const TileBuf& B, int64_t j) {
+  const int lane = threadIdx.x & 31;
+  const unsigned m0 = __ballot_sync(0xffffffffu, B.coarse[lane] <= j);
+  const int lo = (31 - __clz(m0)) * 32;
+  const unsigned m1 = __ballot_sync(0xffffffffu, B.Lx[lo + lane] <= j);
+  return lo + (31 - __clz(m1));
+}
+
+// a warp's member pipeline: the window whose loads are in flight, drained
+// after the next window's loads are issued (possibly in a later tile)
+struct FPipe {
+  int it = 0;
+  int64_t w0 = -1, g0 = 0, g1 = 0;  // pending window (w0 < 0: none)
+};
+
+template <int MS>
+__device__ __forceinline__ void fdrain(const FusedArgs& F, const FPipe& p, const uint8_t* buf) {
+  using V = typename MemberWord<MS>::T;
+  const int lane = threadIdx.x & 31;
+  const int64_t a0 = (p.g0 * MS + 15) & ~int64_t(15), a1 = (p.g1 * MS) & ~int64_t(15);
+  fence_proxy_async();
+  __syncwarp();
+  if (lane == 0 && a1 > a0) {
+    bulk_s2g_plain(F.dst + a0, buf + (a0 - p.w0 * MS), static_cast<uint32_t>(a1 - a0));
+    bulk_commit();
+  }
+  const int64_t h1 = min(a0 / MS, p.g1), t0 = max(a1 / MS, h1);
+  for (int64_t g = p.g0 + lane; g < h1; g += 32)
+    *reinterpret_cast<V*>(F.dst + g * MS) = *reinterpret_cast<const V*>(buf + (g - p.w0) * MS);
+  for (int64_t g = t0 + lane; g < p.g1; g += 32)
+    *reinterpret_cast<V*>(F.dst + g * MS) = *reinterpret_cast<const V*>(buf + (g - p.w0) * MS);
+}
+
+template <int MS>
+__device__ __forceinline__ void fflush(const FusedArgs& F, FPipe& p, uint8_t (*stage)[W * MS]) {
+  if (p.w0 >= 0) {
+    cp_async_wait<0>();
+    fdrain<MS>(F, p, stage[(p.it - 1) & 1]);
+    p.w0 = -1;
+  }
+}
+
+// the warp gathers output window k of the tile whose members are [E, E + A)
+template <int MS>
+__device__ __forceinline__ void gather_window(const FusedArgs& F, const TileBuf& B, int64_t E, int64_t A, int64_t k,
+                                              int* sRec, uint8_t (*stage)[W * MS], FPipe& pp) {
+  const int lane = threadIdx.x & 31;
+  const unsigned le_mask = 0xffffffffu >> (31 - lane);
+  const int64_t w0 = k * W;
+  const int64_t g0 = max(w0, E), g1 = min(w0 + W, E + A);
+  const int64_t j0 = g0 - E, j1 = g1 - E;
+  const int sh = static_cast<int>(g0 - w0);
+  unsigned masks[W_CH];
+#pragma unroll
+  for (int q = 0; q < W_CH; ++q) masks[q] = 0;
+  int nr = 0;
+  for (int c0 = table_search(B, j0);; c0 += 32) {
+    const int c = min(c0 + lane, F_R);
+    const int64_t p = B.Lx[c], pn = B.Lx[c + 1];  // Lx[F_R + 1] is never used: c < F_R is checked
+    const bool ne = c0 + lane < F_R && pn > p && p < j1;
+    const unsigned bal = __ballot_sync(0xffffffffu, ne);
+    const int rank = nr + __popc(bal & (le_mask >> 1));
+    nr += __popc(bal);
+    const int s = ne ? static_cast<int>(max(p - j0, int64_t(0))) + sh : -1;
+    if (ne) sRec[rank] = c;
+#pragma unroll
+    for (int q = 0; q < W_CH; ++q) masks[q] |= __reduce_or_sync(0xffffffffu, (s >> 5) == q ? 1u << (s & 31) : 0u);
+    if (c0 + 32 >= F_R || B.Lx[c0 + 32] >= j1) break;
+  }
+  __syncwarp();
+  uint8_t* buf = stage[pp.it & 1];
+  // the last bulk store (issued one window ago) read this buffer: it must be done reading
+  if (lane == 0) bulk_wait_read<0>();
+  __syncwarp();
+  int cum = 0;
+#pragma unroll
+  for (int q = 0; q < W_CH; ++q) {
+    const int pos = 32 * q + lane;
+    const int r = cum + __popc(masks[q] & le_mask) - 1;
+    if (pos >= sh && w0 + pos < g1)
+      cp_async_member<MS>(buf + pos * MS, F.src + (w0 + pos - E + B.D[sRec[r]]) * F.member_stride);
+    cum += __popc(masks[q]);
+  }
+  cp_async_commit();
+  if (pp.w0 >= 0) {
+    cp_async_wait<1>();
+    fdrain<MS>(F, pp, stage[(pp.it - 1) & 1]);
+  }
+  pp.w0 = w0;
+  pp.g0 = g0;
+  pp.g1 = g1;
+  ++pp.it;
+  __syncwarp();  // sRec is rewritten by the next window
+}
+
+__device__ __forceinline__ int64_t first_window(int64_t E) { return E / W; }
+__device__ __forceinline__ int64_t end_window(int64_t E, int64_t A) { return (E + A + W - 1) / W; }
+
+
+// warp 0: exclusive prefix of block `blk` = the sum of every predecessor
+// block's published total (256 status words per round, no chain through
+// other blocks' prefixes; polls back off while a predecessor is still summing)
+__device__ __forceinline__ int64_t pred_sum(const FusedArgs& F, int64_t blk) {
+  const int lane = threadIdx.x & 31;
+  int64_t acc = 0;
+  for (int64_t e0 = 0; e0 < blk; e0 += 256) {
+    uint64_t st[8];
+    bool missing = false;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int64_t idx = e0 + q * 32 + lane;
+      st[q] = idx < blk ? ld_relaxed(&F.status[idx]) : FLAG_A;
+      missing |= (st[q] >> 62) == 0;
+    }
+    while (__any_sync(0xffffffffu, missing)) {
+      __nanosleep(200);
+      missing = false;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        if ((st[q] >> 62) == 0) st[q] = ld_relaxed(&F.status[e0 + q * 32 + lane]);
+        missing |= (st[q] >> 62) == 0;
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int64_t idx = e0 + q * 32 + lane;
+      if (idx < blk) acc += static_cast<int64_t>(st[q] & VAL_MASK);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  return acc;
+}
+
+
+template <int MS>
+__global__ void __launch_bounds__(F_NT, 2) pack_fused_kernel(const __grid_constant__ FusedArgs F) {
+  extern __shared__ __align__(128) uint8_t fsm[];
+  auto stage_all = reinterpret_cast<uint8_t(*)[2][W * MS]>(fsm);
+  FusedSmem& S = *reinterpret_cast<FusedSmem*>(fsm + F_NW * 2 * W * MS);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  auto stage = stage_all[warp];
+  int* sRec = S.sRec[warp];
+  FPipe pp;
+  FRegs<F_RPT> g;
+
+  while (true) {
+    if (tid == 0) S.item = atomicAdd(&F.hdr->ticket, 1u);
+    __syncthreads();  // also: every warp is done with the previous block's tables
+    const int64_t blk = S.item;
+    if (blk >= F.nblocks) break;
+    const int64_t rec0 = blk * F.block_recs, rec1 = min(F.n, rec0 + F.block_recs);
+    const int nsub = static_cast<int>((rec1 - rec0 + F_R - 1) / F_R);
+    // 1. the block total, published; the first sub-tile's records load meanwhile
+    int64_t acc = 0;
+    if (dtype_size_dev(F.lens_type) == 4) {
+      const bool sgn = F.lens_type == SK_I32;
+#pragma unroll 4
+      for (int64_t r = rec0 + tid; r < rec1; r += F_NT) {
+        const uint32_t v = static_cast<const uint32_t*>(F.lens)[r];
+        acc += sgn ? static_cast<int64_t>(static_cast<int32_t>(v)) : static_cast<int64_t>(v);
+      }
+    } else {
+      for (int64_t r = rec0 + tid; r < rec1; r += F_NT) acc += load_int(F.lens, F.lens_type, r);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) S.warp_tot[warp] = acc;
+    sub_load(F, rec0, static_cast<int>(min(static_cast<int64_t>(F_R), rec1 - rec0)), g);
+    __syncthreads();
+    if (warp == 0) {
+      int64_t Ab = 0;
+#pragma unroll
+      for (int w = 0; w < F_NW; ++w) Ab += S.warp_tot[w];
+      if (lane == 0) st_relaxed(&F.status[blk], FLAG_A | (static_cast<uint64_t>(Ab) & VAL_MASK));
+      const int64_t E = (F.dbg & 2) ? 0 : pred_sum(F, blk);
+      if (lane == 0) {
+        S.E = E;
+        if (rec1 == F.n) {  // the block holding the last record
+          store_int(F.prefix, F.prefix_type, F.n, E + Ab);
+          *F.total = E + Ab;
+        }
+      }
+    }
+    __syncthreads();  // S.E, and warp_tot is free again
+    int64_t run = S.E;
+    // 2. sub-tiles: scan, prefix, gather
+    for (int sb = 0; sb < nsub; ++sb) {
+      const int64_t r0 = rec0 + static_cast<int64_t>(sb) * F_R;
+      const int cnt = static_cast<int>(min(static_cast<int64_t>(F_R), rec1 - r0));
+      int64_t ex[F_RPT];
+      const int64_t A = sub_scan(g, S, ex);
+      const int64_t E = run;
+      run += A;
+      sub_prefix(F, r0, cnt, E, ex);
+      if (sb + 1 < nsub) {  // the next sub-tile's records fly while this one gathers
+        const int64_t r1 = r0 + F_R;
+        sub_load(F, r1, static_cast<int>(min(static_cast<int64_t>(F_R), rec1 - r1)), g);
+      }
+      // past the capacity: not gathered (the caller sees *total > capacity and redoes the pack)
+      const bool gather = A > 0 && E + A <= F.capacity && !(F.dbg & 1);
+      const bool queue = gather && A > DEFER_PER_REC * F_R;
+      if (tid == 0) {
+        if (queue) {
+          const unsigned slot = atomicAdd(&F.hdr->ndef, 1u);
+          F.defer[slot] = DeferEntry{r0, cnt, E, A, 0ull, {0ull, 0ull, 0ull}};
+          __threadfence();  // the entry is visible before the sub-tile counts as finished
+        }
+        atomicAdd(&F.hdr->finished, 1u);
+        S.next = 0;
+      }
+      __syncthreads();  // tables and the window counter are ready
+      if (gather && !queue) {
+        const int64_t k0 = first_window(E);
+        const int nwin = static_cast<int>(end_window(E, A) - k0);
+        while (true) {
+          int k = 0;
+          if (lane == 0) k = atomicAdd(&S.next, 1);
+          k = __shfl_sync(0xffffffffu, k, 0);
+          if (k >= nwin) break;
+          gather_window<MS>(F, S.tb, E, A, k0 + k, sRec, stage, pp);
+        }
+      }
+      __syncthreads();  // the tables are rewritten by the next sub-tile
+    }
+  }
+
+  // queued sub-tiles: once every sub-tile is accounted for (their owners are running), share them out
+  if (tid == 0) {
+    while (*reinterpret_cast<volatile unsigned int*>(&F.hdr->finished) < static_cast<unsigned int>(F.tiles))
+      __nanosleep(256);
+    __threadfence();
+    S.item = *reinterpret_cast<volatile unsigned int*>(&F.hdr->ndef);
+  }
+  __syncthreads();
+  const int64_t ndef = S.item;
+  int64_t have = -1;
+  for (int64_t d = 0; d < ndef; ++d) {
+    const DeferEntry ent = F.defer[d];
+    const int64_t k0 = first_window(ent.E), nwin = end_window(ent.E, ent.A) - k0;
+    const int64_t nchunks = (nwin + DEFER_CHUNK - 1) / DEFER_CHUNK;
+    while (true) {
+      __syncthreads();  // the previous chunk is done with S.item and the tables
+      if (tid == 0) S.item = static_cast<int64_t>(atomicAdd(&F.defer[d].next, 1ull));
+      __syncthreads();
+      const int64_t c = S.item;
+      if (c >= nchunks) break;
+      if (have != d) {
+        sub_load(F, ent.rec0, static_cast<int>(ent.cnt), g);
+        int64_t ex[F_RPT];
+        sub_scan(g, S, ex);
+        __syncthreads();
+        have = d;
+      }
+      const int64_t kb = k0 + c * DEFER_CHUNK, ke = min(kb + DEFER_CHUNK, k0 + nwin);
+      for (int64_t k = kb + warp; k < ke; k += F_NW)
+        gather_window<MS>(F, S.tb, ent.E, ent.A, k, sRec, stage, pp);
+    }
+  }
+  fflush<MS>(F, pp, stage);
+  if (lane == 0) bulk_wait_all();
+}
+
+template <int MS>
+constexpr size_t fused_smem() {
+  return static_cast<size_t>(F_NW) * 2 * W * MS + sizeof(FusedSmem);
 }
 
 // shard rebase: P[i] += offset in the index dtype's modular
@@ -648,10 +1094,17 @@ static cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, c
 
 extern "C" {
 
+// fused pack scratch: header, one look-back status word and one queue entry per
+// tile
+static size_t fused_scratch_bytes(int64_t n) {
+  const int64_t t = (n + jag::F_R - 1) / jag::F_R;  // blocks <= t, sub-tiles <= 2 t
+  return static_cast<size_t>(64 + ((t * 8 + 63) & ~int64_t(63)) + 2 * t * sizeof(jag::DeferEntry));
+}
+
 int sk_jagged_scratch_bytes(int64_t n, size_t* nbytes) {
   if (!nbytes) return set_error(SK_ERR_INVALID, "null out");
   const int64_t tiles = n > 0 ? (n + jag::SCAN_TILE - 1) / jag::SCAN_TILE : 0;
-  *nbytes = static_cast<size_t>(16 + tiles * 8);
+  *nbytes = std::max(static_cast<size_t>(16 + tiles * 8), n > 0 ? fused_scratch_bytes(n) : 0);
   return SK_OK;
 }
 
@@ -771,6 +1224,45 @@ static int launch_gather_async(const jag::ScatterArgs& A, int64_t ntasks, cudaSt
   return SK_OK;
 }
 
+template <int MS>
+static int launch_fused_ms(jag::FusedArgs F, uint8_t* scratch, cudaStream_t s, int dev, const DeviceState* ds) {
+  constexpr size_t smem = jag::fused_smem<MS>();
+  static int occ[64] = {0};
+  int& o = occ[dev & 63];
+  if (!o) {
+    SK_TRY(cudaFuncSetAttribute(jag::pack_fused_kernel<MS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(smem)));
+    SK_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, jag::pack_fused_kernel<MS>, jag::F_NT, smem));
+    o = std::max(o, 1);
+  }
+  // one block of records per CTA (a multiple of 4 records, at least one sub-tile, at most MAX_SUB)
+  const int64_t ctas = static_cast<int64_t>(ds->sm_count) * o;
+  int64_t br = (F.n + ctas - 1) / ctas;
+  br = std::max<int64_t>(jag::F_R, std::min<int64_t>((br + 3) & ~int64_t(3), int64_t(jag::MAX_SUB) * jag::F_R));
+  F.block_recs = br;
+  F.nblocks = (F.n + br - 1) / br;
+  const int64_t last = F.n - (F.nblocks - 1) * br;
+  F.tiles = (F.nblocks - 1) * ((br + jag::F_R - 1) / jag::F_R) + (last + jag::F_R - 1) / jag::F_R;
+  F.hdr = reinterpret_cast<jag::FusedHdr*>(scratch);
+  F.status = reinterpret_cast<uint64_t*>(scratch + 64);
+  const size_t status_bytes = (static_cast<size_t>(F.nblocks) * 8 + 63) & ~size_t(63);
+  F.defer = reinterpret_cast<jag::DeferEntry*>(scratch + 64 + status_bytes);
+  SK_TRY(cudaMemsetAsync(scratch, 0, 64 + status_bytes, s));
+  const int64_t grid = std::min<int64_t>(F.nblocks, ctas);
+  jag::pack_fused_kernel<MS><<<static_cast<unsigned>(grid), jag::F_NT, smem, s>>>(F);
+  SK_TRY(cudaGetLastError());
+  return SK_OK;
+}
+
+static bool fused_pack_ok() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SK_JAGGED_FUSED");
+    v = e ? atoi(e) : 1;
+  }
+  return v != 0;
+}
+
 static bool async_gather_ok() {
   static int v = -1;
   if (v < 0) {
@@ -853,6 +1345,32 @@ int sk_jagged_pack(int64_t n, const void* lens, int lens_type, void* prefix, int
     SK_TRY(cudaMemsetAsync(total_dev, 0, 8, s));
     return SK_OK;
   }
+  // single pass: one aligned 4/8-byte member field into a 16-byte-aligned pool
+  if (fused_pack_ok() && nfields == 1 && A.aligned[0] && (A.field_size[0] == 4 || A.field_size[0] == 8) &&
+      reinterpret_cast<uintptr_t>(A.dst[0]) % 16 == 0) {
+    DeviceState* ds = nullptr;
+    if (int rc = device_state(dev, &ds)) return rc;
+    jag::FusedArgs F{};
+    F.n = n;
+    F.lens = lens;
+    F.lens_type = lens_type;
+    F.prefix = prefix;
+    F.prefix_type = prefix_type;
+    F.total = total_dev;
+    F.src_off = src_off;
+    F.src = A.src_pool + A.field_off[0];
+    F.member_stride = member_stride;
+    F.dst = A.dst[0];
+    F.capacity = capacity;
+    F.pvec = dtype_size(prefix_type) == 4 && reinterpret_cast<uintptr_t>(prefix) % 16 == 0;
+    static const int dbg = [] {
+      const char* e = getenv("SK_FUSED_DBG");
+      return e ? atoi(e) : 0;
+    }();
+    F.dbg = dbg;
+    uint8_t* sc = static_cast<uint8_t*>(scratch);
+    return A.field_size[0] == 8 ? launch_fused_ms<8>(F, sc, s, dev, ds) : launch_fused_ms<4>(F, sc, s, dev, ds);
+  }
   // a prefix type that can wrap below the capacity needs an int64 copy for the gather
   const int bits = 8 * dtype_size(prefix_type) - ((prefix_type == SK_I32 || prefix_type == SK_I64) ? 1 : 0);
   const bool may_wrap = bits < 63 && capacity >= (int64_t(1) << bits);
@@ -891,6 +1409,13 @@ static int launch_rebase(int64_t count, void* p, int64_t offset, cudaStream_t s,
   jag::rebase_kernel<PT><<<static_cast<unsigned>(blocks), 256, 0, s>>>(count, static_cast<PT*>(p),
                                                                         static_cast<uint64_t>(offset));
   SK_TRY(cudaGetLastError());
+  return SK_OK;
+}
+
+// experiments only: copies the fused pack's table-warp timestamps to host memory
+extern "C" int sk_jagged_trace(void* host, size_t bytes) {
+  SK_TRY(cudaDeviceSynchronize());
+  SK_TRY(cudaMemcpyFromSymbol(host, jag::g_fused_trace, std::min(bytes, sizeof(jag::g_fused_trace))));
   return SK_OK;
 }
 

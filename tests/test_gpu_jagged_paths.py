@@ -59,7 +59,9 @@ def _pack(lens, offs, pool_bytes, stride, fields, ptype, cap_extra=0, dst_shift=
     foff = (C.c_int64 * nf)(*[o for o, _ in fields])
     fsz = (C.c_int32 * nf)(*[sz for _, sz in fields])
     dst = (C.c_void_p * nf)(*[o.ptr + dst_shift for o in outs])
-    nat.call("sk_jagged_pack", n, d_lens.ptr, TC["i32"], prefix.ptr, TC[ptype], d_offs.ptr, d_pool.ptr, stride, nf,
+    lcode = {np.dtype(np.int32): "i32", np.dtype(np.uint8): "u8", np.dtype(np.uint16): "u16",
+             np.dtype(np.int64): "i64", np.dtype(np.uint32): "u32"}[lens.dtype]
+    nat.call("sk_jagged_pack", n, d_lens.ptr, TC[lcode], prefix.ptr, TC[ptype], d_offs.ptr, d_pool.ptr, stride, nf,
              foff, fsz, dst, cap, scratch.ptr, scratch.n, total.ptr, nat.stream(0))
     nat.sync(0)
     t = int(total.numpy()[0])
@@ -153,3 +155,97 @@ def test_scatter_over_given_prefix():
     assert out.numpy().tobytes() == want[0]
     for a in (d_p, d_o, d_pool, out):
         a.free()
+
+
+# ---- fused single-pass pack (one aligned 4/8-byte field, 16-byte-aligned pool) ----
+
+def _skewed_inputs(n, seed):
+    """mostly short segments, one block of long ones (a tile over the queueing
+    threshold) and a single giant segment"""
+    rng = np.random.default_rng(seed)
+    lens = rng.integers(0, 6, n).astype(np.int32)
+    lens[1000:1700] = 2000          # ~1.4M members over two or three tiles: queued and shared out
+    lens[n // 2] = 700_000           # one record alone over the threshold
+    lens[n - 300:] = 0               # trailing empty records
+    order = rng.permutation(n)
+    gaps = lens[order].astype(np.int64) + rng.integers(0, 3, n)
+    offs = np.empty(n, np.int64)
+    offs[order] = np.concatenate([[0], np.cumsum(gaps)[:-1]])
+    return lens, offs, int(gaps.sum())
+
+
+@pytest.mark.parametrize("msize", [8, 4])
+def test_fused_pack_skewed_lengths_queue_path(msize):
+    lens, offs, plen = _skewed_inputs(200_000, seed=11)
+    pool = np.random.default_rng(12).integers(0, 256, plen * msize, dtype=np.uint8)
+    p, got, t = _pack(lens, offs, pool, msize, [(0, msize)], "i64", cap_extra=5)
+    pw, want, tw = _expect(lens, offs, pool, msize, [(0, msize)], "i64")
+    assert t == tw and p.tobytes() == pw.tobytes() and got == want
+
+
+def test_fused_pack_all_empty_and_single_record():
+    lens = np.zeros(300_000, np.int32)
+    offs = np.zeros(300_000, np.int64)
+    pool = np.zeros(64, np.uint8)
+    p, got, t = _pack(lens, offs, pool, 8, [(0, 8)], "i32")
+    assert t == 0 and not p.any()
+    lens1 = np.array([123_457], np.int32)
+    pool1 = np.random.default_rng(1).integers(0, 256, (123_457 + 9) * 8, dtype=np.uint8)
+    offs1 = np.array([9], np.int64)
+    p, got, t = _pack(lens1, offs1, pool1, 8, [(0, 8)], "u32")
+    _, want, tw = _expect(lens1, offs1, pool1, 8, [(0, 8)], "u32")
+    assert t == tw and p.tolist() == [0, 123_457] and got == want
+
+
+def test_fused_pack_overflow_reports_total():
+    lens, offs, plen = _inputs(100_000, 20, seed=13)
+    T = int(lens.sum())
+    pool = np.random.default_rng(14).integers(0, 256, plen * 8, dtype=np.uint8)
+    p, got, t = _pack(lens, offs, pool, 8, [(0, 8)], "i32", cap_extra=-T // 2)
+    assert t == T  # the caller sees total > capacity and re-packs
+    pw, _, _ = _expect(lens, offs, pool, 8, [(0, 8)], "i32")
+    assert p.tobytes() == pw.tobytes()  # the prefix is complete either way
+
+
+_SUB = r"""
+import sys, numpy as np
+sys.path.insert(0, {root!r})
+sys.path.insert(0, {tests!r})
+import test_gpu_jagged_paths as T
+for n, ml, ms, pt in [(1, 5, 8, 'i32'), (777, 20, 4, 'u16'), (1_000_000, 20, 8, 'i32'), (300_000, 9, 4, 'u16')]:
+    lens, offs, plen = T._inputs(n, ml, seed=n)
+    pool = np.random.default_rng(2).integers(0, 256, plen * ms + 8, dtype=np.uint8)
+    p, got, t = T._pack(lens, offs, pool, ms, [(0, ms)], pt, cap_extra=3)
+    pw, want, tw = T._expect(lens, offs, pool[:plen * ms], ms, [(0, ms)], pt)
+    assert t == tw and p.tobytes() == pw.tobytes() and got == want, (n, ml, ms, pt)
+lens, offs, plen = T._skewed_inputs(200_000, seed=3)
+pool = np.random.default_rng(4).integers(0, 256, plen * 8, dtype=np.uint8)
+p, got, t = T._pack(lens, offs, pool, 8, [(0, 8)], 'i64')
+pw, want, tw = T._expect(lens, offs, pool, 8, [(0, 8)], 'i64')
+assert t == tw and p.tobytes() == pw.tobytes() and got == want
+print('ok')
+"""
+
+
+@pytest.mark.parametrize("env", [{"SK_JAGGED_FUSED": "0"}])
+def test_pack_variants_in_subprocess(env):
+    """the two-kernel path (scan, then gather) on the fused path's cases"""
+    import os
+    import subprocess
+    import sys
+
+    tests = os.path.dirname(os.path.abspath(__file__))
+    code = _SUB.format(root=os.path.dirname(tests), tests=tests)
+    r = subprocess.run([sys.executable, "-c", code], env={**os.environ, **env}, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("ltype", [np.uint8, np.uint16, np.int64, np.uint32])
+def test_fused_pack_length_types(ltype):
+    lens, offs, plen = _inputs(150_001, 20, seed=21)
+    lens = lens.astype(ltype)
+    pool = np.random.default_rng(22).integers(0, 256, plen * 8, dtype=np.uint8)
+    p, got, t = _pack(lens, offs, pool, 8, [(0, 8)], "i64", cap_extra=1)
+    pw, want, tw = _expect(lens, offs, pool, 8, [(0, 8)], "i64")
+    assert t == tw and p.tobytes() == pw.tobytes() and got == want
