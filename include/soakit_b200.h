@@ -196,8 +196,9 @@ int sk_jagged_pack(int64_t n, const void* lens, int lens_type, void* prefix,
 int sk_jagged_rebase(int64_t count, void* prefix, int prefix_type, int64_t offset,
                      uintptr_t stream);
 
-/* Diagnostics only: copies the fused pack's table-warp timestamps (recorded
-   when SK_FUSED_DBG has bit 8 set) into `host`. */
+/* Diagnostics only: the fused pack's per-CTA timestamps (globaltimer ns:
+   start, block prefix known, blocks done, exit), recorded when the
+   environment variable SK_FUSED_DBG has bit 8 set. */
 int sk_jagged_trace(void* host, size_t bytes);
 
 /* ---- behavior plugin: the case-study per-object kernel (detector/schemas.py) */

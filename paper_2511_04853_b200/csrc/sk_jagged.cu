@@ -14,6 +14,12 @@
 // split: starts[w] = the record holding member w*W, and 1 + the last non-empty
 // record.
 //
+// sk_jagged_pack with one aligned 4/8-byte member field runs both in ONE
+// kernel (pack_fused_kernel, below): per-CTA record blocks whose prefixes come
+// from the predecessor blocks' published totals, then per-sub-tile smem tables
+// feeding the same window gather. The two-kernel path (scan, then gather)
+// serves sk_jagged_scan / sk_jagged_scatter and multi-field members.
+//
 // Gather: one warp per W = 256 consecutive output members, no block barriers.
 // The warp loads its record window (<= 32 records per batch, one per lane),
 // ranks the non-empty ones with ballot/popc and marks where each starts with
@@ -73,12 +79,6 @@ __device__ __forceinline__ void store_int(void* p, int type, int64_t i, int64_t 
   }
 }
 
-__device__ __forceinline__ uint64_t ld_acquire(const uint64_t* p) {
-  uint64_t v;
-  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-
 // the look-back status words carry their value: nothing else is published
 // with them, so relaxed (L2-coherent, no L1 invalidation) access is enough
 __device__ __forceinline__ uint64_t ld_relaxed(const uint64_t* p) {
@@ -89,10 +89,6 @@ __device__ __forceinline__ uint64_t ld_relaxed(const uint64_t* p) {
 
 __device__ __forceinline__ void st_relaxed(uint64_t* p, uint64_t v) {
   asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-
-__device__ __forceinline__ void st_release(uint64_t* p, uint64_t v) {
-  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
 // padded smem index: one int64 of padding per 16 keeps the per-thread
@@ -662,8 +658,14 @@ __global__ void __launch_bounds__(GA_WARPS * 32) gather_async_kernel(const __gri
 // accounted for all warps of all CTAs share the queued sub-tiles' windows
 // (each CTA rebuilds the tables), so skewed lengths cannot serialise on one CTA.
 
-// experiments only (sk_jagged_trace reads it; nothing writes it in this version)
-__device__ unsigned long long g_fused_trace[8 * 16 * 8];
+// experiments only (SK_FUSED_DBG & 8): per-CTA timestamps, read by sk_jagged_trace
+__device__ unsigned long long g_fused_trace[1024 * 8];
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 
 constexpr int F_NW = 8;             // warps per CTA
 constexpr int F_NT = 32 * F_NW;
@@ -704,9 +706,10 @@ struct FusedArgs {
   int64_t nblocks;
   int64_t tiles;        // sub-tiles over all blocks
   FusedHdr* hdr;
-  uint64_t* status;     // per block
+  uint64_t* status;     // per block: its total
   DeferEntry* defer;
   int pvec;             // 4-byte prefix, 16-byte aligned: vector prefix stores
+  int lens16;           // 4/8-byte lengths, 16-byte aligned: vector loads in the block sums
   int dbg;              // experiments only (SK_FUSED_DBG): 1 = no gather, 2 = no look-back
 };
 
@@ -799,15 +802,24 @@ __device__ __forceinline__ int table_search(const TileBuf& B, int64_t j) {
   return lo + (31 - __clz(m1));
 }
 
-// a warp's member pipeline: the window whose loads are in flight, drained
-// after the next window's loads are issued (possibly in a later tile)
+#ifndef SK_FUSED_STAGES
+#define SK_FUSED_STAGES 2
+#endif
+constexpr int F_NS = SK_FUSED_STAGES;  // stage buffers per warp: F_NS - 1 windows in flight behind the newest
+
+// a warp's member pipeline: windows whose loads are in flight, each stored
+// once F_NS - 1 newer windows have been issued (possibly in a later sub-tile)
+struct PendWin {
+  int64_t w0, g0, g1;
+};
 struct FPipe {
-  int it = 0;
-  int64_t w0 = -1, g0 = 0, g1 = 0;  // pending window (w0 < 0: none)
+  int it = 0;  // windows issued
+  int n = 0;   // of those, pending (oldest first)
+  PendWin p[F_NS - 1];
 };
 
 template <int MS>
-__device__ __forceinline__ void fdrain(const FusedArgs& F, const FPipe& p, const uint8_t* buf) {
+__device__ __forceinline__ void fdrain(const FusedArgs& F, const PendWin& p, const uint8_t* buf) {
   using V = typename MemberWord<MS>::T;
   const int lane = threadIdx.x & 31;
   const int64_t a0 = (p.g0 * MS + 15) & ~int64_t(15), a1 = (p.g1 * MS) & ~int64_t(15);
@@ -825,11 +837,13 @@ __device__ __forceinline__ void fdrain(const FusedArgs& F, const FPipe& p, const
 }
 
 template <int MS>
-__device__ __forceinline__ void fflush(const FusedArgs& F, FPipe& p, uint8_t (*stage)[W * MS]) {
-  if (p.w0 >= 0) {
+__device__ __forceinline__ void fflush(const FusedArgs& F, FPipe& pp, uint8_t (*stage)[W * MS]) {
+  if (pp.n) {
     cp_async_wait<0>();
-    fdrain<MS>(F, p, stage[(p.it - 1) & 1]);
-    p.w0 = -1;
+#pragma unroll
+    for (int i = 0; i < F_NS - 1; ++i)
+      if (i < pp.n) fdrain<MS>(F, pp.p[i], stage[(pp.it - pp.n + i) % F_NS]);
+    pp.n = 0;
   }
 }
 
@@ -861,8 +875,8 @@ __device__ __forceinline__ void gather_window(const FusedArgs& F, const TileBuf&
     if (c0 + 32 >= F_R || B.Lx[c0 + 32] >= j1) break;
   }
   __syncwarp();
-  uint8_t* buf = stage[pp.it & 1];
-  // the last bulk store (issued one window ago) read this buffer: it must be done reading
+  uint8_t* buf = stage[pp.it % F_NS];
+  // the latest bulk store (window it - F_NS, drained one window ago) read this buffer
   if (lane == 0) bulk_wait_read<0>();
   __syncwarp();
   int cum = 0;
@@ -875,13 +889,17 @@ __device__ __forceinline__ void gather_window(const FusedArgs& F, const TileBuf&
     cum += __popc(masks[q]);
   }
   cp_async_commit();
-  if (pp.w0 >= 0) {
-    cp_async_wait<1>();
-    fdrain<MS>(F, pp, stage[(pp.it - 1) & 1]);
+  if (pp.n == F_NS - 1) {
+    cp_async_wait<F_NS - 1>();  // the oldest pending window has landed
+    fdrain<MS>(F, pp.p[0], stage[(pp.it - pp.n) % F_NS]);
+#pragma unroll
+    for (int i = 0; i + 1 < F_NS - 1; ++i) pp.p[i] = pp.p[i + 1];
+    --pp.n;
   }
-  pp.w0 = w0;
-  pp.g0 = g0;
-  pp.g1 = g1;
+#pragma unroll
+  for (int i = 0; i < F_NS - 1; ++i)
+    if (i == pp.n) pp.p[i] = PendWin{w0, g0, g1};
+  ++pp.n;
   ++pp.it;
   __syncwarp();  // sRec is rewritten by the next window
 }
@@ -929,16 +947,23 @@ __device__ __forceinline__ int64_t pred_sum(const FusedArgs& F, int64_t blk) {
 template <int MS>
 __global__ void __launch_bounds__(F_NT, 2) pack_fused_kernel(const __grid_constant__ FusedArgs F) {
   extern __shared__ __align__(128) uint8_t fsm[];
-  auto stage_all = reinterpret_cast<uint8_t(*)[2][W * MS]>(fsm);
-  FusedSmem& S = *reinterpret_cast<FusedSmem*>(fsm + F_NW * 2 * W * MS);
+  auto stage_all = reinterpret_cast<uint8_t(*)[F_NS][W * MS]>(fsm);
+  FusedSmem& S = *reinterpret_cast<FusedSmem*>(fsm + F_NW * F_NS * W * MS);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   auto stage = stage_all[warp];
   int* sRec = S.sRec[warp];
   FPipe pp;
   FRegs<F_RPT> g;
+  auto stamp = [&](int k) {
+    if ((F.dbg & 8) && tid == 0 && blockIdx.x < 1024) g_fused_trace[blockIdx.x * 8 + k] = gtimer();
+  };
+  stamp(0);
 
-  while (true) {
-    if (tid == 0) S.item = atomicAdd(&F.hdr->ticket, 1u);
+  for (int round = 0;; ++round) {
+    // the first block is the CTA's own index (CTAs are dispatched in index order, so a block only ever
+    // waits on blocks whose CTAs run -- the assumption CUB's single-pass scan makes); later blocks by
+    // ticket, which hands out indices past the grid in the order CTAs come back for more
+    if (tid == 0) S.item = round == 0 ? blockIdx.x : gridDim.x + atomicAdd(&F.hdr->ticket, 1u);
     __syncthreads();  // also: every warp is done with the previous block's tables
     const int64_t blk = S.item;
     if (blk >= F.nblocks) break;
@@ -946,16 +971,33 @@ __global__ void __launch_bounds__(F_NT, 2) pack_fused_kernel(const __grid_consta
     const int nsub = static_cast<int>((rec1 - rec0 + F_R - 1) / F_R);
     // 1. the block total, published; the first sub-tile's records load meanwhile
     int64_t acc = 0;
-    if (dtype_size_dev(F.lens_type) == 4) {
-      const bool sgn = F.lens_type == SK_I32;
-#pragma unroll 4
-      for (int64_t r = rec0 + tid; r < rec1; r += F_NT) {
-        const uint32_t v = static_cast<const uint32_t*>(F.lens)[r];
-        acc += sgn ? static_cast<int64_t>(static_cast<int32_t>(v)) : static_cast<int64_t>(v);
+    int64_t rs = rec0;  // records before rs are summed by the vector loop
+    if (F.lens16) {
+      // 16-byte loads, 8 in flight per thread: the lengths pass is bandwidth-, not latency-bound
+      if (dtype_size_dev(F.lens_type) == 4) {
+        const bool sgn = F.lens_type == SK_I32;
+        const uint4* L = reinterpret_cast<const uint4*>(static_cast<const uint32_t*>(F.lens) + rec0);
+        const int64_t nv = (rec1 - rec0) / 4;
+#pragma unroll 8
+        for (int64_t i = tid; i < nv; i += F_NT) {
+          const uint4 v = L[i];
+          acc += sgn ? static_cast<int64_t>(static_cast<int32_t>(v.x)) + static_cast<int32_t>(v.y) +
+                           static_cast<int32_t>(v.z) + static_cast<int32_t>(v.w)
+                     : static_cast<int64_t>(v.x) + v.y + v.z + static_cast<int64_t>(v.w);
+        }
+        rs = rec0 + nv * 4;
+      } else {
+        const longlong2* L = reinterpret_cast<const longlong2*>(static_cast<const int64_t*>(F.lens) + rec0);
+        const int64_t nv = (rec1 - rec0) / 2;
+#pragma unroll 8
+        for (int64_t i = tid; i < nv; i += F_NT) {
+          const longlong2 v = L[i];
+          acc += v.x + v.y;
+        }
+        rs = rec0 + nv * 2;
       }
-    } else {
-      for (int64_t r = rec0 + tid; r < rec1; r += F_NT) acc += load_int(F.lens, F.lens_type, r);
     }
+    for (int64_t r = rs + tid; r < rec1; r += F_NT) acc += load_int(F.lens, F.lens_type, r);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     if (lane == 0) S.warp_tot[warp] = acc;
@@ -966,7 +1008,9 @@ __global__ void __launch_bounds__(F_NT, 2) pack_fused_kernel(const __grid_consta
 #pragma unroll
       for (int w = 0; w < F_NW; ++w) Ab += S.warp_tot[w];
       if (lane == 0) st_relaxed(&F.status[blk], FLAG_A | (static_cast<uint64_t>(Ab) & VAL_MASK));
+      stamp(4);
       const int64_t E = (F.dbg & 2) ? 0 : pred_sum(F, blk);
+      stamp(5);
       if (lane == 0) {
         S.E = E;
         if (rec1 == F.n) {  // the block holding the last record
@@ -976,6 +1020,7 @@ __global__ void __launch_bounds__(F_NT, 2) pack_fused_kernel(const __grid_consta
       }
     }
     __syncthreads();  // S.E, and warp_tot is free again
+    stamp(1);
     int64_t run = S.E;
     // 2. sub-tiles: scan, prefix, gather
     for (int sb = 0; sb < nsub; ++sb) {
@@ -997,9 +1042,7 @@ __global__ void __launch_bounds__(F_NT, 2) pack_fused_kernel(const __grid_consta
         if (queue) {
           const unsigned slot = atomicAdd(&F.hdr->ndef, 1u);
           F.defer[slot] = DeferEntry{r0, cnt, E, A, 0ull, {0ull, 0ull, 0ull}};
-          __threadfence();  // the entry is visible before the sub-tile counts as finished
         }
-        atomicAdd(&F.hdr->finished, 1u);
         S.next = 0;
       }
       __syncthreads();  // tables and the window counter are ready
@@ -1016,8 +1059,13 @@ __global__ void __launch_bounds__(F_NT, 2) pack_fused_kernel(const __grid_consta
       }
       __syncthreads();  // the tables are rewritten by the next sub-tile
     }
+    if (tid == 0) {
+      __threadfence();  // queue entries are visible before the block's sub-tiles count as finished
+      atomicAdd(&F.hdr->finished, static_cast<unsigned>(nsub));
+    }
   }
 
+  stamp(2);
   // queued sub-tiles: once every sub-tile is accounted for (their owners are running), share them out
   if (tid == 0) {
     while (*reinterpret_cast<volatile unsigned int*>(&F.hdr->finished) < static_cast<unsigned int>(F.tiles))
@@ -1052,11 +1100,12 @@ __global__ void __launch_bounds__(F_NT, 2) pack_fused_kernel(const __grid_consta
   }
   fflush<MS>(F, pp, stage);
   if (lane == 0) bulk_wait_all();
+  stamp(3);
 }
 
 template <int MS>
 constexpr size_t fused_smem() {
-  return static_cast<size_t>(F_NW) * 2 * W * MS + sizeof(FusedSmem);
+  return static_cast<size_t>(F_NW) * F_NS * W * MS + sizeof(FusedSmem);
 }
 
 // shard rebase: P[i] += offset in the index dtype's modular
@@ -1363,6 +1412,7 @@ int sk_jagged_pack(int64_t n, const void* lens, int lens_type, void* prefix, int
     F.dst = A.dst[0];
     F.capacity = capacity;
     F.pvec = dtype_size(prefix_type) == 4 && reinterpret_cast<uintptr_t>(prefix) % 16 == 0;
+    F.lens16 = (dtype_size(lens_type) == 4 || dtype_size(lens_type) == 8) && reinterpret_cast<uintptr_t>(lens) % 16 == 0;
     static const int dbg = [] {
       const char* e = getenv("SK_FUSED_DBG");
       return e ? atoi(e) : 0;
@@ -1412,7 +1462,7 @@ static int launch_rebase(int64_t count, void* p, int64_t offset, cudaStream_t s,
   return SK_OK;
 }
 
-// experiments only: copies the fused pack's table-warp timestamps to host memory
+// experiments only: the fused pack's per-CTA timestamps (SK_FUSED_DBG & 8)
 extern "C" int sk_jagged_trace(void* host, size_t bytes) {
   SK_TRY(cudaDeviceSynchronize());
   SK_TRY(cudaMemcpyFromSymbol(host, jag::g_fused_trace, std::min(bytes, sizeof(jag::g_fused_trace))));
