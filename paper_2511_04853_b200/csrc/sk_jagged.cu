@@ -1275,6 +1275,7 @@ static int launch_gather_async(const jag::ScatterArgs& A, int64_t ntasks, cudaSt
 
 template <int MS>
 static int launch_fused_ms(jag::FusedArgs F, uint8_t* scratch, cudaStream_t s, int dev, const DeviceState* ds) {
+
   constexpr size_t smem = jag::fused_smem<MS>();
   static int occ[64] = {0};
   int& o = occ[dev & 63];
