@@ -39,16 +39,18 @@ def _gather_index(lens, offs):
     return np.repeat(offs - P[:-1], lens.astype(np.int64)) + np.arange(T, dtype=np.int64), P
 
 
-def _pack(lens, offs, pool_bytes, stride, fields, ptype, cap_extra=0, dst_shift=0):
-    """run sk_jagged_pack; fields = [(offset, size)]; returns (prefix, [field arrays as bytes], total)"""
+def _pack(lens, offs, pool_bytes, stride, fields, ptype, cap_extra=0, dst_shift=0, lens_shift=0, prefix_shift=0):
+    """run sk_jagged_pack; fields = [(offset, size)]; returns (prefix, [field arrays as bytes], total).
+    lens_shift / prefix_shift: pass the lengths / prefix that many elements into their buffers
+    (off the 16-byte alignment the vector paths use)"""
     n = lens.size
     T = int(lens.astype(np.int64).sum())
     cap = T + cap_extra
-    d_lens = DeviceArray.from_numpy(lens, CUDA)
+    d_lens = DeviceArray.from_numpy(np.concatenate([np.zeros(lens_shift, lens.dtype), lens]), CUDA)
     d_offs = DeviceArray.from_numpy(offs, CUDA)
     d_pool = DeviceArray.from_numpy(pool_bytes, CUDA)
     pnp = np.dtype({"i32": np.int32, "u16": np.uint16, "u8": np.uint8, "i64": np.int64, "u32": np.uint32}[ptype])
-    prefix = DeviceArray(n + 1, pnp, CUDA)
+    prefix = DeviceArray(n + 1 + prefix_shift, pnp, CUDA)
     outs = [DeviceArray(max(cap, 1) * sz + 64, np.uint8, CUDA) for _, sz in fields]
     need = C.c_size_t(0)
     nat.call("sk_jagged_scratch_bytes", n, C.byref(need))
@@ -61,12 +63,13 @@ def _pack(lens, offs, pool_bytes, stride, fields, ptype, cap_extra=0, dst_shift=
     dst = (C.c_void_p * nf)(*[o.ptr + dst_shift for o in outs])
     lcode = {np.dtype(np.int32): "i32", np.dtype(np.uint8): "u8", np.dtype(np.uint16): "u16",
              np.dtype(np.int64): "i64", np.dtype(np.uint32): "u32"}[lens.dtype]
-    nat.call("sk_jagged_pack", n, d_lens.ptr, TC[lcode], prefix.ptr, TC[ptype], d_offs.ptr, d_pool.ptr, stride, nf,
+    nat.call("sk_jagged_pack", n, d_lens.ptr + lens_shift * lens.dtype.itemsize, TC[lcode],
+             prefix.ptr + prefix_shift * pnp.itemsize, TC[ptype], d_offs.ptr, d_pool.ptr, stride, nf,
              foff, fsz, dst, cap, scratch.ptr, scratch.n, total.ptr, nat.stream(0))
     nat.sync(0)
     t = int(total.numpy()[0])
     res = [o.numpy()[dst_shift:dst_shift + t * sz].tobytes() for o, (_, sz) in zip(outs, fields)]
-    p = prefix.numpy()
+    p = prefix.numpy()[prefix_shift:]
     for a in (d_lens, d_offs, d_pool, prefix, scratch, total, *outs):
         a.free()
     return p, res, t
@@ -249,3 +252,27 @@ def test_fused_pack_length_types(ltype):
     p, got, t = _pack(lens, offs, pool, 8, [(0, 8)], "i64", cap_extra=1)
     pw, want, tw = _expect(lens, offs, pool, 8, [(0, 8)], "i64")
     assert t == tw and p.tobytes() == pw.tobytes() and got == want
+
+
+@pytest.mark.parametrize("lshift,pshift", [(1, 0), (0, 1), (3, 3)])
+def test_fused_pack_unaligned_lengths_and_prefix(lshift, pshift):
+    """lengths / prefix off 16-byte alignment: scalar block sums and prefix stores"""
+    lens, offs, plen = _inputs(300_007, 20, seed=31 + lshift + pshift)
+    pool = np.random.default_rng(32).integers(0, 256, plen * 8, dtype=np.uint8)
+    p, got, t = _pack(lens, offs, pool, 8, [(0, 8)], "i32", cap_extra=2, lens_shift=lshift, prefix_shift=pshift)
+    pw, want, tw = _expect(lens, offs, pool, 8, [(0, 8)], "i32")
+    assert t == tw and p.tobytes() == pw.tobytes() and got == want
+
+
+def test_fused_pack_many_blocks_per_cta():
+    """more records than one 256-sub-tile block per CTA: blocks handed out by ticket"""
+    n = 296 * 2 * 262_144 + 12_345  # > (CTAs x max block) on a 148-SM part at 2 CTAs/SM
+    rng = np.random.default_rng(33)
+    lens = rng.integers(0, 3, n).astype(np.int32)
+    offs = np.concatenate([[0], np.cumsum(lens.astype(np.int64))[:-1]]) + 5  # in order, shifted by 5 members
+    T = int(lens.sum())
+    pool = np.arange(T + 8, dtype=np.uint64)
+    p, got, t = _pack(lens, offs, pool.view(np.uint8), 8, [(0, 8)], "i64")
+    assert t == T
+    assert np.array_equal(p, np.concatenate([[0], np.cumsum(lens.astype(np.int64))]))
+    assert np.array_equal(np.frombuffer(got[0], np.uint64), np.arange(5, T + 5, dtype=np.uint64))
