@@ -276,3 +276,20 @@ def test_fused_pack_many_blocks_per_cta():
     assert t == T
     assert np.array_equal(p, np.concatenate([[0], np.cumsum(lens.astype(np.int64))]))
     assert np.array_equal(np.frombuffer(got[0], np.uint64), np.arange(5, T + 5, dtype=np.uint64))
+
+
+@pytest.mark.parametrize("stride,fields", [
+    (8, [(0, 4), (4, 4)]),                    # {adc i32, t f32}: 8 staged bytes
+    (16, [(8, 8), (0, 4)]),                   # 12 staged bytes, fields out of record order
+    (16, [(0, 4), (4, 4), (8, 8)]),           # 16
+    (24, [(12, 4), (0, 4), (4, 4), (16, 4)]), # four pools
+])
+def test_fused_pack_member_field_table(stride, fields):
+    """several naturally aligned 4/8-byte member fields scattered into their own pools (SoA scatter;
+    the two-kernel path -- a staged field-table variant of the fused kernel measured slower, 84.6 vs
+    67.8 us on variant 3b)"""
+    lens, offs, plen = _inputs(400_003, 20, seed=41 + stride + len(fields))
+    pool = np.random.default_rng(42).integers(0, 256, plen * stride, dtype=np.uint8)
+    p, got, t = _pack(lens, offs, pool, stride, fields, "i32", cap_extra=9)
+    pw, want, tw = _expect(lens, offs, pool, stride, fields, "i32")
+    assert t == tw and p.tobytes() == pw.tobytes() and got == want

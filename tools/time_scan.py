@@ -14,7 +14,10 @@ from paper_2511_04853_b200.devarray import DeviceArray  # noqa: E402
 
 CUDA = mc.ContextInfo.cuda(0)
 n = int(os.environ.get("N", 1_000_000))
-lens, offsets, pool = wl.cluster_inputs(n, seed=7)
+HITS = bool(os.environ.get("HITS"))  # variant 3b: {adc i32, t f32} members into two pools
+lens, offsets, pool = wl.cluster_inputs(n, seed=7, member_dtype=wl.HIT_DTYPE if HITS else np.uint64)
+if HITS:
+    pool = pool.view(np.uint8)
 if os.environ.get("INORDER"):  # same lengths, segments packed in record order (sequential source reads)
     offsets = np.concatenate([[0], np.cumsum(lens.astype(np.int64))[:-1]])
 T = int(lens.sum())
@@ -27,12 +30,14 @@ sbytes = -(-need.value // 256) * 256 + ((cap + 255) // 256 + 1) * 8
 scratch = DeviceArray(sbytes, np.uint8, CUDA)
 total = DeviceArray(1, np.int64, CUDA)
 out = DeviceArray(cap, np.uint64, CUDA)
+out2 = DeviceArray(cap, np.uint32, CUDA)
 s = nat.stream(0)
 big = DeviceArray(12 << 30, np.uint8, CUDA)
 I32 = nat.TYPE_CODES["i32"]
-foff = (C.c_int64 * 1)(0)
-fsz = (C.c_int32 * 1)(8)
-dst = (C.c_void_p * 1)(out.ptr)
+NF = 2 if HITS else 1
+foff = (C.c_int64 * NF)(*([0, 4] if HITS else [0]))
+fsz = (C.c_int32 * NF)(*([4, 4] if HITS else [8]))
+dst = (C.c_void_p * NF)(*([out.ptr, out2.ptr] if HITS else [out.ptr]))
 
 
 def scan():
@@ -40,11 +45,11 @@ def scan():
 
 
 def scatter():
-    nat.call("sk_jagged_scatter", n, prefix.ptr, I32, d_off.ptr, d_pool.ptr, 8, 1, foff, fsz, dst, T, s)
+    nat.call("sk_jagged_scatter", n, prefix.ptr, I32, d_off.ptr, d_pool.ptr, 8, NF, foff, fsz, dst, T, s)
 
 
 def pack():
-    nat.call("sk_jagged_pack", n, d_lens.ptr, I32, prefix.ptr, I32, d_off.ptr, d_pool.ptr, 8, 1, foff, fsz, dst,
+    nat.call("sk_jagged_pack", n, d_lens.ptr, I32, prefix.ptr, I32, d_off.ptr, d_pool.ptr, 8, NF, foff, fsz, dst,
              cap, scratch.ptr, scratch.n, total.ptr, s)
 
 
