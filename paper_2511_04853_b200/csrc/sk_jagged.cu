@@ -1066,6 +1066,7 @@ __global__ void __launch_bounds__(F_NT, 2) pack_fused_kernel(const __grid_consta
   }
 
   stamp(2);
+  __syncthreads();  // every thread has read S.item (the loop's last ticket) before it is reused
   // queued sub-tiles: once every sub-tile is accounted for (their owners are running), share them out
   if (tid == 0) {
     while (*reinterpret_cast<volatile unsigned int*>(&F.hdr->finished) < static_cast<unsigned int>(F.tiles))

@@ -21,6 +21,15 @@ pool2 = np.random.default_rng(3).integers(0, 256, plen2 * 8, dtype=np.uint8)
 J._pack(lens2, offs2, pool2, 8, [(0, 8)], "u16")                       # wrapping prefix
 J._pack(lens2, offs2, pool2, 8, [(0, 4)], "i32", cap_extra=10)         # 4-byte async
 J._pack(lens2, offs2, pool2, 8, [(0, 8)], "i32", cap_extra=-100)       # overflow: gathers nothing
+lens3 = np.random.default_rng(4).integers(0, 4, 5000).astype(np.int32)
+lens3[100:200] = 1000                                                   # a sub-tile over the queueing threshold
+order = np.random.default_rng(5).permutation(lens3.size)
+gaps = lens3[order].astype(np.int64) + 1
+offs3 = np.empty(lens3.size, np.int64)
+offs3[order] = np.concatenate([[0], np.cumsum(gaps)[:-1]])
+pool3 = np.random.default_rng(6).integers(0, 256, int(gaps.sum()) * 8, dtype=np.uint8)
+J._pack(lens3, offs3, pool3, 8, [(0, 8)], "i64")                       # fused: queued sub-tile shared out
+J._pack(lens2, offs2, pool2, 8, [(0, 8)], "i32", lens_shift=1, prefix_shift=1)  # scalar block sums / prefix
 J.test_scatter_over_given_prefix.__wrapped__ if hasattr(J.test_scatter_over_given_prefix, "__wrapped__") else None
 
 import paper_2511_04853_b200 as sk  # noqa: E402
