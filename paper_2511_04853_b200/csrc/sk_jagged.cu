@@ -87,6 +87,13 @@ __device__ __forceinline__ uint64_t ld_relaxed(const uint64_t* p) {
   return v;
 }
 
+// polling read that must not be served from a stale L1 line: cache-global (L2) access
+__device__ __forceinline__ uint64_t ld_poll(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.global.cg.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
 __device__ __forceinline__ void st_relaxed(uint64_t* p, uint64_t v) {
   asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
@@ -802,6 +809,14 @@ __device__ __forceinline__ int table_search(const TileBuf& B, int64_t j) {
   return lo + (31 - __clz(m1));
 }
 
+#ifndef SK_POLL_CG
+#define SK_POLL_CG 1
+#endif
+#if SK_POLL_CG
+#define POLLFN ld_poll
+#else
+#define POLLFN ld_relaxed
+#endif
 #ifndef SK_FUSED_STAGES
 #define SK_FUSED_STAGES 2
 #endif
@@ -914,21 +929,24 @@ __device__ __forceinline__ int64_t end_window(int64_t E, int64_t A) { return (E 
 __device__ __forceinline__ int64_t pred_sum(const FusedArgs& F, int64_t blk) {
   const int lane = threadIdx.x & 31;
   int64_t acc = 0;
+  int spins = 0;
   for (int64_t e0 = 0; e0 < blk; e0 += 256) {
     uint64_t st[8];
     bool missing = false;
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
       const int64_t idx = e0 + q * 32 + lane;
-      st[q] = idx < blk ? ld_relaxed(&F.status[idx]) : FLAG_A;
+      st[q] = idx < blk ? POLLFN(&F.status[idx]) : FLAG_A;
       missing |= (st[q] >> 62) == 0;
     }
+    if ((F.dbg & 8) && e0 == 0 && lane == 0 && blockIdx.x < 1024) g_fused_trace[blockIdx.x * 8 + 6] = gtimer();
     while (__any_sync(0xffffffffu, missing)) {
+      ++spins;
       __nanosleep(200);
       missing = false;
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
-        if ((st[q] >> 62) == 0) st[q] = ld_relaxed(&F.status[e0 + q * 32 + lane]);
+        if ((st[q] >> 62) == 0) st[q] = POLLFN(&F.status[e0 + q * 32 + lane]);
         missing |= (st[q] >> 62) == 0;
       }
     }
@@ -938,6 +956,7 @@ __device__ __forceinline__ int64_t pred_sum(const FusedArgs& F, int64_t blk) {
       if (idx < blk) acc += static_cast<int64_t>(st[q] & VAL_MASK);
     }
   }
+  if ((F.dbg & 8) && lane == 0 && blockIdx.x < 1024) g_fused_trace[blockIdx.x * 8 + 7] = spins;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
   return acc;
@@ -1001,14 +1020,22 @@ __global__ void __launch_bounds__(F_NT, 2) pack_fused_kernel(const __grid_consta
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     if (lane == 0) S.warp_tot[warp] = acc;
-    sub_load(F, rec0, static_cast<int>(min(static_cast<int64_t>(F_R), rec1 - rec0)), g);
     __syncthreads();
+    int64_t Ab = 0;
     if (warp == 0) {
-      int64_t Ab = 0;
 #pragma unroll
       for (int w = 0; w < F_NW; ++w) Ab += S.warp_tot[w];
-      if (lane == 0) st_relaxed(&F.status[blk], FLAG_A | (static_cast<uint64_t>(Ab) & VAL_MASK));
-      stamp(4);
+      if (lane == 0) {
+        st_relaxed(&F.status[blk], FLAG_A | (static_cast<uint64_t>(Ab) & VAL_MASK));
+        // push the total out now: an unfenced store can sit in the SM for microseconds, and every later
+        // block waits on it (this thread has no loads in flight, so the fence is quick)
+        __threadfence();
+      }
+    }
+    stamp(4);
+    // the first sub-tile's records load while warp 0 sums the predecessors
+    sub_load(F, rec0, static_cast<int>(min(static_cast<int64_t>(F_R), rec1 - rec0)), g);
+    if (warp == 0) {
       const int64_t E = (F.dbg & 2) ? 0 : pred_sum(F, blk);
       stamp(5);
       if (lane == 0) {

@@ -33,7 +33,12 @@ t = buf.reshape(1024, 8).astype(np.int64)
 t = t[t[:, 0] > 0]
 t0 = t[:, 0].min()
 rel = (t - t0) / 1e3
-for k, name in [(0, "start"), (4, "total out"), (5, "preds summed"), (1, "prefix known"), (2, "blocks done"), (3, "exit")]:
+spins = t[:, 7].copy()
+t[:, 7] = t[:, 0]
+rel = (t - t0) / 1e3
+print("pred-sum polling rounds: p50", np.percentile(spins, 50), "max", spins.max())
+for k, name in [(0, "start"), (4, "total out"), (6, "first poll back"), (5, "preds summed"), (1, "prefix known"),
+                (2, "blocks done"), (3, "exit")]:
     q = np.percentile(rel[:, k], [0, 10, 50, 90, 100])
     print(f"{name:13s} us: min {q[0]:6.2f}  p10 {q[1]:6.2f}  p50 {q[2]:6.2f}  p90 {q[3]:6.2f}  max {q[4]:6.2f}")
 if os.environ.get("PERBLOCK"):
