@@ -572,7 +572,8 @@ def run_extras(args, dev: int) -> dict:
         "members": members, "device_ms": round(ms, 4), "members_per_s": round(members / ms * 1e3),
         "gbs": round(algo / ms / 1e6, 1), "frac": round(algo / ms / 1e6 / peak, 3),
         "api_ms": round(ms_api, 4),
-        "note": "device_ms: sk_jagged_pack (scan + gather) queued on the device; api_ms: jagged.pack on a "
+        "note": "device_ms: sk_jagged_pack (one fused kernel: block sums, prefixes, gather) queued on the device; "
+                "api_ms: jagged.pack on a "
                 "Collection, incl. the host readback of the member total that sizes the pool; source segments "
                 "in shuffled order with slack, so ~125 MB of 32 B sectors are read for 92 MB of payload"}
     c3.free()
@@ -590,6 +591,13 @@ def run_extras(args, dev: int) -> dict:
     out["config4_aosoa_100M"] = {"ms": round(ms, 3), "gbs": round(n4 * 76 / ms / 1e6, 1),
                                  "frac": round(n4 * 76 / ms / 1e6 / peak, 3), "objects_per_s": round(n4 / ms * 1e3)}
     ao.free()
+    # the other tile widths SURVEY 8d names (T = 32, 64): same bytes per object
+    for lanes in (32, 64):
+        ao = sk.Aosoa(n4, lanes, fields, cuda)
+        ms = queued(lambda: sk.to_aosoa(a4, fields, lanes, out=ao, sync=False), steps=5)
+        out["config4_aosoa_100M"][f"T{lanes}"] = {"ms": round(ms, 3), "gbs": round(n4 * 76 / ms / 1e6, 1),
+                                                  "frac": round(n4 * 76 / ms / 1e6 / peak, 3)}
+        ao.free()
     a4.free()
     busy.free()
     return out
