@@ -587,6 +587,10 @@ __device__ __forceinline__ void convert_body(const Plan& P) {
     for (int i = tid; i < P.words_per_rec; i += NT) wtab[i] = P.wtab[i];
   if (tid == 0) fence_mbar_init();
   __syncthreads();
+  // back-to-back conversions: the next one's CTAs may start their prologue as ours retire; nothing global
+  // (plan tables come from the kernel parameter) is touched before the previous kernel has completed
+  pdl_allow_next();
+  pdl_wait_prior();
 
   const int64_t first = blockIdx.x;
   const int64_t step = gridDim.x;

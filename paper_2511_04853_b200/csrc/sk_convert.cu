@@ -444,10 +444,30 @@ int make_plan(const sk_conv_desc& d, const DeviceState& ds, bool in_bulk_ok, boo
 int launch_specialized(const sk_conv_desc& d, const Plan& P, const DeviceState& ds, const int* epi_fields,
                        cudaStream_t s, bool* launched);  // sk_rtc.cu
 
+// programmatic stream serialization (PDL): a conversion queued right behind
+// another kernel overlaps its launch and prologue with that kernel's tail
+// (SK_PDL=0 turns it off)
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("SK_PDL");
+    return !(e && *e == '0');
+  }();
+  return on;
+}
+
 int launch(const Plan& P, int grid, cudaStream_t s) {
   if (P.ntiles == 0) return SK_OK;
-  convert_kernel<<<grid, NT, P.smem_total, s>>>(P);
-  SK_TRY(cudaGetLastError());
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(NT);
+  cfg.dynamicSmemBytes = P.smem_total;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  SK_TRY(cudaLaunchKernelEx(&cfg, convert_kernel, P));
   return SK_OK;
 }
 

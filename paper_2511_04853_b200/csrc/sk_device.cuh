@@ -158,6 +158,13 @@ __device__ __forceinline__ void bulk_wait_read() {
 
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
+// programmatic dependent launch: let the next kernel in the stream be scheduled
+// (its CTAs run their prologue and park in pdl_wait_prior), and wait until the
+// previous kernel has completed and its writes are visible. Both are no-ops
+// for a launch without the programmatic-serialization attribute.
+__device__ __forceinline__ void pdl_allow_next() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait_prior() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // generic-proxy smem writes -> visible to the async proxy (bulk store source)
 __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");

@@ -343,6 +343,8 @@ static bool specialise_enabled() {
 
 // Launch the signature-specialised kernel for this plan when it applies.
 // *launched = false means: not eligible / unavailable, use the generic kernel.
+bool pdl_enabled();  // sk_convert.cu
+
 int launch_specialized(const sk_conv_desc& d, const Plan& P, const DeviceState& ds, const int* epi_fields,
                        cudaStream_t s, bool* launched) {
   *launched = false;
@@ -383,8 +385,17 @@ int launch_specialized(const sk_conv_desc& d, const Plan& P, const DeviceState& 
   }
   const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(static_cast<int64_t>(ds.sm_count) * per_sm, P.ntiles));
   void* args[] = {const_cast<Plan*>(&P)};
-  SK_TRY(cudaLaunchKernel(reinterpret_cast<const void*>(c->kernel), dim3(static_cast<unsigned>(grid)), dim3(NT),
-                          args, P.smem_total, s));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(grid));
+  cfg.blockDim = dim3(NT);
+  cfg.dynamicSmemBytes = P.smem_total;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  SK_TRY(cudaLaunchKernelExC(&cfg, reinterpret_cast<const void*>(c->kernel), args));
   *launched = true;
   return SK_OK;
 }
