@@ -1020,6 +1020,9 @@ __global__ void __launch_bounds__(F_NT, 2) pack_fused_kernel(const __grid_consta
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     if (lane == 0) S.warp_tot[warp] = acc;
+    // nothing is written and no scratch word read before the scratch-zeroing kernel ahead of this one has
+    // completed (its trigger came after ITS predecessor completed, so the lengths read above were final)
+    if (round == 0) pdl_wait_prior();
     __syncthreads();
     int64_t Ab = 0;
     if (warp == 0) {
@@ -1131,6 +1134,17 @@ __global__ void __launch_bounds__(F_NT, 2) pack_fused_kernel(const __grid_consta
   stamp(3);
 }
 
+// zeroes the fused pack's scratch header + status words; lets the pack's CTAs
+// launch (and sum their lengths) meanwhile, but only once everything before it
+// in the stream has completed
+__global__ void __launch_bounds__(256) scratch_zero_kernel(uint64_t* p, int64_t words) {
+  pdl_wait_prior();
+  pdl_allow_next();
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < words;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    p[i] = 0;
+}
+
 template <int MS>
 constexpr size_t fused_smem() {
   return static_cast<size_t>(F_NW) * F_NS * W * MS + sizeof(FusedSmem);
@@ -1160,6 +1174,22 @@ static cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, c
   cfg.gridDim = grid;
   cfg.blockDim = block;
   cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_pdl_smem(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                                   Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -1325,10 +1355,11 @@ static int launch_fused_ms(jag::FusedArgs F, uint8_t* scratch, cudaStream_t s, i
   F.status = reinterpret_cast<uint64_t*>(scratch + 64);
   const size_t status_bytes = (static_cast<size_t>(F.nblocks) * 8 + 63) & ~size_t(63);
   F.defer = reinterpret_cast<jag::DeferEntry*>(scratch + 64 + status_bytes);
-  SK_TRY(cudaMemsetAsync(scratch, 0, 64 + status_bytes, s));
+  const int64_t zwords = static_cast<int64_t>((64 + status_bytes) / 8);
+  SK_TRY(launch_pdl(jag::scratch_zero_kernel, dim3(static_cast<unsigned>(std::min<int64_t>((zwords + 255) / 256, 64))),
+                    dim3(256), s, reinterpret_cast<uint64_t*>(scratch), zwords));
   const int64_t grid = std::min<int64_t>(F.nblocks, ctas);
-  jag::pack_fused_kernel<MS><<<static_cast<unsigned>(grid), jag::F_NT, smem, s>>>(F);
-  SK_TRY(cudaGetLastError());
+  SK_TRY(launch_pdl_smem(jag::pack_fused_kernel<MS>, dim3(static_cast<unsigned>(grid)), dim3(jag::F_NT), smem, s, F));
   return SK_OK;
 }
 
