@@ -809,18 +809,9 @@ __device__ __forceinline__ int table_search(const TileBuf& B, int64_t j) {
   return lo + (31 - __clz(m1));
 }
 
-#ifndef SK_POLL_CG
-#define SK_POLL_CG 1
-#endif
-#if SK_POLL_CG
-#define POLLFN ld_poll
-#else
-#define POLLFN ld_relaxed
-#endif
-#ifndef SK_FUSED_STAGES
-#define SK_FUSED_STAGES 2
-#endif
-constexpr int F_NS = SK_FUSED_STAGES;  // stage buffers per warp: F_NS - 1 windows in flight behind the newest
+// stage buffers per warp: F_NS - 1 windows in flight behind the newest (3 and 4 measured slower: the
+// extra shared memory comes out of the L1 the shuffled member reads rely on)
+constexpr int F_NS = 2;
 
 // a warp's member pipeline: windows whose loads are in flight, each stored
 // once F_NS - 1 newer windows have been issued (possibly in a later sub-tile)
@@ -936,7 +927,7 @@ __device__ __forceinline__ int64_t pred_sum(const FusedArgs& F, int64_t blk) {
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
       const int64_t idx = e0 + q * 32 + lane;
-      st[q] = idx < blk ? POLLFN(&F.status[idx]) : FLAG_A;
+      st[q] = idx < blk ? ld_poll(&F.status[idx]) : FLAG_A;
       missing |= (st[q] >> 62) == 0;
     }
     if ((F.dbg & 8) && e0 == 0 && lane == 0 && blockIdx.x < 1024) g_fused_trace[blockIdx.x * 8 + 6] = gtimer();
@@ -946,7 +937,7 @@ __device__ __forceinline__ int64_t pred_sum(const FusedArgs& F, int64_t blk) {
       missing = false;
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
-        if ((st[q] >> 62) == 0) st[q] = POLLFN(&F.status[e0 + q * 32 + lane]);
+        if ((st[q] >> 62) == 0) st[q] = ld_poll(&F.status[e0 + q * 32 + lane]);
         missing |= (st[q] >> 62) == 0;
       }
     }
