@@ -60,6 +60,18 @@ struct Args {
   unsigned long long* event_count;
 };
 
+// appends: one atomic per warp instead of one per lane (a single counter shared
+// by the whole grid serialises in L2 otherwise); returns this lane's slot if `take`
+__device__ __forceinline__ unsigned long long warp_append(unsigned long long* ctr, bool take) {
+  const unsigned m = __ballot_sync(__activemask(), take);
+  if (!m) return 0;
+  const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
+  unsigned long long base = 0;
+  if (lane == leader) base = atomicAdd(ctr, static_cast<unsigned long long>(__popc(m)));
+  base = __shfl_sync(__activemask(), base, leader);
+  return base + __popc(m & ((1u << lane) - 1u));
+}
+
 __device__ __forceinline__ bool higher(const Args& A, int64_t q, int64_t c) {
   const float eq = A.energy[q], ec = A.energy[c];
   return eq > ec || (eq == ec && q < c);  // argsort(-energy, stable) over ascending candidates
@@ -67,37 +79,47 @@ __device__ __forceinline__ bool higher(const Args& A, int64_t q, int64_t c) {
 
 __global__ void init_kernel(Args A) {
   const int64_t total = A.n * A.nevents;
-  for (int64_t i = static_cast<int64_t>(blockIdx.x) * NT + threadIdx.x; i < total;
-       i += static_cast<int64_t>(gridDim.x) * NT) {
-    const float r = __fdiv_rn(A.energy[i], A.noise[i]);  // numpy f32 division (IEEE)
-    A.ratio[i] = r;
-    A.consumed[i] = 0;
-    const bool seed = r > 5.0f;
-    A.state[i] = seed ? PENDING : NONE;
-    if (seed) A.cand[atomicAdd(&A.counters[0], 1ull)] = i;
+  // whole warps iterate together (the candidate append is warp-aggregated)
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * NT;
+  for (int64_t i0 = static_cast<int64_t>(blockIdx.x) * NT + (threadIdx.x & ~31); i0 < total; i0 += stride) {
+    const int64_t i = i0 + (threadIdx.x & 31);
+    bool seed = false;
+    if (i < total) {
+      const float r = __fdiv_rn(A.energy[i], A.noise[i]);  // numpy f32 division (IEEE)
+      A.ratio[i] = r;
+      A.consumed[i] = 0;
+      seed = r > 5.0f;
+      A.state[i] = seed ? PENDING : NONE;
+    }
+    const unsigned long long slot = warp_append(&A.counters[0], seed);
+    if (seed) A.cand[slot] = i;
   }
 }
 
 // phase 1 of a round: which pending seeds are ready
 __global__ void ready_kernel(Args A) {
   const int64_t ncand = static_cast<int64_t>(A.counters[0]);
-  for (int64_t k = static_cast<int64_t>(blockIdx.x) * NT + threadIdx.x; k < ncand;
-       k += static_cast<int64_t>(gridDim.x) * NT) {
-    const int64_t c = A.cand[k];
-    if (A.state[c] != PENDING) continue;
-    atomicAdd(&A.counters[2], 1ull);
-    const int64_t base = (c / A.n) * A.n, loc = c - base;
-    const int64_t cy = loc / A.w, cx = loc - cy * A.w;
-    bool ok = true;
-    for (int64_t y = imax64(0, cy - 4); ok && y <= imin64(A.h - 1, cy + 4); ++y)
-      for (int64_t x = imax64(0, cx - 4); x <= imin64(A.w - 1, cx + 4); ++x) {
-        const int64_t q = base + y * A.w + x;
-        if (q != c && A.state[q] == PENDING && higher(A, q, c)) {
-          ok = false;
-          break;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * NT;
+  for (int64_t k0 = static_cast<int64_t>(blockIdx.x) * NT + (threadIdx.x & ~31); k0 < ncand; k0 += stride) {
+    const int64_t k = k0 + (threadIdx.x & 31);
+    const int64_t c = k < ncand ? A.cand[k] : 0;
+    const bool pend = k < ncand && A.state[c] == PENDING;
+    bool ok = pend;
+    if (pend) {
+      const int64_t base = (c / A.n) * A.n, loc = c - base;
+      const int64_t cy = loc / A.w, cx = loc - cy * A.w;
+      for (int64_t y = imax64(0, cy - 4); ok && y <= imin64(A.h - 1, cy + 4); ++y)
+        for (int64_t x = imax64(0, cx - 4); x <= imin64(A.w - 1, cx + 4); ++x) {
+          const int64_t q = base + y * A.w + x;
+          if (q != c && A.state[q] == PENDING && higher(A, q, c)) {
+            ok = false;
+            break;
+          }
         }
-      }
-    if (ok) A.ready[atomicAdd(&A.counters[1], 1ull)] = c;
+    }
+    warp_append(&A.counters[2], pend);
+    const unsigned long long slot = warp_append(&A.counters[1], ok);
+    if (ok) A.ready[slot] = c;
   }
 }
 
@@ -195,17 +217,38 @@ struct OutArgs {
   int64_t* offsets;
 };
 
-__global__ void write_kernel(const Slot* slots, int64_t np, const int64_t* event_off, const int64_t* event_cnt,
-                             const int64_t* order, OutArgs O) {
-  for (int64_t i = static_cast<int64_t>(blockIdx.x) * NT + threadIdx.x; i < np;
-       i += static_cast<int64_t>(gridDim.x) * NT) {
-    const int64_t p = order[i];
-    const Slot& S = slots[p];
-    const int64_t b = event_off[S.event], m = event_cnt[S.event];
-    int64_t rank = 0;
-    for (int64_t j = 0; j < m; ++j) {
+constexpr int RANK_SMEM = 4096;  // particles of one event ranked out of shared memory
+
+// one CTA per event: the event's priority keys go to smem (broadcast reads),
+// each particle's rank = how many keys outrank it; events with more particles
+// than RANK_SMEM read the keys from global memory instead
+__global__ void __launch_bounds__(NT) write_kernel(const Slot* slots, const int64_t* event_off,
+                                                   const int64_t* event_cnt, const int64_t* order, OutArgs O) {
+  __shared__ float ke[RANK_SMEM];
+  __shared__ int64_t ko[RANK_SMEM];
+  const int64_t ev = blockIdx.x;
+  const int64_t b = event_off[ev], m = event_cnt[ev];
+  const bool in_smem = m <= RANK_SMEM;
+  if (in_smem)
+    for (int64_t j = threadIdx.x; j < m; j += NT) {
       const Slot& Q = slots[order[b + j]];
-      rank += (Q.key_e > S.key_e) || (Q.key_e == S.key_e && Q.origin < S.origin);
+      ke[j] = Q.key_e;
+      ko[j] = Q.origin;
+    }
+  __syncthreads();
+  for (int64_t i = threadIdx.x; i < m; i += NT) {
+    const int64_t p = order[b + i];
+    const Slot& S = slots[p];
+    const float se = S.key_e;
+    const int64_t so = S.origin;
+    int64_t rank = 0;
+    if (in_smem) {
+      for (int64_t j = 0; j < m; ++j) rank += (ke[j] > se) || (ke[j] == se && ko[j] < so);
+    } else {
+      for (int64_t j = 0; j < m; ++j) {
+        const Slot& Q = slots[order[b + j]];
+        rank += (Q.key_e > se) || (Q.key_e == se && Q.origin < so);
+      }
     }
     const int64_t o = b + rank;
     O.energy[o] = S.energy;
@@ -360,7 +403,7 @@ int sk_reco_write(void* handle, float* energy, float* x, float* y, uint64_t* ori
   }
   O.lens = sensor_lens;
   O.offsets = sensor_offsets;
-  reco::write_kernel<<<grid, reco::NT, 0, s>>>(H->A.slots, H->np, d_off, d_cnt, order, O);
+  if (H->nevents) reco::write_kernel<<<H->nevents, reco::NT, 0, s>>>(H->A.slots, d_off, d_cnt, order, O);
   SK_TRY(cudaGetLastError());
   cudaFreeAsync(d_off, s);
   cudaFreeAsync(d_cnt, s);
