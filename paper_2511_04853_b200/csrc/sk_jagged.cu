@@ -441,6 +441,10 @@ template <>
 struct MemberWord<8> {
   using T = uint64_t;
 };
+template <>
+struct MemberWord<16> {  // a staged 16-byte member record (RS kernels)
+  using T = uint4;
+};
 
 // PT: prefix element type. MS: 4 or 8 = one naturally aligned member field of
 // that size (straight-line loads/stores); 0 = the generic field table.
@@ -715,6 +719,12 @@ struct FusedArgs {
   FusedHdr* hdr;
   uint64_t* status;     // per block: its total
   DeferEntry* defer;
+  // RS kernels (several member fields): the whole member record (member_stride = 8 or 16 bytes) is staged
+  // and field f (fsz[f] = 4 or 8 bytes at foff[f]) is split out into pool fdst[f] when the window drains
+  int nf;
+  int fsz[4];
+  int foff[4];
+  uint8_t* fdst[4];
   int pvec;             // 4-byte prefix, 16-byte aligned: vector prefix stores
   int lens16;           // 4/8-byte lengths, 16-byte aligned: vector loads in the block sums
   int dbg;              // experiments only (SK_FUSED_DBG): 1 = no gather, 2 = no look-back
@@ -824,8 +834,30 @@ struct FPipe {
   PendWin p[F_NS - 1];
 };
 
+// RS: split the staged records of the window into the field pools (lanes, coalesced per pool)
 template <int MS>
+__device__ __forceinline__ void fdrain_split(const FusedArgs& F, const PendWin& p, const uint8_t* buf) {
+  const int lane = threadIdx.x & 31;
+  __syncwarp();
+  for (int f = 0; f < F.nf; ++f) {
+    const uint8_t* s = buf + F.foff[f];
+    if (F.fsz[f] == 8) {
+      uint64_t* d = reinterpret_cast<uint64_t*>(F.fdst[f]);
+      for (int64_t g = p.g0 + lane; g < p.g1; g += 32) d[g] = *reinterpret_cast<const uint64_t*>(s + (g - p.w0) * MS);
+    } else {
+      uint32_t* d = reinterpret_cast<uint32_t*>(F.fdst[f]);
+      for (int64_t g = p.g0 + lane; g < p.g1; g += 32) d[g] = *reinterpret_cast<const uint32_t*>(s + (g - p.w0) * MS);
+    }
+  }
+  __syncwarp();
+}
+
+template <int MS, bool RS>
 __device__ __forceinline__ void fdrain(const FusedArgs& F, const PendWin& p, const uint8_t* buf) {
+  if constexpr (RS) {
+    fdrain_split<MS>(F, p, buf);
+    return;
+  }
   using V = typename MemberWord<MS>::T;
   const int lane = threadIdx.x & 31;
   const int64_t a0 = (p.g0 * MS + 15) & ~int64_t(15), a1 = (p.g1 * MS) & ~int64_t(15);
@@ -842,19 +874,19 @@ __device__ __forceinline__ void fdrain(const FusedArgs& F, const PendWin& p, con
     *reinterpret_cast<V*>(F.dst + g * MS) = *reinterpret_cast<const V*>(buf + (g - p.w0) * MS);
 }
 
-template <int MS>
+template <int MS, bool RS>
 __device__ __forceinline__ void fflush(const FusedArgs& F, FPipe& pp, uint8_t (*stage)[W * MS]) {
   if (pp.n) {
     cp_async_wait<0>();
 #pragma unroll
     for (int i = 0; i < F_NS - 1; ++i)
-      if (i < pp.n) fdrain<MS>(F, pp.p[i], stage[(pp.it - pp.n + i) % F_NS]);
+      if (i < pp.n) fdrain<MS, RS>(F, pp.p[i], stage[(pp.it - pp.n + i) % F_NS]);
     pp.n = 0;
   }
 }
 
 // the warp gathers output window k of the tile whose members are [E, E + A)
-template <int MS>
+template <int MS, bool RS>
 __device__ __forceinline__ void gather_window(const FusedArgs& F, const TileBuf& B, int64_t E, int64_t A, int64_t k,
                                               int* sRec, uint8_t (*stage)[W * MS], FPipe& pp) {
   const int lane = threadIdx.x & 31;
@@ -897,7 +929,7 @@ __device__ __forceinline__ void gather_window(const FusedArgs& F, const TileBuf&
   cp_async_commit();
   if (pp.n == F_NS - 1) {
     cp_async_wait<F_NS - 1>();  // the oldest pending window has landed
-    fdrain<MS>(F, pp.p[0], stage[(pp.it - pp.n) % F_NS]);
+    fdrain<MS, RS>(F, pp.p[0], stage[(pp.it - pp.n) % F_NS]);
 #pragma unroll
     for (int i = 0; i + 1 < F_NS - 1; ++i) pp.p[i] = pp.p[i + 1];
     --pp.n;
@@ -954,7 +986,7 @@ __device__ __forceinline__ int64_t pred_sum(const FusedArgs& F, int64_t blk) {
 }
 
 
-template <int MS>
+template <int MS, bool RS>
 __global__ void __launch_bounds__(F_NT, 2) pack_fused_kernel(const __grid_constant__ FusedArgs F) {
   extern __shared__ __align__(128) uint8_t fsm[];
   auto stage_all = reinterpret_cast<uint8_t(*)[F_NS][W * MS]>(fsm);
@@ -1075,7 +1107,7 @@ __global__ void __launch_bounds__(F_NT, 2) pack_fused_kernel(const __grid_consta
           if (lane == 0) k = atomicAdd(&S.next, 1);
           k = __shfl_sync(0xffffffffu, k, 0);
           if (k >= nwin) break;
-          gather_window<MS>(F, S.tb, E, A, k0 + k, sRec, stage, pp);
+          gather_window<MS, RS>(F, S.tb, E, A, k0 + k, sRec, stage, pp);
         }
       }
       __syncthreads();  // the tables are rewritten by the next sub-tile
@@ -1117,10 +1149,10 @@ __global__ void __launch_bounds__(F_NT, 2) pack_fused_kernel(const __grid_consta
       }
       const int64_t kb = k0 + c * DEFER_CHUNK, ke = min(kb + DEFER_CHUNK, k0 + nwin);
       for (int64_t k = kb + warp; k < ke; k += F_NW)
-        gather_window<MS>(F, S.tb, ent.E, ent.A, k, sRec, stage, pp);
+        gather_window<MS, RS>(F, S.tb, ent.E, ent.A, k, sRec, stage, pp);
     }
   }
-  fflush<MS>(F, pp, stage);
+  fflush<MS, RS>(F, pp, stage);
   if (lane == 0) bulk_wait_all();
   stamp(3);
 }
@@ -1322,16 +1354,16 @@ static int launch_gather_async(const jag::ScatterArgs& A, int64_t ntasks, cudaSt
   return SK_OK;
 }
 
-template <int MS>
+template <int MS, bool RS>
 static int launch_fused_ms(jag::FusedArgs F, uint8_t* scratch, cudaStream_t s, int dev, const DeviceState* ds) {
 
   constexpr size_t smem = jag::fused_smem<MS>();
   static int occ[64] = {0};
   int& o = occ[dev & 63];
   if (!o) {
-    SK_TRY(cudaFuncSetAttribute(jag::pack_fused_kernel<MS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    SK_TRY(cudaFuncSetAttribute(jag::pack_fused_kernel<MS, RS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(smem)));
-    SK_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, jag::pack_fused_kernel<MS>, jag::F_NT, smem));
+    SK_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, jag::pack_fused_kernel<MS, RS>, jag::F_NT, smem));
     o = std::max(o, 1);
   }
   // one block of records per CTA (a multiple of 4 records, at least one sub-tile, at most MAX_SUB)
@@ -1350,7 +1382,7 @@ static int launch_fused_ms(jag::FusedArgs F, uint8_t* scratch, cudaStream_t s, i
   SK_TRY(launch_pdl(jag::scratch_zero_kernel, dim3(static_cast<unsigned>(std::min<int64_t>((zwords + 255) / 256, 64))),
                     dim3(256), s, reinterpret_cast<uint64_t*>(scratch), zwords));
   const int64_t grid = std::min<int64_t>(F.nblocks, ctas);
-  SK_TRY(launch_pdl_smem(jag::pack_fused_kernel<MS>, dim3(static_cast<unsigned>(grid)), dim3(jag::F_NT), smem, s, F));
+  SK_TRY(launch_pdl_smem(jag::pack_fused_kernel<MS, RS>, dim3(static_cast<unsigned>(grid)), dim3(jag::F_NT), smem, s, F));
   return SK_OK;
 }
 
@@ -1445,9 +1477,16 @@ int sk_jagged_pack(int64_t n, const void* lens, int lens_type, void* prefix, int
     SK_TRY(cudaMemsetAsync(total_dev, 0, 8, s));
     return SK_OK;
   }
-  // single pass: one aligned 4/8-byte member field into a 16-byte-aligned pool
-  if (fused_pack_ok() && nfields == 1 && A.aligned[0] && (A.field_size[0] == 4 || A.field_size[0] == 8) &&
-      reinterpret_cast<uintptr_t>(A.dst[0]) % 16 == 0) {
+  // single pass: one aligned 4/8-byte member field into a 16-byte-aligned pool, or (RS) 2-4 naturally
+  // aligned 4/8-byte fields of an 8- or 16-byte member record in a record-aligned source pool
+  const bool single = nfields == 1 && A.aligned[0] && (A.field_size[0] == 4 || A.field_size[0] == 8) &&
+                      reinterpret_cast<uintptr_t>(A.dst[0]) % 16 == 0;
+  bool split = nfields >= 2 && nfields <= 4 && (member_stride == 8 || member_stride == 16) &&
+               reinterpret_cast<uintptr_t>(src_pool) % member_stride == 0;
+  for (int f = 0; f < nfields && split; ++f)
+    split = A.aligned[f] && (A.field_size[f] == 4 || A.field_size[f] == 8) &&
+            reinterpret_cast<uintptr_t>(A.dst[f]) % A.field_size[f] == 0;
+  if (fused_pack_ok() && (single || split)) {
     DeviceState* ds = nullptr;
     if (int rc = device_state(dev, &ds)) return rc;
     jag::FusedArgs F{};
@@ -1458,7 +1497,13 @@ int sk_jagged_pack(int64_t n, const void* lens, int lens_type, void* prefix, int
     F.prefix_type = prefix_type;
     F.total = total_dev;
     F.src_off = src_off;
-    F.src = A.src_pool + A.field_off[0];
+    F.src = single ? A.src_pool + A.field_off[0] : A.src_pool;
+    F.nf = nfields;
+    for (int f = 0; f < nfields && f < 4; ++f) {
+      F.fsz[f] = A.field_size[f];
+      F.foff[f] = static_cast<int>(A.field_off[f]);
+      F.fdst[f] = A.dst[f];
+    }
     F.member_stride = member_stride;
     F.dst = A.dst[0];
     F.capacity = capacity;
@@ -1470,7 +1515,11 @@ int sk_jagged_pack(int64_t n, const void* lens, int lens_type, void* prefix, int
     }();
     F.dbg = dbg;
     uint8_t* sc = static_cast<uint8_t*>(scratch);
-    return A.field_size[0] == 8 ? launch_fused_ms<8>(F, sc, s, dev, ds) : launch_fused_ms<4>(F, sc, s, dev, ds);
+    if (split)
+      return member_stride == 16 ? launch_fused_ms<16, true>(F, sc, s, dev, ds)
+                                 : launch_fused_ms<8, true>(F, sc, s, dev, ds);
+    return A.field_size[0] == 8 ? launch_fused_ms<8, false>(F, sc, s, dev, ds)
+                                : launch_fused_ms<4, false>(F, sc, s, dev, ds);
   }
   // a prefix type that can wrap below the capacity needs an int64 copy for the gather
   const int bits = 8 * dtype_size(prefix_type) - ((prefix_type == SK_I32 || prefix_type == SK_I64) ? 1 : 0);

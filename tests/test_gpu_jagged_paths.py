@@ -285,9 +285,9 @@ def test_fused_pack_many_blocks_per_cta():
     (24, [(12, 4), (0, 4), (4, 4), (16, 4)]), # four pools
 ])
 def test_fused_pack_member_field_table(stride, fields):
-    """several naturally aligned 4/8-byte member fields scattered into their own pools (SoA scatter;
-    the two-kernel path -- a staged field-table variant of the fused kernel measured slower, 84.6 vs
-    67.8 us on variant 3b)"""
+    """several naturally aligned 4/8-byte member fields scattered into their own pools (SoA scatter):
+    8- and 16-byte member records take the fused kernel with record staging and a split drain, the
+    24-byte one the two-kernel path"""
     lens, offs, plen = _inputs(400_003, 20, seed=41 + stride + len(fields))
     pool = np.random.default_rng(42).integers(0, 256, plen * stride, dtype=np.uint8)
     p, got, t = _pack(lens, offs, pool, stride, fields, "i32", cap_extra=9)
