@@ -30,6 +30,9 @@ offs3[order] = np.concatenate([[0], np.cumsum(gaps)[:-1]])
 pool3 = np.random.default_rng(6).integers(0, 256, int(gaps.sum()) * 8, dtype=np.uint8)
 J._pack(lens3, offs3, pool3, 8, [(0, 8)], "i64")                       # fused: queued sub-tile shared out
 J._pack(lens2, offs2, pool2, 8, [(0, 8)], "i32", lens_shift=1, prefix_shift=1)  # scalar block sums / prefix
+J._pack(lens2, offs2, pool2, 8, [(0, 4), (4, 4)], "i32")               # fused, record staged + split drain
+pool16 = np.random.default_rng(7).integers(0, 256, plen2 * 16, dtype=np.uint8)
+J._pack(lens2, offs2, pool16, 16, [(8, 8), (0, 4)], "i64")             # 16-byte records
 J.test_scatter_over_given_prefix.__wrapped__ if hasattr(J.test_scatter_over_given_prefix, "__wrapped__") else None
 
 import paper_2511_04853_b200 as sk  # noqa: E402
