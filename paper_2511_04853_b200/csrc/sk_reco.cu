@@ -72,128 +72,210 @@ __device__ __forceinline__ unsigned long long warp_append(unsigned long long* ct
   return base + __popc(m & ((1u << lane) - 1u));
 }
 
+// appends with one global atomic per CTA call (every thread of the CTA calls
+// it, uniformly): the warps reserve ranges in smem, thread 0 reserves the CTA's
+// range in the global counter. A single counter shared by the grid serialises
+// in L2 at a few hundred thousand atomics.
+__device__ __forceinline__ unsigned long long cta_append(unsigned long long* ctr, bool take, unsigned* s_cnt,
+                                                         unsigned long long* s_base) {
+  const unsigned m = __ballot_sync(0xffffffffu, take);
+  const int lane = threadIdx.x & 31;
+  unsigned woff = 0;
+  if (lane == 0 && m) woff = atomicAdd(s_cnt, static_cast<unsigned>(__popc(m)));
+  woff = __shfl_sync(0xffffffffu, woff, 0);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    *s_base = *s_cnt ? atomicAdd(ctr, static_cast<unsigned long long>(*s_cnt)) : 0ull;
+    *s_cnt = 0;
+  }
+  __syncthreads();
+  return *s_base + woff + __popc(m & ((1u << lane) - 1u));
+}
+
 __device__ __forceinline__ bool higher(const Args& A, int64_t q, int64_t c) {
   const float eq = A.energy[q], ec = A.energy[c];
   return eq > ec || (eq == ec && q < c);  // argsort(-energy, stable) over ascending candidates
 }
 
-__global__ void init_kernel(Args A) {
+__global__ void __launch_bounds__(NT) init_kernel(Args A) {
+  __shared__ unsigned s_cnt;
+  __shared__ unsigned long long s_base;
+  if (threadIdx.x == 0) s_cnt = 0;
+  __syncthreads();
   const int64_t total = A.n * A.nevents;
-  // whole warps iterate together (the candidate append is warp-aggregated)
+  // 4 cells per thread per iteration, strided by the grid (4 independent loads in flight per thread); the
+  // loop runs on the CTA's base index, so every thread takes part in every candidate append
   const int64_t stride = static_cast<int64_t>(gridDim.x) * NT;
-  for (int64_t i0 = static_cast<int64_t>(blockIdx.x) * NT + (threadIdx.x & ~31); i0 < total; i0 += stride) {
-    const int64_t i = i0 + (threadIdx.x & 31);
-    bool seed = false;
-    if (i < total) {
-      const float r = __fdiv_rn(A.energy[i], A.noise[i]);  // numpy f32 division (IEEE)
-      A.ratio[i] = r;
-      A.consumed[i] = 0;
-      seed = r > 5.0f;
-      A.state[i] = seed ? PENDING : NONE;
+  for (int64_t c0 = static_cast<int64_t>(blockIdx.x) * NT; c0 < total; c0 += 4 * stride) {
+    float e[4], nz[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t i = c0 + u * stride + threadIdx.x;
+      e[u] = i < total ? A.energy[i] : 0.0f;
+      nz[u] = i < total ? A.noise[i] : 1.0f;
     }
-    const unsigned long long slot = warp_append(&A.counters[0], seed);
-    if (seed) A.cand[slot] = i;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t i = c0 + u * stride + threadIdx.x;
+      bool seed = false;
+      if (i < total) {
+        const float r = __fdiv_rn(e[u], nz[u]);  // numpy f32 division (IEEE)
+        A.ratio[i] = r;
+        A.consumed[i] = 0;
+        seed = r > 5.0f;
+        A.state[i] = seed ? PENDING : NONE;
+      }
+      const unsigned long long slot = cta_append(&A.counters[0], seed, &s_cnt, &s_base);
+      if (seed) A.cand[slot] = i;
+    }
   }
 }
 
-// phase 1 of a round: which pending seeds are ready
+// phase 1 of a round: which pending seeds are ready. A warp takes 32
+// candidates at a time; for each pending one the lanes split its 9x9
+// neighbourhood (3 cells each) and vote. Appends are one atomic per batch.
 __global__ void ready_kernel(Args A) {
+  const int lane = threadIdx.x & 31;
   const int64_t ncand = static_cast<int64_t>(A.counters[0]);
-  const int64_t stride = static_cast<int64_t>(gridDim.x) * NT;
-  for (int64_t k0 = static_cast<int64_t>(blockIdx.x) * NT + (threadIdx.x & ~31); k0 < ncand; k0 += stride) {
-    const int64_t k = k0 + (threadIdx.x & 31);
-    const int64_t c = k < ncand ? A.cand[k] : 0;
-    const bool pend = k < ncand && A.state[c] == PENDING;
-    bool ok = pend;
-    if (pend) {
+  const int64_t nwarps = static_cast<int64_t>(gridDim.x) * (NT / 32);
+  for (int64_t k0 = (static_cast<int64_t>(blockIdx.x) * (NT / 32) + (threadIdx.x >> 5)) * 32; k0 < ncand;
+       k0 += nwarps * 32) {
+    const int64_t k = k0 + lane;
+    const int64_t mine = k < ncand ? A.cand[k] : 0;
+    const bool pend = k < ncand && A.state[mine] == PENDING;
+    unsigned todo = __ballot_sync(0xffffffffu, pend);
+    bool ok = false;
+    while (todo) {
+      const int owner = __ffs(todo) - 1;
+      todo &= todo - 1;
+      const int64_t c = __shfl_sync(0xffffffffu, mine, owner);
       const int64_t base = (c / A.n) * A.n, loc = c - base;
       const int64_t cy = loc / A.w, cx = loc - cy * A.w;
-      for (int64_t y = imax64(0, cy - 4); ok && y <= imin64(A.h - 1, cy + 4); ++y)
-        for (int64_t x = imax64(0, cx - 4); x <= imin64(A.w - 1, cx + 4); ++x) {
-          const int64_t q = base + y * A.w + x;
-          if (q != c && A.state[q] == PENDING && higher(A, q, c)) {
-            ok = false;
-            break;
+      bool blocked = false;
+#pragma unroll
+      for (int r = 0; r < 3; ++r) {
+        const int cell = lane + 32 * r;  // 0..80 over the 9x9 window, row-major
+        if (cell < 81) {
+          const int64_t y = cy + cell / 9 - 4, x = cx + cell % 9 - 4;
+          if (y >= 0 && y < A.h && x >= 0 && x < A.w) {
+            const int64_t q = base + y * A.w + x;
+            blocked |= q != c && A.state[q] == PENDING && higher(A, q, c);
           }
         }
+      }
+      const bool okc = !__any_sync(0xffffffffu, blocked);
+      if (lane == owner) ok = okc;
     }
-    warp_append(&A.counters[2], pend);
-    const unsigned long long slot = warp_append(&A.counters[1], ok);
-    if (ok) A.ready[slot] = c;
+    const unsigned pm = __ballot_sync(0xffffffffu, pend), rm = __ballot_sync(0xffffffffu, ok);
+    unsigned long long rb = 0;
+    if (lane == 0) {
+      if (pm) atomicAdd(&A.counters[2], static_cast<unsigned long long>(__popc(pm)));
+      if (rm) rb = atomicAdd(&A.counters[1], static_cast<unsigned long long>(__popc(rm)));
+    }
+    rb = __shfl_sync(0xffffffffu, rb, 0);
+    if (ok) A.ready[rb + __popc(rm & ((1u << lane) - 1u))] = mine;
   }
 }
 
-// phase 2 of a round: process the ready seeds (pairwise disjoint windows)
+// phase 2 of a round: process the ready seeds (pairwise disjoint windows).
+// One warp per seed: lane l < 25 examines window cell (l / 5 - 2, l % 5 - 2),
+// so the cell loads run in parallel; lane 0 then adds the contributors up in
+// the reference's row-major order (reconstruct.py:84-117), fetching each by
+// shuffle, so every sum is bit-identical to the sequential walk.
 __global__ void process_kernel(Args A) {
+  const int lane = threadIdx.x & 31;
   const int64_t nready = static_cast<int64_t>(A.counters[1]);
-  for (int64_t k = static_cast<int64_t>(blockIdx.x) * NT + threadIdx.x; k < nready;
-       k += static_cast<int64_t>(gridDim.x) * NT) {
+  const int64_t nwarps = static_cast<int64_t>(gridDim.x) * (NT / 32);
+  for (int64_t k = static_cast<int64_t>(blockIdx.x) * (NT / 32) + (threadIdx.x >> 5); k < nready; k += nwarps) {
     const int64_t s = A.ready[k];
     if (A.consumed[s]) {  // taken by an earlier particle: the reference skips it
-      A.state[s] = DECIDED;
+      if (lane == 0) A.state[s] = DECIDED;
       continue;
     }
     const int64_t ev = s / A.n, base = ev * A.n, loc = s - base;
     const int64_t sy = loc / A.w, sx = loc - sy * A.w;
-    int64_t con[MAXC];
-    int nc = 0;
-    for (int64_t y = imax64(0, sy - 2); y <= imin64(A.h - 1, sy + 2); ++y)
-      for (int64_t x = imax64(0, sx - 2); x <= imin64(A.w - 1, sx + 2); ++x) {
-        const int64_t f = base + y * A.w + x;
-        if (!A.consumed[f] && A.ratio[f] > 2.0f) {
-          A.consumed[f] = 1;
-          if (A.state[f] == PENDING && f != s) A.state[f] = DECIDED;  // a consumed seed is always skipped
-          con[nc++] = f;
-        }
-      }
+    const int64_t y = sy + lane / 5 - 2, x = sx + lane % 5 - 2;
+    const bool inwin = lane < 25 && y >= 0 && y < A.h && x >= 0 && x < A.w;
+    const int64_t f = base + y * A.w + x;
+    bool take = false;
+    float e32 = 0.0f, r32 = 0.0f;
+    int t = 0;
+    bool noisy = false;
+    if (inwin && !A.consumed[f]) {
+      r32 = A.ratio[f];
+      take = r32 > 2.0f;
+    }
+    if (take) {
+      e32 = A.energy[f];
+      t = A.type[f] & 3;
+      noisy = A.noisy[f] != 0;
+    }
+    __syncwarp();  // every lane has read `consumed` before any marks it
+    if (take) {
+      A.consumed[f] = 1;
+      if (f != s && A.state[f] == PENDING) A.state[f] = DECIDED;  // a consumed seed is always skipped
+    }
+    const unsigned mask = __ballot_sync(0xffffffffu, take);
+    const int nc = __popc(mask);
+    const double lx = static_cast<double>(x), ly = static_cast<double>(y);
     // reconstruct.py:84-117, same operation order (no FMA: -fmad=false)
     double e64[4] = {0, 0, 0, 0}, sig64[4] = {0, 0, 0, 0};
     int cnt[4] = {0, 0, 0, 0};
     double sw = 0, swx = 0, swy = 0;
-    for (int i = 0; i < nc; ++i) {
-      const int64_t f = con[i], lf = f - base;
-      const double e = static_cast<double>(A.energy[f]);
-      const int t = A.type[f] & 3;
-      e64[t] = __dadd_rn(e64[t], e);
-      sig64[t] = __dadd_rn(sig64[t], static_cast<double>(A.ratio[f]));
-      if (A.noisy[f]) ++cnt[t];
+    for (int i = 0; i < 25; ++i) {
+      const float ei = __shfl_sync(0xffffffffu, e32, i), ri = __shfl_sync(0xffffffffu, r32, i);
+      const int ti = __shfl_sync(0xffffffffu, t, i);
+      const int ni = __shfl_sync(0xffffffffu, static_cast<int>(noisy), i);
+      const double xi = __shfl_sync(0xffffffffu, lx, i), yi = __shfl_sync(0xffffffffu, ly, i);
+      if (!((mask >> i) & 1u)) continue;
+      const double e = static_cast<double>(ei);
+      e64[ti] = __dadd_rn(e64[ti], e);
+      sig64[ti] = __dadd_rn(sig64[ti], static_cast<double>(ri));
+      if (ni) ++cnt[ti];
       sw = __dadd_rn(sw, e);
-      swx = __dadd_rn(swx, __dmul_rn(e, static_cast<double>(lf % A.w)));
-      swy = __dadd_rn(swy, __dmul_rn(e, static_cast<double>(lf / A.w)));
+      swx = __dadd_rn(swx, __dmul_rn(e, xi));
+      swy = __dadd_rn(swy, __dmul_rn(e, yi));
     }
     const double xbar = __ddiv_rn(swx, sw), ybar = __ddiv_rn(swy, sw);
     double vx = 0, vy = 0;
-    for (int i = 0; i < nc; ++i) {
-      const int64_t lf = con[i] - base;
-      const double e = static_cast<double>(A.energy[con[i]]);
-      const double dx = __dsub_rn(static_cast<double>(lf % A.w), xbar);
-      const double dy = __dsub_rn(static_cast<double>(lf / A.w), ybar);
+    for (int i = 0; i < 25; ++i) {
+      const float ei = __shfl_sync(0xffffffffu, e32, i);
+      const double xi = __shfl_sync(0xffffffffu, lx, i), yi = __shfl_sync(0xffffffffu, ly, i);
+      if (!((mask >> i) & 1u)) continue;
+      const double e = static_cast<double>(ei);
+      const double dx = __dsub_rn(xi, xbar), dy = __dsub_rn(yi, ybar);
       vx = __dadd_rn(vx, __dmul_rn(e, __dmul_rn(dx, dx)));
       vy = __dadd_rn(vy, __dmul_rn(e, __dmul_rn(dy, dy)));
     }
-    const unsigned long long p = atomicAdd(&A.counters[3], 1ull);
-    Slot& S = A.slots[p];
-    float e32[4];
-    for (int t = 0; t < 4; ++t) {
-      e32[t] = __double2float_rn(e64[t]);
-      S.ec[t] = e32[t];
-      S.sig[t] = __double2float_rn(sig64[t]);
-      S.nc[t] = static_cast<uint8_t>(cnt[t]);
+    unsigned long long p = 0;
+    if (lane == 0) p = atomicAdd(&A.counters[3], 1ull);
+    p = __shfl_sync(0xffffffffu, p, 0);
+    if (take) {  // contributor list, row-major: rank of this lane among the taken ones
+      A.contrib[p * MAXC + __popc(mask & ((1u << lane) - 1u))] = static_cast<uint64_t>(f - base);
     }
-    S.energy = __double2float_rn(__dadd_rn(__dadd_rn(__dadd_rn(static_cast<double>(e32[0]), static_cast<double>(e32[1])),
-                                                      static_cast<double>(e32[2])),
-                                            static_cast<double>(e32[3])));
-    S.x = __double2float_rn(xbar);
-    S.y = __double2float_rn(ybar);
-    S.xvar = __double2float_rn(__ddiv_rn(vx, sw));
-    S.yvar = __double2float_rn(__ddiv_rn(vy, sw));
-    S.nsens = nc;
-    S.event = static_cast<int32_t>(ev);
-    S.origin = loc;
-    S.key_e = A.energy[s];
-    for (int i = 0; i < nc; ++i) A.contrib[p * MAXC + i] = static_cast<uint64_t>(con[i] - base);
-    atomicAdd(&A.event_count[ev], 1ull);
-    A.state[s] = DECIDED;
+    if (lane == 0) {
+      Slot& S = A.slots[p];
+      float c32[4];
+      for (int q = 0; q < 4; ++q) {
+        c32[q] = __double2float_rn(e64[q]);
+        S.ec[q] = c32[q];
+        S.sig[q] = __double2float_rn(sig64[q]);
+        S.nc[q] = static_cast<uint8_t>(cnt[q]);
+      }
+      S.energy = __double2float_rn(__dadd_rn(
+          __dadd_rn(__dadd_rn(static_cast<double>(c32[0]), static_cast<double>(c32[1])), static_cast<double>(c32[2])),
+          static_cast<double>(c32[3])));
+      S.x = __double2float_rn(xbar);
+      S.y = __double2float_rn(ybar);
+      S.xvar = __double2float_rn(__ddiv_rn(vx, sw));
+      S.yvar = __double2float_rn(__ddiv_rn(vy, sw));
+      S.nsens = nc;
+      S.event = static_cast<int32_t>(ev);
+      S.origin = loc;
+      S.key_e = A.energy[s];
+      atomicAdd(&A.event_count[ev], 1ull);
+      A.state[s] = DECIDED;
+    }
   }
 }
 
@@ -228,6 +310,8 @@ __global__ void __launch_bounds__(NT) write_kernel(const Slot* slots, const int6
   __shared__ int64_t ko[RANK_SMEM];
   const int64_t ev = blockIdx.x;
   const int64_t b = event_off[ev], m = event_cnt[ev];
+  const int64_t first = static_cast<int64_t>(blockIdx.y) * NT;  // this CTA ranks particles [first, first + NT)
+  if (first >= m) return;
   const bool in_smem = m <= RANK_SMEM;
   if (in_smem)
     for (int64_t j = threadIdx.x; j < m; j += NT) {
@@ -236,7 +320,7 @@ __global__ void __launch_bounds__(NT) write_kernel(const Slot* slots, const int6
       ko[j] = Q.origin;
     }
   __syncthreads();
-  for (int64_t i = threadIdx.x; i < m; i += NT) {
+  for (int64_t i = first + threadIdx.x; i < m; i += static_cast<int64_t>(gridDim.y) * NT) {
     const int64_t p = order[b + i];
     const Slot& S = slots[p];
     const float se = S.key_e;
@@ -334,13 +418,16 @@ int sk_reco_run(int64_t w, int64_t h, int nevents, const float* energy, const fl
   if (e == cudaSuccess)
     e = cudaMallocAsync(reinterpret_cast<void**>(&A.contrib), std::max<size_t>(1, ncand) * reco::MAXC * 8, s);
   if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync(particle slots)");
-  const int cgrid = std::max(1, std::min<int>(ds->sm_count * 8, static_cast<int>((ncand + reco::NT - 1) / reco::NT)));
+  // ready: one warp per 32 candidates; process: one warp per ready seed
+  const int rgrid = std::max(1, std::min<int>(ds->sm_count * 8, static_cast<int>((ncand + reco::NT - 1) / reco::NT)));
+  const int cgrid =
+      std::max(1, std::min<int>(ds->sm_count * 8, static_cast<int>((ncand + reco::NT / 32 - 1) / (reco::NT / 32))));
   int r = 0;
   unsigned long long pending = ncand;
   while (pending) {
     for (int k = 0; k < 4; ++k, ++r) {  // four rounds per host check
       SK_TRY(cudaMemsetAsync(&A.counters[1], 0, 16, s));  // nready, pending
-      reco::ready_kernel<<<cgrid, reco::NT, 0, s>>>(A);
+      reco::ready_kernel<<<rgrid, reco::NT, 0, s>>>(A);
       reco::process_kernel<<<cgrid, reco::NT, 0, s>>>(A);
     }
     SK_TRY(cudaGetLastError());
@@ -403,7 +490,11 @@ int sk_reco_write(void* handle, float* energy, float* x, float* y, uint64_t* ori
   }
   O.lens = sensor_lens;
   O.offsets = sensor_offsets;
-  if (H->nevents) reco::write_kernel<<<H->nevents, reco::NT, 0, s>>>(H->A.slots, d_off, d_cnt, order, O);
+  int64_t mmax = 0;
+  for (int i = 0; i < H->nevents; ++i) mmax = std::max(mmax, H->counts[i]);
+  const unsigned chunks = static_cast<unsigned>(std::min<int64_t>((mmax + reco::NT - 1) / reco::NT, 65535));
+  if (H->nevents && chunks)
+    reco::write_kernel<<<dim3(H->nevents, chunks), reco::NT, 0, s>>>(H->A.slots, d_off, d_cnt, order, O);
   SK_TRY(cudaGetLastError());
   cudaFreeAsync(d_off, s);
   cudaFreeAsync(d_cnt, s);
