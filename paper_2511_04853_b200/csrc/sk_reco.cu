@@ -131,40 +131,32 @@ __global__ void __launch_bounds__(NT) init_kernel(Args A) {
   }
 }
 
-// phase 1 of a round: which pending seeds are ready. A warp takes 32
-// candidates at a time; for each pending one the lanes split its 9x9
-// neighbourhood (3 cells each) and vote. Appends are one atomic per batch.
+// phase 1 of a round: which pending seeds are ready. One thread per
+// candidate, its 9x9 neighbourhood a row (9 independent loads) at a time;
+// the pending count and the ready appends are aggregated per warp.
 __global__ void ready_kernel(Args A) {
   const int lane = threadIdx.x & 31;
   const int64_t ncand = static_cast<int64_t>(A.counters[0]);
-  const int64_t nwarps = static_cast<int64_t>(gridDim.x) * (NT / 32);
-  for (int64_t k0 = (static_cast<int64_t>(blockIdx.x) * (NT / 32) + (threadIdx.x >> 5)) * 32; k0 < ncand;
-       k0 += nwarps * 32) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * NT;
+  for (int64_t k0 = static_cast<int64_t>(blockIdx.x) * NT + (threadIdx.x & ~31); k0 < ncand; k0 += stride) {
     const int64_t k = k0 + lane;
-    const int64_t mine = k < ncand ? A.cand[k] : 0;
-    const bool pend = k < ncand && A.state[mine] == PENDING;
-    unsigned todo = __ballot_sync(0xffffffffu, pend);
-    bool ok = false;
-    while (todo) {
-      const int owner = __ffs(todo) - 1;
-      todo &= todo - 1;
-      const int64_t c = __shfl_sync(0xffffffffu, mine, owner);
+    const int64_t c = k < ncand ? A.cand[k] : 0;
+    const bool pend = k < ncand && A.state[c] == PENDING;
+    bool ok = pend;
+    if (pend) {
       const int64_t base = (c / A.n) * A.n, loc = c - base;
       const int64_t cy = loc / A.w, cx = loc - cy * A.w;
-      bool blocked = false;
+      const int64_t x0 = imax64(0, cx - 4), x1 = imin64(A.w - 1, cx + 4);
+      for (int64_t y = imax64(0, cy - 4); ok && y <= imin64(A.h - 1, cy + 4); ++y) {
+        uint8_t st[9];
 #pragma unroll
-      for (int r = 0; r < 3; ++r) {
-        const int cell = lane + 32 * r;  // 0..80 over the 9x9 window, row-major
-        if (cell < 81) {
-          const int64_t y = cy + cell / 9 - 4, x = cx + cell % 9 - 4;
-          if (y >= 0 && y < A.h && x >= 0 && x < A.w) {
-            const int64_t q = base + y * A.w + x;
-            blocked |= q != c && A.state[q] == PENDING && higher(A, q, c);
-          }
+        for (int d = 0; d < 9; ++d) st[d] = x0 + d <= x1 ? A.state[base + y * A.w + x0 + d] : NONE;
+#pragma unroll
+        for (int d = 0; d < 9; ++d) {
+          const int64_t q = base + y * A.w + x0 + d;
+          if (st[d] == PENDING && q != c && higher(A, q, c)) ok = false;
         }
       }
-      const bool okc = !__any_sync(0xffffffffu, blocked);
-      if (lane == owner) ok = okc;
     }
     const unsigned pm = __ballot_sync(0xffffffffu, pend), rm = __ballot_sync(0xffffffffu, ok);
     unsigned long long rb = 0;
@@ -173,7 +165,7 @@ __global__ void ready_kernel(Args A) {
       if (rm) rb = atomicAdd(&A.counters[1], static_cast<unsigned long long>(__popc(rm)));
     }
     rb = __shfl_sync(0xffffffffu, rb, 0);
-    if (ok) A.ready[rb + __popc(rm & ((1u << lane) - 1u))] = mine;
+    if (ok) A.ready[rb + __popc(rm & ((1u << lane) - 1u))] = c;
   }
 }
 
