@@ -60,75 +60,58 @@ struct Args {
   unsigned long long* event_count;
 };
 
-// appends: one atomic per warp instead of one per lane (a single counter shared
-// by the whole grid serialises in L2 otherwise); returns this lane's slot if `take`
-__device__ __forceinline__ unsigned long long warp_append(unsigned long long* ctr, bool take) {
-  const unsigned m = __ballot_sync(__activemask(), take);
-  if (!m) return 0;
-  const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
-  unsigned long long base = 0;
-  if (lane == leader) base = atomicAdd(ctr, static_cast<unsigned long long>(__popc(m)));
-  base = __shfl_sync(__activemask(), base, leader);
-  return base + __popc(m & ((1u << lane) - 1u));
-}
-
-// appends with one global atomic per CTA call (every thread of the CTA calls
-// it, uniformly): the warps reserve ranges in smem, thread 0 reserves the CTA's
-// range in the global counter. A single counter shared by the grid serialises
-// in L2 at a few hundred thousand atomics.
-__device__ __forceinline__ unsigned long long cta_append(unsigned long long* ctr, bool take, unsigned* s_cnt,
-                                                         unsigned long long* s_base) {
-  const unsigned m = __ballot_sync(0xffffffffu, take);
-  const int lane = threadIdx.x & 31;
-  unsigned woff = 0;
-  if (lane == 0 && m) woff = atomicAdd(s_cnt, static_cast<unsigned>(__popc(m)));
-  woff = __shfl_sync(0xffffffffu, woff, 0);
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    *s_base = *s_cnt ? atomicAdd(ctr, static_cast<unsigned long long>(*s_cnt)) : 0ull;
-    *s_cnt = 0;
-  }
-  __syncthreads();
-  return *s_base + woff + __popc(m & ((1u << lane) - 1u));
-}
-
 __device__ __forceinline__ bool higher(const Args& A, int64_t q, int64_t c) {
   const float eq = A.energy[q], ec = A.energy[c];
   return eq > ec || (eq == ec && q < c);  // argsort(-energy, stable) over ascending candidates
 }
 
+constexpr int SEED_CAP = 2048;  // seeds a CTA collects in smem before one global append
+
+// ratio / state / consumed for every cell, and the seed (candidate) list. A CTA
+// streams one contiguous range of cells (4 independent loads in flight per
+// thread), collects its seeds in smem and appends them with ONE global atomic
+// (a counter shared by the grid serialises at hundreds of thousands of atomics).
 __global__ void __launch_bounds__(NT) init_kernel(Args A) {
-  __shared__ unsigned s_cnt;
+  __shared__ int64_t seeds[SEED_CAP];
+  __shared__ unsigned s_n;
   __shared__ unsigned long long s_base;
-  if (threadIdx.x == 0) s_cnt = 0;
+  if (threadIdx.x == 0) s_n = 0;
   __syncthreads();
   const int64_t total = A.n * A.nevents;
-  // 4 cells per thread per iteration, strided by the grid (4 independent loads in flight per thread); the
-  // loop runs on the CTA's base index, so every thread takes part in every candidate append
-  const int64_t stride = static_cast<int64_t>(gridDim.x) * NT;
-  for (int64_t c0 = static_cast<int64_t>(blockIdx.x) * NT; c0 < total; c0 += 4 * stride) {
+  const int64_t chunk = ((total + gridDim.x - 1) / gridDim.x + 4 * NT - 1) / (4 * NT) * (4 * NT);
+  const int64_t start = static_cast<int64_t>(blockIdx.x) * chunk, end = min(total, start + chunk);
+  for (int64_t c0 = start; c0 < end; c0 += 4 * NT) {
     float e[4], nz[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      const int64_t i = c0 + u * stride + threadIdx.x;
-      e[u] = i < total ? A.energy[i] : 0.0f;
-      nz[u] = i < total ? A.noise[i] : 1.0f;
+      const int64_t i = c0 + u * NT + threadIdx.x;
+      e[u] = i < end ? A.energy[i] : 0.0f;
+      nz[u] = i < end ? A.noise[i] : 1.0f;
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      const int64_t i = c0 + u * stride + threadIdx.x;
-      bool seed = false;
-      if (i < total) {
+      const int64_t i = c0 + u * NT + threadIdx.x;
+      if (i < end) {
         const float r = __fdiv_rn(e[u], nz[u]);  // numpy f32 division (IEEE)
         A.ratio[i] = r;
         A.consumed[i] = 0;
-        seed = r > 5.0f;
+        const bool seed = r > 5.0f;
         A.state[i] = seed ? PENDING : NONE;
+        if (seed) {
+          const unsigned pos = atomicAdd(&s_n, 1u);
+          if (pos < SEED_CAP)
+            seeds[pos] = i;
+          else
+            A.cand[atomicAdd(&A.counters[0], 1ull)] = i;  // an unusually dense range: straight to global
+        }
       }
-      const unsigned long long slot = cta_append(&A.counters[0], seed, &s_cnt, &s_base);
-      if (seed) A.cand[slot] = i;
     }
   }
+  __syncthreads();
+  const unsigned m = min(s_n, static_cast<unsigned>(SEED_CAP));
+  if (threadIdx.x == 0) s_base = m ? atomicAdd(&A.counters[0], static_cast<unsigned long long>(m)) : 0ull;
+  __syncthreads();
+  for (unsigned j = threadIdx.x; j < m; j += NT) A.cand[s_base + j] = seeds[j];
 }
 
 // phase 1 of a round: which pending seeds are ready. One thread per
