@@ -987,7 +987,7 @@ __device__ __forceinline__ int64_t pred_sum(const FusedArgs& F, int64_t blk) {
 
 
 template <int MS, bool RS>
-__global__ void __launch_bounds__(F_NT, 2) pack_fused_kernel(const __grid_constant__ FusedArgs F) {
+__global__ void __launch_bounds__(F_NT, 3) pack_fused_kernel(const __grid_constant__ FusedArgs F) {
   extern __shared__ __align__(128) uint8_t fsm[];
   auto stage_all = reinterpret_cast<uint8_t(*)[F_NS][W * MS]>(fsm);
   FusedSmem& S = *reinterpret_cast<FusedSmem*>(fsm + F_NW * F_NS * W * MS);
