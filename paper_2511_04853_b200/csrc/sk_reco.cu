@@ -53,7 +53,7 @@ struct Args {
   uint8_t* state;
   uint8_t* consumed;
   int64_t* cand;
-  unsigned long long* counters;  // [0] ncand [1] nready [2] pending [3] nparticles
+  unsigned long long* counters;  // [0] ncand [1] nready [2] pending [3] unused [4] this round's first slot
   int64_t* ready;
   Slot* slots;
   uint64_t* contrib;  // MAXC per slot
@@ -163,8 +163,14 @@ __global__ void process_kernel(Args A) {
   const int64_t nwarps = static_cast<int64_t>(gridDim.x) * (NT / 32);
   for (int64_t k = static_cast<int64_t>(blockIdx.x) * (NT / 32) + (threadIdx.x >> 5); k < nready; k += nwarps) {
     const int64_t s = A.ready[k];
+    // slot = this round's first slot + the ready index (no shared particle counter); a skipped seed leaves
+    // a hole that the ordering pass drops
+    const unsigned long long p = A.counters[4] + static_cast<unsigned long long>(k);
     if (A.consumed[s]) {  // taken by an earlier particle: the reference skips it
-      if (lane == 0) A.state[s] = DECIDED;
+      if (lane == 0) {
+        A.state[s] = DECIDED;
+        A.slots[p].event = -1;
+      }
       continue;
     }
     const int64_t ev = s / A.n, base = ev * A.n, loc = s - base;
@@ -222,9 +228,6 @@ __global__ void process_kernel(Args A) {
       vx = __dadd_rn(vx, __dmul_rn(e, __dmul_rn(dx, dx)));
       vy = __dadd_rn(vy, __dmul_rn(e, __dmul_rn(dy, dy)));
     }
-    unsigned long long p = 0;
-    if (lane == 0) p = atomicAdd(&A.counters[3], 1ull);
-    p = __shfl_sync(0xffffffffu, p, 0);
     if (take) {  // contributor list, row-major: rank of this lane among the taken ones
       A.contrib[p * MAXC + __popc(mask & ((1u << lane) - 1u))] = static_cast<uint64_t>(f - base);
     }
@@ -254,12 +257,21 @@ __global__ void process_kernel(Args A) {
   }
 }
 
+// between rounds: the slots of the round just processed are taken, the
+// ready / pending counts start again
+__global__ void round_start_kernel(unsigned long long* counters) {
+  counters[4] += counters[1];
+  counters[1] = 0;
+  counters[2] = 0;
+}
+
 // order: bucket particles by event, then rank by priority inside the event
 __global__ void bucket_kernel(const Slot* slots, int64_t np, const int64_t* event_off,
                               unsigned long long* cursor, int64_t* order) {
   for (int64_t p = static_cast<int64_t>(blockIdx.x) * NT + threadIdx.x; p < np;
        p += static_cast<int64_t>(gridDim.x) * NT) {
     const int e = slots[p].event;
+    if (e < 0) continue;  // a seed consumed before its turn
     order[event_off[e] + static_cast<int64_t>(atomicAdd(&cursor[e], 1ull))] = p;
   }
 }
@@ -330,7 +342,8 @@ struct Handle {
   int device = 0;
   int64_t w = 0, h = 0, n = 0;
   int nevents = 0;
-  int64_t np = 0;
+  int64_t np = 0;      // particles
+  int64_t nslots = 0;  // particle slots written, holes (skipped seeds) included
   void* ws = nullptr;
   Args A;
   std::vector<int64_t> counts;
@@ -401,7 +414,7 @@ int sk_reco_run(int64_t w, int64_t h, int nevents, const float* energy, const fl
   unsigned long long pending = ncand;
   while (pending) {
     for (int k = 0; k < 4; ++k, ++r) {  // four rounds per host check
-      SK_TRY(cudaMemsetAsync(&A.counters[1], 0, 16, s));  // nready, pending
+      reco::round_start_kernel<<<1, 1, 0, s>>>(A.counters);
       reco::ready_kernel<<<rgrid, reco::NT, 0, s>>>(A);
       reco::process_kernel<<<cgrid, reco::NT, 0, s>>>(A);
     }
@@ -409,14 +422,19 @@ int sk_reco_run(int64_t w, int64_t h, int nevents, const float* energy, const fl
     SK_TRY(cudaMemcpyAsync(&pending, &A.counters[2], 8, cudaMemcpyDeviceToHost, s));
     SK_TRY(cudaStreamSynchronize(s));
   }
-  unsigned long long np = 0;
-  SK_TRY(cudaMemcpyAsync(&np, &A.counters[3], 8, cudaMemcpyDeviceToHost, s));
+  unsigned long long cnt[5] = {0, 0, 0, 0, 0};
+  SK_TRY(cudaMemcpyAsync(cnt, A.counters, sizeof(cnt), cudaMemcpyDeviceToHost, s));
   H->counts.assign(nevents, 0);
   std::vector<unsigned long long> ec(nevents > 0 ? nevents : 1);
   if (nevents) SK_TRY(cudaMemcpyAsync(ec.data(), A.event_count, nevents * 8, cudaMemcpyDeviceToHost, s));
   SK_TRY(cudaStreamSynchronize(s));
-  for (int i = 0; i < nevents; ++i) H->counts[i] = static_cast<int64_t>(ec[i]);
-  H->np = static_cast<int64_t>(np);
+  int64_t np = 0;
+  for (int i = 0; i < nevents; ++i) {
+    H->counts[i] = static_cast<int64_t>(ec[i]);
+    np += H->counts[i];
+  }
+  H->np = np;
+  H->nslots = static_cast<int64_t>(cnt[4] + cnt[1]);  // slots of every round, holes included
   *nparticles = H->np;
   if (rounds) *rounds = r;
   *handle = H;
@@ -454,8 +472,9 @@ int sk_reco_write(void* handle, float* energy, float* x, float* y, uint64_t* ori
   SK_TRY(cudaMemcpyAsync(d_off, off.data(), ev_bytes, cudaMemcpyHostToDevice, s));
   SK_TRY(cudaMemcpyAsync(d_cnt, H->counts.data(), H->nevents * 8, cudaMemcpyHostToDevice, s));
   SK_TRY(cudaMemsetAsync(cursor, 0, ev_bytes, s));
-  const int grid = std::max(1, std::min<int>(ds->sm_count * 8, static_cast<int>((H->np + reco::NT - 1) / reco::NT)));
-  reco::bucket_kernel<<<grid, reco::NT, 0, s>>>(H->A.slots, H->np, d_off, cursor, order);
+  const int bgrid =
+      std::max(1, std::min<int>(ds->sm_count * 8, static_cast<int>((H->nslots + reco::NT - 1) / reco::NT)));
+  reco::bucket_kernel<<<bgrid, reco::NT, 0, s>>>(H->A.slots, H->nslots, d_off, cursor, order);
   reco::OutArgs O;
   O.energy = energy; O.x = x; O.y = y; O.xvar = x_variance; O.yvar = y_variance; O.origin = origin;
   for (int t = 0; t < 4; ++t) {
