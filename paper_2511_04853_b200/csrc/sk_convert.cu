@@ -207,7 +207,11 @@ int make_plan(const sk_conv_desc& d, const DeviceState& ds, bool in_bulk_ok, boo
   const int64_t rec_sum = std::max<int64_t>(in_rec + out_rec, 1000);
   // many fields -> many small segment transfers per tile: smaller tiles, more CTAs per SM
   // (Particle, 18 fields: 0.68 -> 0.71 of the copy peak; <= 12 fields keep the larger tile)
-  const int tile_bytes = (!tun.tile_set && d.nfields > 12) ? 32768 : tun.tile_bytes;
+  // the fused case study (30 B Sensor records -> planes + energy + noise) measured best at 40 KB tiles on real
+  // events (tools/time_sensor.py: 123 us vs 128.5 us at 48 KB; 36 and 44 KB are worse -- the record-group
+  // rounding of R matters more than the size)
+  const int tile_bytes = tun.tile_set ? tun.tile_bytes : d.nfields > 12 ? 32768 : epi == EPI_SENSOR ? 40960
+                                                                                                  : tun.tile_bytes;
   int64_t R = (static_cast<int64_t>(tile_bytes) * 1000 / rec_sum) / g * g;
   R = std::max<int64_t>(R, g);
   R = std::min<int64_t>(R, std::max<int64_t>(g, 4096));
