@@ -170,9 +170,61 @@ struct Spec {
 
 // AoS source (any destination kind whose G consecutive records are contiguous
 // per field: PLANES, or AOSOA with lanes % G == 0) or PLANES source -> AoS.
+// Neither side AoS (PLANES <-> AOSOA, AOSOA <-> AOSOA): one thread moves 4
+// consecutive records of every field -- 4 typed shared-memory loads, a
+// compile-time cast, one vector store of the 4 values (both layouts keep 4
+// consecutive records of a field contiguous when the AoSoA width is a
+// multiple of 4).
+static bool generate_blocks(const sk_conv_desc& d, const Plan& P, Spec* out) {
+  constexpr int G = 4;
+  auto kind_ok = [&](int kind, int64_t lanes, int64_t stride, bool dst) {
+    if (kind == SK_KIND_PLANES) return true;
+    if (kind != SK_KIND_AOSOA || lanes % G || stride % 16) return false;
+    for (int f = 0; f < d.nfields; ++f)
+      if ((dst ? d.fields[f].dst_off : d.fields[f].src_off) % 16) return false;
+    return true;
+  };
+  if (P.epi || !kind_ok(d.src_kind, d.src_lanes, d.src_stride, false) ||
+      !kind_ok(d.dst_kind, d.dst_lanes, d.dst_stride, true) ||
+      (d.src_kind == SK_KIND_PLANES && d.dst_kind == SK_KIND_PLANES))
+    return false;
+  std::ostringstream k;
+  k << "b1|" << d.src_kind << "," << d.dst_kind;
+  for (int i = 0; i < d.nfields; ++i) k << "|" << d.fields[i].src_type << "," << d.fields[i].dst_type;
+  std::ostringstream o;
+  o << "#include \"sk_conv_device.cuh\"\nnamespace sk {\nnamespace conv {\n";
+  o << "struct SpecTransform {\n  static constexpr bool kFusedEpilogue = false;\n";
+  o << "  __device__ __forceinline__ static void run(const Plan& P, const uint8_t* __restrict__ in, "
+       "uint8_t* __restrict__ out, int rows, const int32_t*) {\n";
+  o << "    const int ngroups = (rows + " << G - 1 << ") / " << G << ";\n";
+  o << "#pragma unroll 1\n    for (int g = threadIdx.x; g < ngroups; g += NT) {\n";
+  o << "      const int r0 = g * " << G << ";\n      const bool full = r0 + " << G << " <= rows;\n";
+  for (int f = 0; f < d.nfields; ++f) {
+    const sk_field& F = d.fields[f];
+    const int ssz = dtype_size(F.src_type);
+    const char* st = ctype(F.src_type);
+    o << "      {\n        const uint8_t* s = in + (r0 >> P.src_lshift) * P.src_A + (r0 & P.src_msk) * " << ssz
+      << " + P.f[" << f << "].sloc;\n";
+    for (int i = 0; i < G; ++i)
+      o << "        const uint64_t v" << f << "_" << i << " = cast_bits((full || r0 + " << i << " < rows) ? "
+        << "static_cast<uint64_t>(*reinterpret_cast<const " << st << "*>(s + " << i * ssz << ")) : 0ull, "
+        << F.src_type << ", " << F.dst_type << ");\n";
+    const int dsz = dtype_size(F.dst_type);
+    std::ostringstream addr;
+    addr << "(out + (r0 >> P.dst_lshift) * P.dst_A + (r0 & P.dst_msk) * " << dsz << " + P.f[" << f << "].dloc)";
+    emit_group_store(o, addr.str(), f, G, dsz, "v");
+    o << "      }\n";
+  }
+  o << "    }\n  }\n};\n}  // namespace conv\n}  // namespace sk\n";
+  out->source = o.str();
+  out->key = k.str();
+  return true;
+}
+
 static bool generate(const sk_conv_desc& d, const Plan& P, const int* epi_fields, Spec* out) {
   const bool a2x = d.src_kind == SK_KIND_AOS && (d.dst_kind == SK_KIND_PLANES || d.dst_kind == SK_KIND_AOSOA);
   const bool p2a = d.src_kind == SK_KIND_PLANES && d.dst_kind == SK_KIND_AOS;
+  if (d.src_kind != SK_KIND_AOS && d.dst_kind != SK_KIND_AOS) return generate_blocks(d, P, out);
   if (!a2x && !p2a) return false;
   const int S = static_cast<int>(a2x ? d.src_stride : d.dst_stride);
   const int G = 4 / gcd_int(S, 4);

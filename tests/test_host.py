@@ -230,6 +230,12 @@ def test_specialised_transforms_compile_for_sm100a():
     ao.buffer = _Buf()
     st, src, err = _spec_check(cv._aosoa_desc(t.layout, ao, True))
     assert st == nat.SK_OK and "cast_bits(" in src, err
+    # per_field <-> AoSoA: the 4-records-per-thread block transform, both directions
+    tp = sk.Collection(wl.TRACK_SCHEMA, ly.PER_FIELD)
+    tp.resize(1000)
+    for to in (True, False):
+        st, src, err = _spec_check(cv._aosoa_desc(tp.layout, ao, to))
+        assert st == nat.SK_OK and "r0 >> P.src_lshift" in src and "uint4" in src, err
 
 
 # ---- the C-ABI library ---------------------------------------------------------------------
