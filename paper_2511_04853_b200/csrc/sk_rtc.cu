@@ -223,7 +223,7 @@ static bool generate_blocks(const sk_conv_desc& d, const Plan& P, Spec* out) {
 
 static bool generate(const sk_conv_desc& d, const Plan& P, const int* epi_fields, Spec* out) {
   const bool a2x = d.src_kind == SK_KIND_AOS && (d.dst_kind == SK_KIND_PLANES || d.dst_kind == SK_KIND_AOSOA);
-  const bool p2a = d.src_kind == SK_KIND_PLANES && d.dst_kind == SK_KIND_AOS;
+  const bool p2a = (d.src_kind == SK_KIND_PLANES || d.src_kind == SK_KIND_AOSOA) && d.dst_kind == SK_KIND_AOS;
   if (d.src_kind != SK_KIND_AOS && d.dst_kind != SK_KIND_AOS) return generate_blocks(d, P, out);
   if (!a2x && !p2a) return false;
   const int S = static_cast<int>(a2x ? d.src_stride : d.dst_stride);
@@ -300,10 +300,10 @@ static bool generate(const sk_conv_desc& d, const Plan& P, const int* epi_fields
       const sk_field& F = d.fields[f];
       const int ssz = dtype_size(F.src_type);
       const char* st = ctype(F.src_type);
-      for (int i = 0; i < G; ++i)
+      for (int i = 0; i < G; ++i)  // (r >> lshift) * A + (r & msk) * size + loc: planes or AoSoA blocks
         o << "      const uint64_t r" << f << "_" << i << " = (full || r0 + " << i << " < rows) ? static_cast<uint64_t>("
-          << "*reinterpret_cast<const " << st << "*>(in + P.f[" << f << "].sloc + (r0 + " << i << ") * " << ssz
-          << ")) : 0ull;\n";
+          << "*reinterpret_cast<const " << st << "*>(in + ((r0 + " << i << ") >> P.src_lshift) * P.src_A + ((r0 + " << i
+          << ") & P.src_msk) * " << ssz << " + P.f[" << f << "].sloc)) : 0ull;\n";
       for (int i = 0; i < G; ++i)
         o << "      const uint64_t v" << f << "_" << i << " = cast_bits(r" << f << "_" << i << ", " << F.src_type << ", "
           << F.dst_type << ");\n";
@@ -401,7 +401,8 @@ int launch_specialized(const sk_conv_desc& d, const Plan& P, const DeviceState& 
                        cudaStream_t s, bool* launched) {
   *launched = false;
   if (!specialise_enabled() || P.ntiles == 0) return SK_OK;
-  if (P.n_elem == 0 && !P.epi) return SK_OK;  // pure word mode is already at the copy roofline
+  // pure word mode is already at the copy roofline -- except out of AoSoA tiles (0.83 vs 0.93+ specialised)
+  if (P.n_elem == 0 && !P.epi && d.src_kind != SK_KIND_AOSOA) return SK_OK;
   Spec spec;
   if (!generate(d, P, epi_fields, &spec)) return SK_OK;
   Compiled* c = nullptr;

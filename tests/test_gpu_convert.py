@@ -287,10 +287,12 @@ def test_engine_uses_tma_bulk_path_for_aligned_collections():
     assert info["bulk_in"] and info["bulk_out"] and info["mode"] == 1
 
 
+@pytest.mark.parametrize("back_kind", [ly.PER_FIELD, ly.AOS])
 @pytest.mark.parametrize("lanes", [4, 32, 64])
-def test_aosoa_to_planes_all_fields_vs_records(lanes):
-    """AoSoA -> per_field (the block-to-block specialised transform): identity fields come back bit-exact,
-    f64 fields stored as f32 come back as f64(f32(x)) (numpy astype both ways)"""
+def test_aosoa_to_planes_all_fields_vs_records(lanes, back_kind):
+    """AoSoA -> per_field (the block transform) and AoSoA -> AoS (the record-group transform reading AoSoA
+    blocks): identity fields come back bit-exact, f64 fields stored as f32 come back as f64(f32(x))
+    (numpy astype both ways)"""
     n = 50_001
     recs = wl.track_records(n)
     host = aos_collection(wl.TRACK_SCHEMA, recs, n, PINNED)
@@ -300,7 +302,7 @@ def test_aosoa_to_planes_all_fields_vs_records(lanes):
     code = {"charge": "i32", "id": "u64"}
     fields = [sk.AosoaField(nm, "f32" if nm in ("px", "py") else code.get(nm, "f64")) for nm in names]
     a = sk.to_aosoa(src, fields, lanes)
-    back = sk.Collection(wl.TRACK_SCHEMA, ly.PER_FIELD, CUDA)
+    back = sk.Collection(wl.TRACK_SCHEMA, back_kind, CUDA)
     sk.from_aosoa(a, back)
     with mc.execution_scope(mc.CUDA):
         for nm in names:
