@@ -58,4 +58,20 @@ noise = DeviceArray(len(a), np.float32, CUDA)
 sensor.transfer_calibrate(p, a, noise)
 parts = sk.Collection(sensor.PARTICLE_SCHEMA, ly.PER_FIELD, CUDA)
 sensor.reconstruct_from_collection(p, 40, 30, out=parts, events=2, noise=noise)
+# AoSoA: AoS -> AoSoA (record groups), per_field -> AoSoA and AoSoA -> per_field (block transform),
+# AoSoA -> AoS (record groups reading AoSoA blocks)
+for m in (3, 1001):
+    trk = sk.Collection(wl.TRACK_SCHEMA, ly.AOS, mc.ContextInfo.pinned())
+    trk.resize(m)
+    trk.layout._struct_buf._data[: m * 60] = wl.track_records(m).view(np.uint8)
+    ta = sk.Collection(wl.TRACK_SCHEMA, ly.AOS, CUDA)
+    tr.copy_collection(ta, trk)
+    tp = sk.Collection(wl.TRACK_SCHEMA, ly.PER_FIELD, CUDA)
+    tr.copy_collection(tp, ta)
+    flds = [sk.AosoaField("pz", "f32"), sk.AosoaField("charge", "i32"), sk.AosoaField("id", "u64")]
+    for src in (ta, tp):
+        ao = sk.to_aosoa(src, flds, 32)
+        sk.from_aosoa(ao, tp)
+        sk.from_aosoa(ao, ta)
+        ao.free()
 print("sanitize paths done", len(parts))
