@@ -189,7 +189,8 @@ static bool generate_blocks(const sk_conv_desc& d, const Plan& P, Spec* out) {
       (d.src_kind == SK_KIND_PLANES && d.dst_kind == SK_KIND_PLANES))
     return false;
   std::ostringstream k;
-  k << "b1|" << d.src_kind << "," << d.dst_kind;
+  k << "b1|" << d.src_kind << "," << d.dst_kind << "," << d.src_lanes << "," << d.dst_lanes << ","
+    << (d.src_kind == SK_KIND_AOSOA ? d.src_stride : 0) << "," << (d.dst_kind == SK_KIND_AOSOA ? d.dst_stride : 0);
   for (int i = 0; i < d.nfields; ++i) k << "|" << d.fields[i].src_type << "," << d.fields[i].dst_type;
   std::ostringstream o;
   o << "#include \"sk_conv_device.cuh\"\nnamespace sk {\nnamespace conv {\n";
@@ -203,15 +204,23 @@ static bool generate_blocks(const sk_conv_desc& d, const Plan& P, Spec* out) {
     const sk_field& F = d.fields[f];
     const int ssz = dtype_size(F.src_type);
     const char* st = ctype(F.src_type);
-    o << "      {\n        const uint8_t* s = in + (r0 >> P.src_lshift) * P.src_A + (r0 & P.src_msk) * " << ssz
-      << " + P.f[" << f << "].sloc;\n";
+    o << "      {\n        const uint8_t* s = in + P.f[" << f << "].sloc + ";
+    if (d.src_kind == SK_KIND_PLANES)
+      o << "r0 * " << ssz << ";\n";
+    else
+      o << "(r0 >> " << P.src_lshift << ") * " << d.src_stride << " + (r0 & " << d.src_lanes - 1 << ") * " << ssz
+        << ";\n";
     for (int i = 0; i < G; ++i)
       o << "        const uint64_t v" << f << "_" << i << " = cast_bits((full || r0 + " << i << " < rows) ? "
         << "static_cast<uint64_t>(*reinterpret_cast<const " << st << "*>(s + " << i * ssz << ")) : 0ull, "
         << F.src_type << ", " << F.dst_type << ");\n";
     const int dsz = dtype_size(F.dst_type);
     std::ostringstream addr;
-    addr << "(out + (r0 >> P.dst_lshift) * P.dst_A + (r0 & P.dst_msk) * " << dsz << " + P.f[" << f << "].dloc)";
+    if (d.dst_kind == SK_KIND_PLANES)
+      addr << "(out + P.f[" << f << "].dloc + r0 * " << dsz << ")";
+    else
+      addr << "(out + P.f[" << f << "].dloc + (r0 >> " << P.dst_lshift << ") * " << d.dst_stride << " + (r0 & "
+           << d.dst_lanes - 1 << ") * " << dsz << ")";
     emit_group_store(o, addr.str(), f, G, dsz, "v");
     o << "      }\n";
   }
@@ -238,7 +247,8 @@ static bool generate(const sk_conv_desc& d, const Plan& P, const int* epi_fields
   if (P.epi && !a2x) return false;
 
   std::ostringstream k;  // the signature: everything the generated code bakes in
-  k << "v1|" << d.src_kind << "," << d.dst_kind << "," << S << "," << G << "," << P.epi;
+  k << "v1|" << d.src_kind << "," << d.dst_kind << "," << S << "," << G << "," << P.epi << "," << d.src_lanes << ","
+    << (d.src_kind == SK_KIND_AOSOA ? d.src_stride : 0);
   for (int i = 0; i < d.nfields; ++i)
     k << "|" << d.fields[i].src_type << "," << d.fields[i].dst_type << "," << d.fields[i].src_off << ","
       << d.fields[i].dst_off;
@@ -255,7 +265,15 @@ static bool generate(const sk_conv_desc& d, const Plan& P, const int* epi_fields
   o << "      const int r0 = g * " << G << ";\n      const bool full = r0 + " << G << " <= rows;\n";
   if (a2x) {
     o << "      const uint32_t* w = reinterpret_cast<const uint32_t*>(in) + g * " << GW << ";\n";
-    for (int q = 0; q < GW; ++q) o << "      const uint32_t W" << q << " = w[" << q << "];\n";
+    if (GW % 4 == 0) {
+      // an even group stride in words puts many lanes on one bank: 16-byte loads cut the conflicts 4x
+      for (int q = 0; q < GW / 4; ++q) {
+        o << "      const uint4 Q" << q << " = reinterpret_cast<const uint4*>(w)[" << q << "];\n";
+        for (int l = 0; l < 4; ++l) o << "      const uint32_t W" << 4 * q + l << " = Q" << q << "." << "xyzw"[l] << ";\n";
+      }
+    } else {
+      for (int q = 0; q < GW; ++q) o << "      const uint32_t W" << q << " = w[" << q << "];\n";
+    }
     // extract + cast every field of every record
     for (int f = 0; f < d.nfields; ++f) {
       const sk_field& F = d.fields[f];
@@ -300,15 +318,23 @@ static bool generate(const sk_conv_desc& d, const Plan& P, const int* epi_fields
       const sk_field& F = d.fields[f];
       const int ssz = dtype_size(F.src_type);
       const char* st = ctype(F.src_type);
-      for (int i = 0; i < G; ++i)  // (r >> lshift) * A + (r & msk) * size + loc: planes or AoSoA blocks
+      for (int i = 0; i < G; ++i) {
+        // planes: loc + r * size; AoSoA blocks (lanes, tile baked in): (r >> log2 lanes) * tile + (r & lanes-1) * size + loc
+        std::ostringstream a;
+        if (d.src_kind == SK_KIND_PLANES)
+          a << "(r0 + " << i << ") * " << ssz;
+        else
+          a << "((r0 + " << i << ") >> " << P.src_lshift << ") * " << d.src_stride << " + ((r0 + " << i
+            << ") & " << d.src_lanes - 1 << ") * " << ssz;
         o << "      const uint64_t r" << f << "_" << i << " = (full || r0 + " << i << " < rows) ? static_cast<uint64_t>("
-          << "*reinterpret_cast<const " << st << "*>(in + ((r0 + " << i << ") >> P.src_lshift) * P.src_A + ((r0 + " << i
-          << ") & P.src_msk) * " << ssz << " + P.f[" << f << "].sloc)) : 0ull;\n";
+          << "*reinterpret_cast<const " << st << "*>(in + P.f[" << f << "].sloc + " << a.str() << ")) : 0ull;\n";
+      }
       for (int i = 0; i < G; ++i)
         o << "      const uint64_t v" << f << "_" << i << " = cast_bits(r" << f << "_" << i << ", " << F.src_type << ", "
           << F.dst_type << ");\n";
     }
     o << "      uint32_t* w = reinterpret_cast<uint32_t*>(out) + g * " << GW << ";\n";
+    const bool vec = GW % 4 == 0;  // an even group stride in words: 16-byte stores (4x fewer bank conflicts)
     for (int q = 0; q < GW; ++q) {
       std::ostringstream expr;
       bool any = false;
@@ -325,7 +351,13 @@ static bool generate(const sk_conv_desc& d, const Plan& P, const int* epi_fields
           any = true;
         }
       }
-      o << "      w[" << q << "] = " << (any ? expr.str() : std::string("0u")) << ";\n";
+      if (vec)
+        o << "      const uint32_t O" << q << " = " << (any ? expr.str() : std::string("0u")) << ";\n";
+      else
+        o << "      w[" << q << "] = " << (any ? expr.str() : std::string("0u")) << ";\n";
+      if (vec && q % 4 == 3)
+        o << "      reinterpret_cast<uint4*>(w)[" << q / 4 << "] = make_uint4(O" << q - 3 << ", O" << q - 2 << ", O" << q - 1
+          << ", O" << q << ");\n";
     }
   }
   o << "    }\n  }\n};\n}  // namespace conv\n}  // namespace sk\n";
@@ -402,7 +434,16 @@ int launch_specialized(const sk_conv_desc& d, const Plan& P, const DeviceState& 
   *launched = false;
   if (!specialise_enabled() || P.ntiles == 0) return SK_OK;
   // pure word mode is already at the copy roofline -- except out of AoSoA tiles (0.83 vs 0.93+ specialised)
-  if (P.n_elem == 0 && !P.epi && d.src_kind != SK_KIND_AOSOA) return SK_OK;
+  static const bool force = [] {
+    const char* v = getenv("SK_SPECIALIZE");
+    return v && v[0] == '2';
+  }();
+  // word mode with sub-word slots (1-/2-byte fields) in a 16-byte-multiple record (Particle's 64 B with
+  // noisy_count[4]) loses to the record-group transform: 0.70 -> 0.88 / 0.92 for Particle AoS <-> planes; in
+  // odd-stride records (Sensor, 30 B) word mode stays ahead (planes -> AoS 1.00 vs 0.76)
+  const int64_t aos_stride = d.src_kind == SK_KIND_AOS ? d.src_stride : d.dst_kind == SK_KIND_AOS ? d.dst_stride : 0;
+  const bool subword_even = P.nsub > 0 && aos_stride % 16 == 0;
+  if (P.n_elem == 0 && !P.epi && d.src_kind != SK_KIND_AOSOA && !subword_even && !force) return SK_OK;
   Spec spec;
   if (!generate(d, P, epi_fields, &spec)) return SK_OK;
   Compiled* c = nullptr;

@@ -235,7 +235,7 @@ def test_specialised_transforms_compile_for_sm100a():
     tp.resize(1000)
     for to in (True, False):
         st, src, err = _spec_check(cv._aosoa_desc(tp.layout, ao, to))
-        assert st == nat.SK_OK and "r0 >> P.src_lshift" in src and "uint4" in src, err
+        assert st == nat.SK_OK and "(r0 >> 7) * 2048" in src and "uint4" in src, err  # T = 128 baked in
 
 
 # ---- the C-ABI library ---------------------------------------------------------------------
