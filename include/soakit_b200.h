@@ -178,9 +178,14 @@ int sk_jagged_scatter(int64_t n, const void* prefix, int prefix_type,
    sized by the pools' `capacity` (members) and reads the true total from
    *total_dev on the device, so it is complete iff *total_dev <= capacity; the
    caller reads *total_dev afterwards and, on overflow, grows the pools and
-   gathers again with sk_jagged_scatter. Scratch: at least sk_jagged_scratch_bytes;
-   with (ceil(capacity / 256) + 1) * 8 more bytes after it (256-aligned) the
-   call allocates nothing (the scan writes the gather's work split there). */
+   gathers again with sk_jagged_scatter. One naturally aligned 4/8-byte member
+   field (16-byte-aligned pool), or 2-4 such fields of an 8/16-byte member
+   record, runs as ONE kernel (prefixes and gather fused; the scratch holds its
+   per-block status words). Other member layouts run the scan and the gather
+   back to back. Scratch: at least sk_jagged_scratch_bytes; with
+   (ceil(capacity / 256) + 1) * 8 more bytes after it (256-aligned) the
+   two-kernel path allocates nothing (the scan writes the gather's work split
+   there). The scratch is not retained after the call's work completes. */
 int sk_jagged_pack(int64_t n, const void* lens, int lens_type, void* prefix,
                    int prefix_type, const int64_t* src_off, const void* src_pool,
                    int64_t member_stride, int nfields, const int64_t* field_off,
