@@ -413,7 +413,8 @@ int sk_reco_run(int64_t w, int64_t h, int nevents, const float* energy, const fl
   int r = 0;
   unsigned long long pending = ncand;
   while (pending) {
-    for (int k = 0; k < 4; ++k, ++r) {  // four rounds per host check
+    // rounds per host check: 8 first (full events converge in ~6), then 4
+    for (int k = 0; k < (r ? 4 : 8); ++k, ++r) {
       reco::round_start_kernel<<<1, 1, 0, s>>>(A.counters);
       reco::ready_kernel<<<rgrid, reco::NT, 0, s>>>(A);
       reco::process_kernel<<<cgrid, reco::NT, 0, s>>>(A);
