@@ -291,13 +291,16 @@ constexpr int RANK_SMEM = 4096;  // particles of one event ranked out of shared 
 // one CTA per event: the event's priority keys go to smem (broadcast reads),
 // each particle's rank = how many keys outrank it; events with more particles
 // than RANK_SMEM read the keys from global memory instead
+constexpr int RANK_SPLIT = 4;                 // threads per particle in the ranking
+constexpr int RANK_PER_CTA = NT / RANK_SPLIT;  // particles ranked per CTA
+
 __global__ void __launch_bounds__(NT) write_kernel(const Slot* slots, const int64_t* event_off,
                                                    const int64_t* event_cnt, const int64_t* order, OutArgs O) {
   __shared__ float ke[RANK_SMEM];
   __shared__ int64_t ko[RANK_SMEM];
   const int64_t ev = blockIdx.x;
   const int64_t b = event_off[ev], m = event_cnt[ev];
-  const int64_t first = static_cast<int64_t>(blockIdx.y) * NT;  // this CTA ranks particles [first, first + NT)
+  const int64_t first = static_cast<int64_t>(blockIdx.y) * RANK_PER_CTA;  // particles [first, first + RANK_PER_CTA)
   if (first >= m) return;
   const bool in_smem = m <= RANK_SMEM;
   if (in_smem)
@@ -307,20 +310,29 @@ __global__ void __launch_bounds__(NT) write_kernel(const Slot* slots, const int6
       ko[j] = Q.origin;
     }
   __syncthreads();
-  for (int64_t i = first + threadIdx.x; i < m; i += static_cast<int64_t>(gridDim.y) * NT) {
-    const int64_t p = order[b + i];
+  const int q = threadIdx.x % RANK_SPLIT;  // this thread counts keys j = q, q + RANK_SPLIT, ...
+  for (int64_t i0 = first; i0 < m; i0 += static_cast<int64_t>(gridDim.y) * RANK_PER_CTA) {
+    const int64_t i = i0 + threadIdx.x / RANK_SPLIT;
+    const bool have = i < m;
+    const int64_t p = have ? order[b + i] : 0;
     const Slot& S = slots[p];
-    const float se = S.key_e;
-    const int64_t so = S.origin;
+    const float se = have ? S.key_e : 0.0f;
+    const int64_t so = have ? S.origin : 0;
     int64_t rank = 0;
-    if (in_smem) {
-      for (int64_t j = 0; j < m; ++j) rank += (ke[j] > se) || (ke[j] == se && ko[j] < so);
-    } else {
-      for (int64_t j = 0; j < m; ++j) {
-        const Slot& Q = slots[order[b + j]];
-        rank += (Q.key_e > se) || (Q.key_e == se && Q.origin < so);
+    if (have) {
+      if (in_smem) {
+        for (int64_t j = q; j < m; j += RANK_SPLIT)
+          rank += static_cast<int>(ke[j] > se) | (static_cast<int>(ke[j] == se) & static_cast<int>(ko[j] < so));
+      } else {
+        for (int64_t j = q; j < m; j += RANK_SPLIT) {
+          const Slot& Q = slots[order[b + j]];
+          rank += static_cast<int>(Q.key_e > se) | (static_cast<int>(Q.key_e == se) & static_cast<int>(Q.origin < so));
+        }
       }
     }
+#pragma unroll
+    for (int o = 1; o < RANK_SPLIT; o <<= 1) rank += __shfl_xor_sync(0xffffffffu, rank, o);
+    if (!have || q) continue;
     const int64_t o = b + rank;
     O.energy[o] = S.energy;
     O.x[o] = S.x;
@@ -487,7 +499,8 @@ int sk_reco_write(void* handle, float* energy, float* x, float* y, uint64_t* ori
   O.offsets = sensor_offsets;
   int64_t mmax = 0;
   for (int i = 0; i < H->nevents; ++i) mmax = std::max(mmax, H->counts[i]);
-  const unsigned chunks = static_cast<unsigned>(std::min<int64_t>((mmax + reco::NT - 1) / reco::NT, 65535));
+  const unsigned chunks =
+      static_cast<unsigned>(std::min<int64_t>((mmax + reco::RANK_PER_CTA - 1) / reco::RANK_PER_CTA, 65535));
   if (H->nevents && chunks)
     reco::write_kernel<<<dim3(H->nevents, chunks), reco::NT, 0, s>>>(H->A.slots, d_off, d_cnt, order, O);
   SK_TRY(cudaGetLastError());
