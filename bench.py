@@ -192,7 +192,7 @@ def run_ours(args) -> None:
     aos = device_collection(wl.OBJ8_SCHEMA, ly.AOS, n, ipc=world > 1)  # exportable: the P2P leg pulls it
     soa = device_collection(wl.OBJ8_SCHEMA, ly.PER_FIELD, n)
     # the global 1e9-record image is splitmix64(seed, word); this shard is its slice
-    wl.fill_random_device(aos.layout._struct_buf.ptr, n * 32, seed=20251104, device=dev, first_word=lo * 4)
+    wl.fill_random_device(aos.layout._struct_buf.ptr, n * 32, seed=SEED, device=dev, first_word=lo * 4)
 
     def step():
         tr.copy_collection(soa, aos, {"async": True})
@@ -218,18 +218,8 @@ def run_ours(args) -> None:
     launch_ms = max_over_ranks(statistics.mean(per_launch))
     achieved = n * BYTES_PER_OBJECT / (launch_ms / 1e3) / 1e9  # per GPU, slowest rank's launch time
 
-    # parity spot check of the timed output (first 4096 records of this shard)
-    probe = 4096 if n >= 4096 else n
-    raw = np.empty(probe * 32, np.uint8)
-    nat.memcpy(raw.ctypes.data, aos.layout._struct_buf.ptr, raw.nbytes, dev)
-    nat.sync(dev)
-    rec = raw.view(wl.OBJ8_AOS_DTYPE)
-    for i in range(8):
-        got = np.empty(probe, rec.dtype[i])
-        nat.memcpy(got.ctypes.data, soa.layout.plane_address(soa.plan.leaf(f"f{i}")), got.nbytes, dev)
-        nat.sync(dev)
-        if got.tobytes() != np.ascontiguousarray(rec[f"f{i}"]).tobytes():
-            raise SystemExit(f"rank {rank}: converted plane f{i} differs from the AoS input")
+    # parity of the timed output at full scale (the run fails on any mismatch)
+    parity = verify_obj8_shard(aos, soa, n, lo, dev, rank)
 
     # ---- e2e: pinned HOST AoS -> device SoA through the public API, result read back ----
     m = min(args.e2e_objects, n)
@@ -396,7 +386,7 @@ def run_ours(args) -> None:
         "scaling": "strong",
         "vs_baseline": None,
         "dtype": "u8",
-        "data": "synthetic (splitmix64 record images generated on-device, seed 20251104)",
+        "data": f"synthetic (splitmix64 record images generated on-device, seed {SEED})",
         "config": {"workload": WORKLOAD, "objects_total": n_total, "objects_per_gpu": n, "record_bytes": 32,
                    "algorithmic_bytes_per_object": BYTES_PER_OBJECT,
                    "sharding": "contiguous object-index ranges, no data-path collective",
@@ -417,6 +407,7 @@ def run_ours(args) -> None:
         "gpu_launches": args.steps,
         "clocks": clk,
         "cpu_baseline": cpu,
+        "parity": parity,
     }
     if p2p:
         line["p2p"] = p2p
@@ -425,6 +416,114 @@ def run_ours(args) -> None:
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+SEED = 20251104
+
+
+def verify_obj8_shard(aos, soa, n: int, lo: int, dev: int, rank: int) -> dict:
+    """Check the converted shard two ways; SystemExit on any mismatch.
+
+    1. Sampled records against the CPU oracle (oracle/restate.splitmix_image:
+       the input image restated from its definition, not read back): the
+       first and last 4096-record tiles, the tiles that start at AoS byte
+       offsets 2^32, 2^33, 2^34 (past any 32-bit offset), and 64 seeded
+       random tiles. Semantics: transfer.py:196-233 / layouts.py:573-598.
+    2. Every record: the planes are converted back to AoS (K2) into a third
+       buffer and compared byte-for-byte with the input AoS on the device
+       (sk_compare_bytes), so the whole 32 GB image is covered."""
+    import ctypes as C
+
+    import numpy as np
+
+    from oracle import restate
+    from paper_2511_04853_b200 import _native as nat
+    from paper_2511_04853_b200 import layouts as ly, memctx as mc, schema as sc, transfer as tr
+    from paper_2511_04853_b200 import workloads as wl
+    import paper_2511_04853_b200 as sk
+
+    t = min(4096, n)
+    starts = {0, n - t}
+    for e in (32, 33, 34):
+        r = (1 << e) // 32
+        if r + t <= n:
+            starts.add(r)
+    rng = np.random.default_rng(1234 + rank)
+    starts.update(int(x) for x in rng.integers(0, max(1, n - t + 1), 64))
+    got = np.empty(t * 4, np.uint8)
+    for r0 in sorted(starts):
+        want = restate.splitmix_image(SEED, lo * 4, r0 * 32, t * 32).view(wl.OBJ8_AOS_DTYPE)
+        for i in range(8):
+            nat.memcpy(got.ctypes.data, soa.layout.plane_address(soa.plan.leaf(f"f{i}")) + r0 * 4, got.nbytes, dev)
+            nat.sync(dev)
+            if got.tobytes() != np.ascontiguousarray(want[f"f{i}"]).tobytes():
+                raise SystemExit(f"rank {rank}: plane f{i} of records [{r0}, {r0 + t}) differs from the oracle")
+    back = sk.Collection(wl.OBJ8_SCHEMA, ly.AOS, mc.ContextInfo.cuda(dev))
+    with mc.execution_scope(mc.CUDA):
+        back.reserve(n)
+    tr.copy_collection(back, soa)
+    bad = nat.malloc(dev, 8)
+    nat.call("sk_compare_bytes", back.layout._struct_buf.ptr, aos.layout._struct_buf.ptr, n * 32, bad,
+             nat.stream(dev))
+    cnt = C.c_uint64(0)
+    nat.memcpy(C.addressof(cnt), bad, 8, dev)
+    nat.sync(dev)
+    nat.free(dev, bad)
+    back.free()
+    if cnt.value:
+        raise SystemExit(f"rank {rank}: AoS -> planes -> AoS round trip differs in {cnt.value} bytes")
+    return {"sampled_vs_oracle": f"{len(starts)} tiles of {t} records (first, last, AoS byte offsets 2^32/2^33/2^34, "
+                                 "64 random) x 8 planes, byte-exact vs oracle/restate.splitmix_image",
+            "full_round_trip": f"{n} records: planes -> AoS (K2) == input AoS, 0 of {n * 32} bytes differ "
+                               "(sk_compare_bytes on the device)"}
+
+
+def verify_aosoa_tiles(ao, n: int, fields, dev: int, seed: int = 4, samples: int = 32) -> str:
+    """First, last and random AoSoA tiles vs oracle/restate.to_aosoa over the
+    Track records restated from the splitmix image (seed 4, word 0)."""
+    import numpy as np
+
+    from oracle import restate
+    from paper_2511_04853_b200 import _native as nat
+    from paper_2511_04853_b200 import workloads as wl
+
+    lanes, tb = ao.lanes, ao.tile_bytes
+    rng = np.random.default_rng(99)
+    tiles = sorted({0, ao.ntiles - 1, *(int(x) for x in rng.integers(0, ao.ntiles, samples))})
+    spec = [(f.leaf, f.dtype) for f in fields]
+    got = np.empty(tb, np.uint8)
+    for t in tiles:
+        r0, r1 = t * lanes, min(n, (t + 1) * lanes)
+        rec = restate.splitmix_image(seed, 0, r0 * 60, (r1 - r0) * 60).view(wl.TRACK_AOS_DTYPE)
+        want = restate.to_aosoa(rec, spec, lanes, tb)
+        nat.memcpy(got.ctypes.data, ao.buffer.ptr + t * tb, tb, dev)
+        nat.sync(dev)
+        if got.tobytes() != want:
+            raise SystemExit(f"config 4: AoSoA tile {t} (T={lanes}) differs from the oracle")
+    return f"{len(tiles)} tiles (first, last, random) byte-exact vs oracle/restate.to_aosoa"
+
+
+def verify_sensor_events(coll, noise, dev: int, events) -> str:
+    """Energy and noise of sampled events vs the oracle's event generator and
+    case-study arithmetic (events.py:85-133, detector/schemas.py:29-41)."""
+    import numpy as np
+
+    from oracle import restate
+    from paper_2511_04853_b200 import _native as nat
+
+    n = 436 * 436
+    e_ptr = coll.layout.plane_address(coll.plan.leaf("energy"))
+    for e in events:
+        ev = restate.generate_event(436, 436, seed=e, density=0.002)
+        energy = restate.calibrate(ev["counts"], ev["parameter_A"], ev["parameter_B"])
+        want_noise = restate.noise(energy, ev["noise_A"], ev["noise_B"], ev["noisy"])
+        got_e, got_n = np.empty(n, np.float32), np.empty(n, np.float32)
+        nat.memcpy(got_e.ctypes.data, e_ptr + e * n * 4, n * 4, dev)
+        nat.memcpy(got_n.ctypes.data, noise.ptr + e * n * 4, n * 4, dev)
+        nat.sync(dev)
+        if got_e.tobytes() != energy.tobytes() or got_n.tobytes() != want_noise.tobytes():
+            raise SystemExit(f"config 2: event {e} energy/noise differ from the oracle")
+    return f"events {list(events)}: energy and noise bit-exact vs the oracle (generate_event + calibrate + noise)"
 
 
 def _traffic(n: int):
@@ -524,6 +623,7 @@ def run_extras(args, dev: int) -> dict:
         "event_generation_ms": round(ms_gen, 3), "event_generation_cells_per_s": round(cells / ms_gen * 1e3),
         "data": "64 events 436x436, seeds 0..63, density 0.002, generated on-device (bit-exact with "
                 "detector/events.py:85-133)"}
+    out["config2_sensor_64x190096"]["parity"] = verify_sensor_events(p2, noise, dev, (0, 31, 63))
     # the reference's second phase on the same events: reconstruct + transfer back (bench.py:180-184)
     from paper_2511_04853_b200 import sensor as sn
 
@@ -561,13 +661,19 @@ def run_extras(args, dev: int) -> dict:
     need = C.c_size_t(0)
     nat.call("sk_jagged_scratch_bytes", nc, C.byref(need))
     scratch = DeviceArray(-(-need.value // 256) * 256 + ((cap + 255) // 256 + 1) * 8, np.uint8, cuda)
-    total = DeviceArray(1, np.int64, cuda)
+    total = DeviceArray(2, np.int64, cuda)
     pool_out = DeviceArray(cap, np.uint64, cuda)
     foff, fsz, dst = (C.c_int64 * 1)(0), (C.c_int32 * 1)(8), (C.c_void_p * 1)(pool_out.ptr)
     strm = nat.stream(dev)
-    ms = queued(lambda: nat.call("sk_jagged_pack", nc, d_lens.ptr, i32, prefix.ptr, i32, d_off.ptr, d_pool.ptr, 8, 1,
-                                 foff, fsz, dst, cap, scratch.ptr, scratch.n, total.ptr, strm), steps=20)
+    ms = queued(lambda: nat.call("sk_jagged_pack", nc, d_lens.ptr, i32, prefix.ptr, i32, d_off.ptr, d_pool.ptr,
+                                 pool.size, 8, 1, foff, fsz, dst, cap, scratch.ptr, scratch.n, total.ptr, strm),
+                steps=20)
     algo = nc * 16 + members * 16
+    from oracle import restate
+
+    want_p, want_m = restate.jagged_pack(lens, offsets, pool, np.int32)
+    if prefix.numpy().tobytes() != want_p.tobytes() or pool_out.numpy()[:members].tobytes() != want_m.tobytes():
+        raise SystemExit("config 3: packed prefix/pool differ from the oracle")
     out["config3_jagged_1M"] = {
         "members": members, "device_ms": round(ms, 4), "members_per_s": round(members / ms * 1e3),
         "gbs": round(algo / ms / 1e6, 1), "frac": round(algo / ms / 1e6 / peak, 3),
@@ -575,7 +681,8 @@ def run_extras(args, dev: int) -> dict:
         "note": "device_ms: sk_jagged_pack (one fused kernel: block sums, prefixes, gather) queued on the device; "
                 "api_ms: jagged.pack on a "
                 "Collection, incl. the host readback of the member total that sizes the pool; source segments "
-                "in shuffled order with slack, so ~125 MB of 32 B sectors are read for 92 MB of payload"}
+                "in shuffled order with slack, so ~125 MB of 32 B sectors are read for 92 MB of payload",
+        "parity": "whole prefix (1,000,001 x i32) and pool byte-exact vs oracle/restate.jagged_pack"}
     c3.free()
     for d in (d_lens, d_off, d_pool, prefix, scratch, total, pool_out):
         d.free()
@@ -590,13 +697,15 @@ def run_extras(args, dev: int) -> dict:
     ms = queued(lambda: sk.to_aosoa(a4, fields, 128, out=ao, sync=False), steps=10)
     out["config4_aosoa_100M"] = {"ms": round(ms, 3), "gbs": round(n4 * 76 / ms / 1e6, 1),
                                  "frac": round(n4 * 76 / ms / 1e6 / peak, 3), "objects_per_s": round(n4 / ms * 1e3)}
+    out["config4_aosoa_100M"]["parity"] = verify_aosoa_tiles(ao, n4, fields, dev)
     ao.free()
     # the other tile widths SURVEY 8d names (T = 32, 64): same bytes per object
     for lanes in (32, 64):
         ao = sk.Aosoa(n4, lanes, fields, cuda)
         ms = queued(lambda: sk.to_aosoa(a4, fields, lanes, out=ao, sync=False), steps=5)
         out["config4_aosoa_100M"][f"T{lanes}"] = {"ms": round(ms, 3), "gbs": round(n4 * 76 / ms / 1e6, 1),
-                                                  "frac": round(n4 * 76 / ms / 1e6 / peak, 3)}
+                                                  "frac": round(n4 * 76 / ms / 1e6 / peak, 3),
+                                                  "parity": verify_aosoa_tiles(ao, n4, fields, dev, samples=8)}
         ao.free()
     a4.free()
     busy.free()

@@ -174,24 +174,37 @@ int sk_jagged_scatter(int64_t n, const void* prefix, int prefix_type,
                       const int32_t* field_size, void* const* dst_pools,
                       int64_t total, uintptr_t stream);
 
+/* Validation of a pack's inputs: *bad_dev (device int64, zeroed first) counts
+   the records with a negative length or a non-empty segment
+   [src_off, src_off + len) outside [0, src_members) of the source pool. The
+   reference raises before it mutates anything (np.asarray of each segment,
+   collection.py:546); callers with device-resident inputs run this first. */
+int sk_jagged_validate(int64_t n, const void* lens, int lens_type, const int64_t* src_off,
+                       int64_t src_members, int64_t* bad_dev, uintptr_t stream);
 /* scan + gather in one call with no host round trip: the gather is
-   sized by the pools' `capacity` (members) and reads the true total from
-   *total_dev on the device, so it is complete iff *total_dev <= capacity; the
-   caller reads *total_dev afterwards and, on overflow, grows the pools and
-   gathers again with sk_jagged_scatter. One naturally aligned 4/8-byte member
-   field (16-byte-aligned pool), or 2-4 such fields of an 8/16-byte member
-   record, runs as ONE kernel (prefixes and gather fused; the scratch holds its
-   per-block status words). Other member layouts run the scan and the gather
-   back to back. Scratch: at least sk_jagged_scratch_bytes; with
+   sized by the pools' `capacity` (members) and reads the true total on the
+   device, so it is complete iff total <= capacity. total_dev points at TWO
+   device int64: [0] the total, [1] the count of invalid records (as
+   sk_jagged_validate; src_pool holds src_members member records). The caller
+   reads both afterwards: invalid records -> nothing was gathered for their
+   sub-tiles (the prefix is written regardless), raise; total > capacity ->
+   grow the pools and gather again with sk_jagged_scatter. One naturally
+   aligned 4/8-byte member field (16-byte-aligned pool), or 2-4 such fields of
+   an 8/16-byte member record, runs as ONE kernel (prefixes and gather fused;
+   the scratch holds its per-block status words); the kernel needs no
+   co-residency of its CTAs beyond in-order dispatch (a CTA only waits on
+   lower-indexed blocks' published totals). Other member layouts run
+   validate, scan and gather back to
+   back. Scratch: at least sk_jagged_scratch_bytes; with
    (ceil(capacity / 256) + 1) * 8 more bytes after it (256-aligned) the
    two-kernel path allocates nothing (the scan writes the gather's work split
    there). The scratch is not retained after the call's work completes. */
 int sk_jagged_pack(int64_t n, const void* lens, int lens_type, void* prefix,
                    int prefix_type, const int64_t* src_off, const void* src_pool,
-                   int64_t member_stride, int nfields, const int64_t* field_off,
-                   const int32_t* field_size, void* const* dst_pools, int64_t capacity,
-                   void* scratch, size_t scratch_bytes, int64_t* total_dev,
-                   uintptr_t stream);
+                   int64_t src_members, int64_t member_stride, int nfields,
+                   const int64_t* field_off, const int32_t* field_size,
+                   void* const* dst_pools, int64_t capacity, void* scratch,
+                   size_t scratch_bytes, int64_t* total_dev, uintptr_t stream);
 /* Sharded jagged collections (no reference counterpart -- the
    reference has no sharding): after each shard packed locally and the shard
    totals were exclusive-scanned across ranks, prefix[0..count) += offset in
@@ -266,6 +279,12 @@ int sk_reco_free(void* handle, uintptr_t stream);
    images the benches convert. */
 int sk_fill_random(void* dst, size_t nbytes, uint64_t seed, uint64_t first_word,
                    uintptr_t stream);
+/* Count the bytes where a[i] != b[i] into *mismatches (device memory; zeroed
+   first, on the stream): full-size identity checks of round trips (AoS ->
+   planes -> AoS) without copying the collections to the host. A verification
+   utility, not a reference interface. */
+int sk_compare_bytes(const void* a, const void* b, size_t nbytes, unsigned long long* mismatches,
+                     uintptr_t stream);
 
 /* ---- multi-GPU shards: CUDA IPC for cross-process peer pulls --- */
 /* cudaMalloc'd (IPC-exportable) device memory; pool allocations from sk_malloc

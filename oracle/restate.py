@@ -227,3 +227,17 @@ def reconstruct(energy, noise, sensor_type, noisy, width: int, height: int) -> d
     res["sensor_lens"] = np.array([a.size for a in out["sensors"]], np.int32)
     res["sensors"] = np.concatenate(out["sensors"]) if m else np.empty(0, np.uint64)
     return res
+
+
+# ---- bench inputs: the splitmix64 record images sk_fill_random writes --------------------
+
+def splitmix_image(seed: int, first_word: int, byte_off: int, nbytes: int) -> np.ndarray:
+    """Bytes [byte_off, byte_off + nbytes) of the synthetic image whose 8-byte
+    word w is splitmix64(seed, first_word + w), little-endian (the same
+    counter-based mixer as events.py:37-44, keyed by word index). The bench
+    uses it to check sampled records of collections too large to copy back."""
+    w0, w1 = byte_off // 8, -(-(byte_off + nbytes) // 8)
+    words = mix_stream(seed, first_word + w0, w1 - w0)
+    raw = words.view(np.uint8)
+    s = byte_off - w0 * 8
+    return raw[s : s + nbytes]

@@ -102,8 +102,9 @@ _SIGNATURES = {
     "sk_jagged_scan": [_I64, _P, _I, _P, _I, _P, _SZ, _P, _U],
     "sk_jagged_scatter": [_I64, _P, _I, _P, _P, _I64, _I, C.POINTER(_I64), C.POINTER(C.c_int32), C.POINTER(_P),
                           _I64, _U],
-    "sk_jagged_pack": [_I64, _P, _I, _P, _I, _P, _P, _I64, _I, C.POINTER(_I64), C.POINTER(C.c_int32), C.POINTER(_P),
-                       _I64, _P, _SZ, _P, _U],
+    "sk_jagged_pack": [_I64, _P, _I, _P, _I, _P, _P, _I64, _I64, _I, C.POINTER(_I64), C.POINTER(C.c_int32),
+                       C.POINTER(_P), _I64, _P, _SZ, _P, _U],
+    "sk_jagged_validate": [_I64, _P, _I, _P, _I64, _P, _U],
     "sk_jagged_rebase": [_I64, _P, _I, _I64, _U],
     "sk_jagged_trace": [_P, _SZ],
     "sk_sensor_calibrate": [_I64, _P, _P, _P, _P, _U],
@@ -117,6 +118,7 @@ _SIGNATURES = {
                       C.POINTER(_P), _U],
     "sk_reco_free": [_P, _U],
     "sk_fill_random": [_P, _SZ, C.c_uint64, C.c_uint64, _U],
+    "sk_compare_bytes": [_P, _P, _SZ, _P, _U],
     "sk_malloc_shareable": [_I, _SZ, C.POINTER(_P)],
     "sk_free_shareable": [_I, _P],
     "sk_ipc_handle_size": [C.POINTER(_SZ)],

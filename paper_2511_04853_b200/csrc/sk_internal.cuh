@@ -28,6 +28,7 @@ struct DeviceState {
   bool init = false;
   int sm_count = 0;
   int max_smem_optin = 0;
+  int l2_bytes = 0;
   cudaStream_t stream = nullptr;   // default work stream
   cudaStream_t copy_in = nullptr;  // H2D stream of the transfer pipeline
   cudaStream_t copy_out = nullptr; // D2H stream of the transfer pipeline

@@ -28,6 +28,7 @@
 // j + (src_off[c] - P[c]). The next window's loads are in flight while this
 // window's members are.
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
 #include <utility>
@@ -309,6 +310,7 @@ struct ScatterArgs {
   int64_t member_stride;
   int64_t total;             // members to gather, or the capacity bound when total_dev is set
   const int64_t* total_dev;  // device-resident total (fused pack): gather min(*total_dev, total)
+  const int64_t* bad_dev;    // device-resident count of invalid segments (pack): gather nothing unless 0
   const int64_t* starts;     // starts[w] = record holding member w*W
   const unsigned long long* last_rec;  // 1 + last non-empty record
   int nfields;
@@ -367,6 +369,7 @@ __device__ __forceinline__ void store_member(uint8_t* p, uint64_t v, int isz) {
 // bound, else nothing -- on overflow the (narrow) prefix may have wrapped and
 // the host redoes the pack with grown pools, so no search may run over it.
 __device__ __forceinline__ int64_t eff_total(const ScatterArgs& A) {
+  if (A.bad_dev && *A.bad_dev) return 0;
   if (!A.total_dev) return A.total;
   const int64_t t = *A.total_dev;
   return t <= A.total ? t : 0;
@@ -698,8 +701,9 @@ struct DeferEntry {
   int64_t rec0;  // first record of the sub-tile
   int64_t cnt;   // its records
   int64_t E, A;
-  unsigned long long next;  // next chunk to hand out
-  unsigned long long pad[3];
+  unsigned long long next;   // next chunk to hand out
+  unsigned long long ready;  // = the launch's generation (release) once the fields above are written
+  unsigned long long pad[2];
 };
 
 struct FusedArgs {
@@ -729,6 +733,9 @@ struct FusedArgs {
   int pvec;             // 4-byte prefix, 16-byte aligned: vector prefix stores
   int lens16;           // 4/8-byte lengths, 16-byte aligned: vector loads in the block sums
   int dbg;              // experiments only (SK_FUSED_DBG): 1 = no gather, 2 = no look-back
+  int64_t src_members;  // member records in the source pool: segments must lie inside it
+  int64_t* bad;         // += records whose segment does not (their sub-tiles are not gathered)
+  unsigned long long gen;  // this launch's queue generation (queue entries are not zeroed between calls)
 };
 
 struct __align__(16) TileBuf {
@@ -741,6 +748,7 @@ struct FusedSmem {
   TileBuf tb;
   int sRec[F_NW][W];        // per warp: rank -> record of the current window
   int64_t warp_tot[F_NW];
+  int warp_bad[F_NW];       // the warp holds a record whose segment lies outside the source pool
   int64_t item, E, A;
   int next;                 // next window of the current sub-tile
 };
@@ -763,25 +771,41 @@ __device__ __forceinline__ void sub_load(const FusedArgs& F, int64_t r0, int cnt
 
 // all threads: the loaded sub-tile -> tables; returns the sub-tile total.
 // incl[i] = tile-local inclusive prefix of this thread's records.
-__device__ __forceinline__ int64_t sub_scan(const FRegs<F_RPT>& g, FusedSmem& S, int64_t (&ex)[F_RPT]) {
+// `bad` is set when a record of the sub-tile has a negative length or a segment outside the source pool
+// (counted into *F.bad when `count` is set); such a sub-tile is not gathered.
+__device__ __forceinline__ int64_t sub_scan(const FusedArgs& F, const FRegs<F_RPT>& g, FusedSmem& S,
+                                            int64_t (&ex)[F_RPT], bool& bad, bool count) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   int64_t acc = 0;
+  unsigned nbad = 0;
 #pragma unroll
-  for (int i = 0; i < F_RPT; ++i) acc += g.len[i];
+  for (int i = 0; i < F_RPT; ++i) {
+    acc += g.len[i];
+    // empty segments are valid whatever their offset (an empty list reads nothing)
+    nbad += g.len[i] < 0 || (g.len[i] > 0 && (g.off[i] < 0 || g.off[i] > F.src_members - g.len[i]));
+  }
   int64_t x = acc;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
     const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
     if (lane >= o) x += y;
   }
-  if (lane == 31) S.warp_tot[warp] = x;
+  const unsigned wbad = __reduce_add_sync(0xffffffffu, nbad);
+  if (lane == 31) {
+    S.warp_tot[warp] = x;
+    S.warp_bad[warp] = wbad != 0;
+    if (count && wbad) atomicAdd(reinterpret_cast<unsigned long long*>(F.bad), static_cast<unsigned long long>(wbad));
+  }
   __syncthreads();
   int64_t woff = 0, agg = 0;
+  int anybad = 0;
 #pragma unroll
   for (int w = 0; w < F_NW; ++w) {
     if (w < warp) woff += S.warp_tot[w];
     agg += S.warp_tot[w];
+    anybad |= S.warp_bad[w];
   }
+  bad = anybad != 0;
   int64_t run = woff + x - acc;
   const int e0 = tid * F_RPT;
 #pragma unroll
@@ -1081,7 +1105,8 @@ __global__ void __launch_bounds__(F_NT, 3) pack_fused_kernel(const __grid_consta
       const int64_t r0 = rec0 + static_cast<int64_t>(sb) * F_R;
       const int cnt = static_cast<int>(min(static_cast<int64_t>(F_R), rec1 - r0));
       int64_t ex[F_RPT];
-      const int64_t A = sub_scan(g, S, ex);
+      bool bad;
+      const int64_t A = sub_scan(F, g, S, ex, bad, true);
       const int64_t E = run;
       run += A;
       sub_prefix(F, r0, cnt, E, ex);
@@ -1090,12 +1115,19 @@ __global__ void __launch_bounds__(F_NT, 3) pack_fused_kernel(const __grid_consta
         sub_load(F, r1, static_cast<int>(min(static_cast<int64_t>(F_R), rec1 - r1)), g);
       }
       // past the capacity: not gathered (the caller sees *total > capacity and redoes the pack)
-      const bool gather = A > 0 && E + A <= F.capacity && !(F.dbg & 1);
+      const bool gather = A > 0 && E + A <= F.capacity && !bad && !(F.dbg & 1);
       const bool queue = gather && A > DEFER_PER_REC * F_R;
       if (tid == 0) {
         if (queue) {
           const unsigned slot = atomicAdd(&F.hdr->ndef, 1u);
-          F.defer[slot] = DeferEntry{r0, cnt, E, A, 0ull, {0ull, 0ull, 0ull}};
+          DeferEntry& d = F.defer[slot];
+          d.rec0 = r0;
+          d.cnt = cnt;
+          d.E = E;
+          d.A = A;
+          d.next = 0;
+          __threadfence();
+          st_release(&d.ready, F.gen);
         }
         S.next = 0;
       }
@@ -1113,25 +1145,22 @@ __global__ void __launch_bounds__(F_NT, 3) pack_fused_kernel(const __grid_consta
       }
       __syncthreads();  // the tables are rewritten by the next sub-tile
     }
-    if (tid == 0) {
-      __threadfence();  // queue entries are visible before the block's sub-tiles count as finished
-      atomicAdd(&F.hdr->finished, static_cast<unsigned>(nsub));
-    }
   }
 
   stamp(2);
   __syncthreads();  // every thread has read S.item (the loop's last ticket) before it is reused
-  // queued sub-tiles: once every sub-tile is accounted for (their owners are running), share them out
-  if (tid == 0) {
-    while (*reinterpret_cast<volatile unsigned int*>(&F.hdr->finished) < static_cast<unsigned int>(F.tiles))
-      __nanosleep(256);
-    __threadfence();
-    S.item = *reinterpret_cast<volatile unsigned int*>(&F.hdr->ndef);
-  }
+  // queued sub-tiles: help with the entries queued so far. No CTA waits for another to queue or finish
+  // anything (an entry queued later is drained by its owner, which runs this loop after queuing it), so
+  // the grid needs no co-residency; an entry whose slot is taken but not yet written is being written
+  // by a running CTA.
+  if (tid == 0) S.item = *reinterpret_cast<volatile unsigned int*>(&F.hdr->ndef);
   __syncthreads();
   const int64_t ndef = S.item;
   int64_t have = -1;
   for (int64_t d = 0; d < ndef; ++d) {
+    if (tid == 0)
+      while (ld_acquire(&F.defer[d].ready) != F.gen) __nanosleep(64);
+    __syncthreads();
     const DeferEntry ent = F.defer[d];
     const int64_t k0 = first_window(ent.E), nwin = end_window(ent.E, ent.A) - k0;
     const int64_t nchunks = (nwin + DEFER_CHUNK - 1) / DEFER_CHUNK;
@@ -1144,7 +1173,8 @@ __global__ void __launch_bounds__(F_NT, 3) pack_fused_kernel(const __grid_consta
       if (have != d) {
         sub_load(F, ent.rec0, static_cast<int>(ent.cnt), g);
         int64_t ex[F_RPT];
-        sub_scan(g, S, ex);
+        bool bad;
+        sub_scan(F, g, S, ex, bad, false);
         __syncthreads();
         have = d;
       }
@@ -1161,9 +1191,10 @@ __global__ void __launch_bounds__(F_NT, 3) pack_fused_kernel(const __grid_consta
 // zeroes the fused pack's scratch header + status words; lets the pack's CTAs
 // launch (and sum their lengths) meanwhile, but only once everything before it
 // in the stream has completed
-__global__ void __launch_bounds__(256) scratch_zero_kernel(uint64_t* p, int64_t words) {
+__global__ void __launch_bounds__(256) scratch_zero_kernel(uint64_t* p, int64_t words, int64_t* extra) {
   pdl_wait_prior();
   pdl_allow_next();
+  if (extra && blockIdx.x == 0 && threadIdx.x == 0) *extra = 0;
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < words;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x)
     p[i] = 0;
@@ -1172,6 +1203,26 @@ __global__ void __launch_bounds__(256) scratch_zero_kernel(uint64_t* p, int64_t 
 template <int MS>
 constexpr size_t fused_smem() {
   return static_cast<size_t>(F_NW) * F_NS * W * MS + sizeof(FusedSmem);
+}
+
+// segments that read outside the source pool: negative lengths, or a non-empty
+// segment [off, off + len) not inside [0, members) -> *bad counts them
+__global__ void __launch_bounds__(256) validate_kernel(int64_t n, const void* __restrict__ lens, int lens_type,
+                                                       const int64_t* __restrict__ src_off, int64_t members,
+                                                       unsigned long long* bad) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  unsigned long long cnt = 0;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const int64_t len = load_int(lens, lens_type, i);
+    if (len < 0) {
+      ++cnt;
+    } else if (len > 0) {
+      const int64_t off = src_off[i];
+      cnt += off < 0 || off > members - len;
+    }
+  }
+  for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(bad, cnt);
 }
 
 // shard rebase: P[i] += offset in the index dtype's modular
@@ -1369,7 +1420,11 @@ static int launch_fused_ms(jag::FusedArgs F, uint8_t* scratch, cudaStream_t s, i
   }
   // one block of records per CTA (a multiple of 4 records, at least one sub-tile, at most MAX_SUB)
   const int64_t ctas = static_cast<int64_t>(ds->sm_count) * o;
-  int64_t br = (F.n + ctas - 1) / ctas;
+  static const int64_t bpc = [] {  // record blocks per CTA (later ones handed out by ticket)
+    const char* e = getenv("SK_FUSED_BPC");
+    return e ? std::max<int64_t>(1, atoll(e)) : int64_t(1);
+  }();
+  int64_t br = (F.n + ctas * bpc - 1) / (ctas * bpc);
   br = std::max<int64_t>(jag::F_R, std::min<int64_t>((br + 3) & ~int64_t(3), int64_t(jag::MAX_SUB) * jag::F_R));
   F.block_recs = br;
   F.nblocks = (F.n + br - 1) / br;
@@ -1381,7 +1436,7 @@ static int launch_fused_ms(jag::FusedArgs F, uint8_t* scratch, cudaStream_t s, i
   F.defer = reinterpret_cast<jag::DeferEntry*>(scratch + 64 + status_bytes);
   const int64_t zwords = static_cast<int64_t>((64 + status_bytes) / 8);
   SK_TRY(launch_pdl(jag::scratch_zero_kernel, dim3(static_cast<unsigned>(std::min<int64_t>((zwords + 255) / 256, 64))),
-                    dim3(256), s, reinterpret_cast<uint64_t*>(scratch), zwords));
+                    dim3(256), s, reinterpret_cast<uint64_t*>(scratch), zwords, F.bad));
   const int64_t grid = std::min<int64_t>(F.nblocks, ctas);
   SK_TRY(launch_pdl_smem(jag::pack_fused_kernel<MS, RS>, dim3(static_cast<unsigned>(grid)), dim3(jag::F_NT), smem, s, F));
   return SK_OK;
@@ -1455,11 +1510,30 @@ int sk_jagged_scatter(int64_t n, const void* prefix, int prefix_type, const int6
   return rc;
 }
 
+int sk_jagged_validate(int64_t n, const void* lens, int lens_type, const int64_t* src_off, int64_t src_members,
+                       int64_t* bad_dev, uintptr_t stream) {
+  if (n < 0 || src_members < 0) return set_error(SK_ERR_INVALID, "negative sizes");
+  if (!bad_dev) return set_error(SK_ERR_INVALID, "bad_dev is required");
+  if (!int_type(lens_type) || lens_type == SK_BOOL) return set_error(SK_ERR_INVALID, "lengths need an integer type");
+  int dev = 0;
+  SK_TRY(cudaGetDevice(&dev));
+  cudaStream_t s = resolve_stream(dev, stream);
+  SK_TRY(cudaMemsetAsync(bad_dev, 0, 8, s));
+  if (n == 0) return SK_OK;
+  DeviceState* ds = nullptr;
+  if (int rc = device_state(dev, &ds)) return rc;
+  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, ds->sm_count * 8ll));
+  jag::validate_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(n, lens, lens_type, src_off, src_members,
+                                                                     reinterpret_cast<unsigned long long*>(bad_dev));
+  SK_TRY(cudaGetLastError());
+  return SK_OK;
+}
+
 int sk_jagged_pack(int64_t n, const void* lens, int lens_type, void* prefix, int prefix_type, const int64_t* src_off,
-                   const void* src_pool, int64_t member_stride, int nfields, const int64_t* field_off,
-                   const int32_t* field_size, void* const* dst_pools, int64_t capacity, void* scratch,
-                   size_t scratch_bytes, int64_t* total_dev, uintptr_t stream) {
-  if (n < 0 || capacity < 0) return set_error(SK_ERR_INVALID, "negative sizes");
+                   const void* src_pool, int64_t src_members, int64_t member_stride, int nfields,
+                   const int64_t* field_off, const int32_t* field_size, void* const* dst_pools, int64_t capacity,
+                   void* scratch, size_t scratch_bytes, int64_t* total_dev, uintptr_t stream) {
+  if (n < 0 || capacity < 0 || src_members < 0) return set_error(SK_ERR_INVALID, "negative sizes");
   if (!total_dev) return set_error(SK_ERR_INVALID, "total_dev is required");
   if (!int_type(lens_type) || !int_type(prefix_type) || lens_type == SK_BOOL || prefix_type == SK_BOOL)
     return set_error(SK_ERR_INVALID, "jagged lengths and prefix need integer types");
@@ -1475,7 +1549,7 @@ int sk_jagged_pack(int64_t n, const void* lens, int lens_type, void* prefix, int
   cudaStream_t s = resolve_stream(dev, stream);
   if (n == 0) {
     SK_TRY(cudaMemsetAsync(prefix, 0, dtype_size(prefix_type), s));
-    SK_TRY(cudaMemsetAsync(total_dev, 0, 8, s));
+    SK_TRY(cudaMemsetAsync(total_dev, 0, 16, s));
     return SK_OK;
   }
   // single pass: one aligned 4/8-byte member field into a 16-byte-aligned pool, or (RS) 2-4 naturally
@@ -1515,6 +1589,10 @@ int sk_jagged_pack(int64_t n, const void* lens, int lens_type, void* prefix, int
       return e ? atoi(e) : 0;
     }();
     F.dbg = dbg;
+    F.src_members = src_members;
+    F.bad = total_dev + 1;
+    static std::atomic<unsigned long long> generation{0};
+    F.gen = ++generation;
     uint8_t* sc = static_cast<uint8_t*>(scratch);
     if (split)
       return member_stride == 16 ? launch_fused_ms<16, true>(F, sc, s, dev, ds)
@@ -1538,13 +1616,15 @@ int sk_jagged_pack(int64_t n, const void* lens, int lens_type, void* prefix, int
   if (own_starts) SK_TRY(cudaMallocAsync(&starts, starts_need, s));
   unsigned long long* last_rec = reinterpret_cast<unsigned long long*>(static_cast<uint8_t*>(scratch) + 8);
   jag::ScanOut O{prefix, prefix_type, total_dev, p64, ntasks ? starts : nullptr, ntasks, last_rec};
-  int rc = launch_scan(n, lens, lens_type, scratch, need, O, s);
+  int rc = sk_jagged_validate(n, lens, lens_type, src_off, src_members, total_dev + 1, stream);
+  if (rc == SK_OK) rc = launch_scan(n, lens, lens_type, scratch, need, O, s);
   // gather bounded by the pools' capacity; the kernel reads the true total on the device
   if (rc == SK_OK && ntasks) {
     A.prefix = p64 ? static_cast<const void*>(p64) : prefix;
     A.prefix_type = p64 ? SK_I64 : prefix_type;
     A.starts = starts;
     A.last_rec = last_rec;
+    A.bad_dev = total_dev + 1;
     rc = launch_gather(A, ntasks, s, dev);
   }
   if (own_starts) cudaFreeAsync(starts, s);

@@ -48,6 +48,7 @@ int device_state(int device, DeviceState** out) {
     SK_TRY(cudaSetDevice(device));
     SK_TRY(cudaDeviceGetAttribute(&d.sm_count, cudaDevAttrMultiProcessorCount, device));
     SK_TRY(cudaDeviceGetAttribute(&d.max_smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+    SK_TRY(cudaDeviceGetAttribute(&d.l2_bytes, cudaDevAttrL2CacheSize, device));
     SK_TRY(cudaStreamCreateWithFlags(&d.stream, cudaStreamNonBlocking));
     SK_TRY(cudaStreamCreateWithFlags(&d.copy_in, cudaStreamNonBlocking));
     SK_TRY(cudaStreamCreateWithFlags(&d.copy_out, cudaStreamNonBlocking));
@@ -379,7 +380,53 @@ __global__ void fill_random_kernel(uint8_t* dst, size_t nbytes, uint64_t seed, u
     dst[nw * 8 + threadIdx.x] = static_cast<uint8_t>(splitmix64(seed, first + nw) >> (8 * threadIdx.x));
 }
 
+// mismatching bytes of a vs b (verification of full-size round trips on the
+// device: a 32 GB identity check must not cross PCIe)
+__global__ void compare_kernel(const uint8_t* a, const uint8_t* b, size_t n, unsigned long long* count) {
+  const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+  const size_t tid = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  unsigned long long bad = 0;
+  const bool vec = ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b)) & 15) == 0;
+  size_t done = 0;
+  if (vec) {
+    const size_t nv = n / 16;
+    const uint4* va = reinterpret_cast<const uint4*>(a);
+    const uint4* vb = reinterpret_cast<const uint4*>(b);
+    for (size_t i = tid; i < nv; i += stride) {
+      const uint4 x = va[i], y = vb[i];
+      const uint32_t d[4] = {x.x ^ y.x, x.y ^ y.y, x.z ^ y.z, x.w ^ y.w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k)  // count bytes, not words
+        bad += __popc(((d[k] | (d[k] >> 1) | (d[k] >> 2) | (d[k] >> 3) | (d[k] >> 4) | (d[k] >> 5) |
+                        (d[k] >> 6) | (d[k] >> 7)) & 0x01010101u));
+    }
+    done = nv * 16;
+  }
+  for (size_t i = done + tid; i < n; i += stride) bad += a[i] != b[i];
+  for (int o = 16; o; o >>= 1) bad += __shfl_xor_sync(0xffffffffu, bad, o);
+  if ((threadIdx.x & 31) == 0 && bad) atomicAdd(count, bad);
+}
+
 }  // namespace sk
+
+extern "C" int sk_compare_bytes(const void* a, const void* b, size_t nbytes, unsigned long long* mismatches,
+                                uintptr_t stream) {
+  if (!mismatches) return set_error(SK_ERR_INVALID, "mismatch counter must be a device pointer");
+  cudaStream_t s;
+  int rc = stream_of(stream, &s);
+  if (rc) return rc;
+  SK_TRY(cudaMemsetAsync(mismatches, 0, sizeof(unsigned long long), s));
+  if (nbytes == 0) return SK_OK;
+  int dev = 0;
+  SK_TRY(cudaGetDevice(&dev));
+  DeviceState* d = nullptr;
+  rc = device_state(dev, &d);
+  if (rc) return rc;
+  sk::compare_kernel<<<d->sm_count * 8, 256, 0, s>>>(static_cast<const uint8_t*>(a), static_cast<const uint8_t*>(b),
+                                                     nbytes, mismatches);
+  SK_TRY(cudaGetLastError());
+  return SK_OK;
+}
 
 extern "C" int sk_fill_random(void* dst, size_t nbytes, uint64_t seed, uint64_t first_word, uintptr_t stream) {
   if (nbytes == 0) return SK_OK;

@@ -49,8 +49,8 @@ class _Workspace:
     def __init__(self, dev: int) -> None:
         self.dev = dev
         self.scratch: DeviceArray | None = None
-        self.total = DeviceArray(1, np.int64, memctx.ContextInfo.cuda(dev))
-        self.host_total = memctx.allocate(memctx.ContextInfo.pinned(), 8)
+        self.total = DeviceArray(2, np.int64, memctx.ContextInfo.cuda(dev))  # [total, invalid records]
+        self.host_total = memctx.allocate(memctx.ContextInfo.pinned(), 16)
 
     def scratch_for(self, nbytes: int) -> DeviceArray:
         if self.scratch is None or self.scratch.n < nbytes:
@@ -85,6 +85,25 @@ def scan(lens: DeviceArray, prefix_ptr: int, prefix_code: str, dev: int, keep: l
     return int(ws.host_total._data.view(np.int64)[0])
 
 
+def _check_host_segments(lens, offsets, members: int) -> None:
+    """Validate-before-mutate for host inputs (the reference's np.asarray of
+    each segment raises before anything changes, collection.py:546)."""
+    lens = np.asarray(lens)
+    offsets = np.asarray(offsets, dtype=np.int64)
+    if lens.size and int(lens.min()) < 0:
+        raise BoundsError(f"negative segment length at record {int(np.argmin(lens))}")
+    ne = lens > 0
+    bad = ne & ((offsets < 0) | (offsets > members - lens.astype(np.int64)))
+    if bad.any():
+        i = int(np.flatnonzero(bad)[0])
+        raise BoundsError(f"segment of record {i} ([{offsets[i]}, {offsets[i] + int(lens[i])})) lies outside the "
+                          f"source pool of {members} members")
+
+
+def _invalid_segments(bad: int) -> BoundsError:
+    return BoundsError(f"{bad} segment(s) have a negative length or lie outside the source pool")
+
+
 def pack(coll, path: str, lens, src_offsets, src_pool, member_stride: int | None = None,
          member_offsets: Mapping[str, int] | None = None) -> int:
     """Fill jagged vector `path` of `coll` from a member pool; returns the total.
@@ -116,6 +135,13 @@ def pack(coll, path: str, lens, src_offsets, src_pool, member_stride: int | None
         member_stride = leaves[0].value_type.size_bytes
     if set(member_offsets) != {lf.dotted for lf in leaves}:
         raise KindError(f"member_offsets must name exactly the leaves {[lf.dotted for lf in leaves]}")
+    pool_bytes = src_pool.nbytes if isinstance(src_pool, DeviceArray) else np.asarray(src_pool).nbytes
+    members = pool_bytes // int(member_stride) if member_stride else 0
+    if not isinstance(lens, DeviceArray) and not isinstance(src_offsets, DeviceArray):
+        _check_host_segments(lens, src_offsets, members)
+        checked = True
+    else:
+        checked = False
     pool_d = _as_device(src_pool, None, dev, keep)
 
     pleaf = plan.leaf(path + ".prefix_sum")
@@ -141,11 +167,23 @@ def pack(coll, path: str, lens, src_offsets, src_pool, member_stride: int | None
         scratch = ws.scratch_for(-(-need.value // 256) * 256 + starts_bytes)
         ptrs = (C.c_void_p * nf)(*[lay.plane_address(lf, 0) for lf in leaves])
         nat.call("sk_jagged_pack", n, lens_d.ptr, nat.TYPE_CODES[_NP_CODE[lens_d.dtype]], prefix_ptr,
-                 nat.TYPE_CODES[pcode], off_d.ptr, pool_d.ptr, int(member_stride), nf, offs, sizes, ptrs, cap,
-                 scratch.ptr, scratch.n, ws.total.ptr, nat.stream(dev))
-        nat.memcpy(ws.host_total.ptr, ws.total.ptr, 8, dev)
+                 nat.TYPE_CODES[pcode], off_d.ptr, pool_d.ptr, members, int(member_stride), nf, offs, sizes, ptrs,
+                 cap, scratch.ptr, scratch.n, ws.total.ptr, nat.stream(dev))
+        nat.memcpy(ws.host_total.ptr, ws.total.ptr, 16, dev)
         nat.sync(dev)
-        total = int(ws.host_total._data.view(np.int64)[0])
+        total, bad = (int(v) for v in ws.host_total._data.view(np.int64)[:2])
+        if bad:
+            # device inputs were checked by the kernel, which already wrote the prefix plane: leave the
+            # vector empty and consistent (prefix all zero), then raise
+            nat.call("sk_memset_async", prefix_ptr, 0, (n + 1) * psz, nat.stream(dev))
+            with lay.engine_ops():
+                lay._set_sizes_for_engine({path: 0})
+            coll._bump()
+            nat.sync(dev)
+            for t in keep:
+                t.free()
+            raise _invalid_segments(bad)
+        checked = True
         if total <= cap:
             coll._bump()
             with lay.engine_ops():
@@ -155,6 +193,17 @@ def pack(coll, path: str, lens, src_offsets, src_pool, member_stride: int | None
             return total
         # overflow: the pools must grow first -- redo as scan, resize, gather
 
+    if not checked:  # device inputs on the scan + gather path: validate before anything is written
+        ws = _workspace(dev)
+        nat.call("sk_jagged_validate", n, lens_d.ptr, nat.TYPE_CODES[_NP_CODE[lens_d.dtype]], off_d.ptr, members,
+                 ws.total.ptr + 8, nat.stream(dev))
+        nat.memcpy(ws.host_total.ptr, ws.total.ptr + 8, 8, dev)
+        nat.sync(dev)
+        bad = int(ws.host_total._data.view(np.int64)[0])
+        if bad:
+            for t in keep:
+                t.free()
+            raise _invalid_segments(bad)
     total = scan(lens_d, prefix_ptr, pcode, dev, keep)
 
     coll._bump()

@@ -189,6 +189,37 @@ def test_hundred_million_round_trip_on_device():
         c.free()
 
 
+def test_past_four_gib_offsets_vs_oracle():
+    """160M Obj8 records = 5.12 GB of AoS: tiles whose AoS byte offsets lie
+    past 2^32 (and the last record) are checked against the oracle's
+    restatement of the splitmix input image, both directions (K1 and K2)."""
+    n, seed = 160_000_000, 31
+    src = sk.Collection(wl.OBJ8_SCHEMA, ly.AOS, CUDA)
+    with mc.execution_scope(mc.CUDA):
+        src.reserve(n)
+    with src.layout.engine_ops():
+        src.layout._set_sizes_for_engine({sc.MAIN_TAG: n})
+    wl.fill_random_device(src.layout._struct_buf.ptr, n * 32, seed=seed, device=0)
+    planes = sk.Collection(wl.OBJ8_SCHEMA, ly.PER_FIELD, CUDA)
+    tr.copy_collection(planes, src)
+    t = 8192
+    first_past = (1 << 32) // 32
+    starts = [first_past - t // 2, first_past, 150_000_000, n - t]
+    for r0 in starts:
+        want = R.splitmix_image(seed, 0, r0 * 32, t * 32).view(wl.OBJ8_AOS_DTYPE)
+        for i in range(8):
+            got = device_to_numpy(planes.layout.plane_address(planes.plan.leaf(f"f{i}")) + r0 * 4, t * 4)
+            assert got.tobytes() == np.ascontiguousarray(want[f"f{i}"]).tobytes(), (r0, i)
+    back = sk.Collection(wl.OBJ8_SCHEMA, ly.AOS, CUDA)
+    tr.copy_collection(back, planes)
+    for r0 in starts:
+        got = device_to_numpy(back.layout._struct_buf.ptr + r0 * 32, t * 32)
+        assert got.tobytes() == R.splitmix_image(seed, 0, r0 * 32, t * 32).tobytes(), r0
+    assert device_bytes_equal(src.layout._struct_buf.ptr, back.layout._struct_buf.ptr, n * 32)
+    for c in (src, planes, back):
+        c.free()
+
+
 TRACK_FIELDS = [("pz", "f32"), ("px", "f32"), ("x", "f32"), ("charge", "i32")]
 
 

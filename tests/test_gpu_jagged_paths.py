@@ -12,9 +12,13 @@ import ctypes as C
 import numpy as np
 import pytest
 
+import paper_2511_04853_b200 as sk
 from paper_2511_04853_b200 import _native as nat
+from paper_2511_04853_b200 import jagged, layouts as ly
 from paper_2511_04853_b200 import memctx as mc
+from paper_2511_04853_b200 import workloads as wl
 from paper_2511_04853_b200.devarray import DeviceArray
+from paper_2511_04853_b200.errors import BoundsError
 
 pytestmark = pytest.mark.gpu
 
@@ -56,7 +60,7 @@ def _pack(lens, offs, pool_bytes, stride, fields, ptype, cap_extra=0, dst_shift=
     nat.call("sk_jagged_scratch_bytes", n, C.byref(need))
     sbytes = -(-need.value // 256) * 256 + ((cap + 255) // 256 + 1) * 8
     scratch = DeviceArray(sbytes, np.uint8, CUDA)
-    total = DeviceArray(1, np.int64, CUDA)
+    total = DeviceArray(2, np.int64, CUDA)
     nf = len(fields)
     foff = (C.c_int64 * nf)(*[o for o, _ in fields])
     fsz = (C.c_int32 * nf)(*[sz for _, sz in fields])
@@ -64,10 +68,12 @@ def _pack(lens, offs, pool_bytes, stride, fields, ptype, cap_extra=0, dst_shift=
     lcode = {np.dtype(np.int32): "i32", np.dtype(np.uint8): "u8", np.dtype(np.uint16): "u16",
              np.dtype(np.int64): "i64", np.dtype(np.uint32): "u32"}[lens.dtype]
     nat.call("sk_jagged_pack", n, d_lens.ptr + lens_shift * lens.dtype.itemsize, TC[lcode],
-             prefix.ptr + prefix_shift * pnp.itemsize, TC[ptype], d_offs.ptr, d_pool.ptr, stride, nf,
+             prefix.ptr + prefix_shift * pnp.itemsize, TC[ptype], d_offs.ptr, d_pool.ptr, pool_bytes.size // stride,
+             stride, nf,
              foff, fsz, dst, cap, scratch.ptr, scratch.n, total.ptr, nat.stream(0))
     nat.sync(0)
-    t = int(total.numpy()[0])
+    t, bad = (int(v) for v in total.numpy())
+    assert bad == 0
     res = [o.numpy()[dst_shift:dst_shift + t * sz].tobytes() for o, (_, sz) in zip(outs, fields)]
     p = prefix.numpy()[prefix_shift:]
     for a in (d_lens, d_offs, d_pool, prefix, scratch, total, *outs):
@@ -293,3 +299,127 @@ def test_fused_pack_member_field_table(stride, fields):
     p, got, t = _pack(lens, offs, pool, stride, fields, "i32", cap_extra=9)
     pw, want, tw = _expect(lens, offs, pool, stride, fields, "i32")
     assert t == tw and p.tobytes() == pw.tobytes() and got == want
+
+
+# ---- invalid segments: reported, never read (lens >= 0, offsets + lens inside the pool) ----
+
+def _pack_raw(lens, offs, pool_members, fields, stride=8, fused=True):
+    """sk_jagged_pack on device arrays; returns (total, invalid count)"""
+    n = lens.size
+    d_lens, d_offs = DeviceArray.from_numpy(lens, CUDA), DeviceArray.from_numpy(offs, CUDA)
+    d_pool = DeviceArray(max(pool_members, 1) * stride, np.uint8, CUDA)
+    prefix = DeviceArray(n + 1, np.int64 if fused else np.uint16, CUDA)
+    cap = 1 << 16
+    outs = [DeviceArray(cap * sz, np.uint8, CUDA) for _, sz in fields]
+    need = C.c_size_t(0)
+    nat.call("sk_jagged_scratch_bytes", n, C.byref(need))
+    scratch = DeviceArray(-(-need.value // 256) * 256 + ((cap + 255) // 256 + 1) * 8, np.uint8, CUDA)
+    total = DeviceArray(2, np.int64, CUDA)
+    nf = len(fields)
+    foff = (C.c_int64 * nf)(*[o for o, _ in fields])
+    fsz = (C.c_int32 * nf)(*[sz for _, sz in fields])
+    dst = (C.c_void_p * nf)(*[o.ptr for o in outs])
+    nat.call("sk_jagged_pack", n, d_lens.ptr, TC["i32"], prefix.ptr, TC["i64" if fused else "u16"], d_offs.ptr,
+             d_pool.ptr, pool_members, stride, nf, foff, fsz, dst, cap, scratch.ptr, scratch.n, total.ptr,
+             nat.stream(0))
+    t, bad = (int(v) for v in total.numpy())
+    for a in (d_lens, d_offs, d_pool, prefix, scratch, total, *outs):
+        a.free()
+    return t, bad
+
+
+@pytest.mark.parametrize("fused", [True, False])
+def test_pack_counts_invalid_segments(fused):
+    """fused kernel (one 8-byte field) and validate + scan + gather (a 2-byte field) both count records
+    whose segment leaves the source pool, and gather nothing for them"""
+    n = 50_000
+    rng = np.random.default_rng(3)
+    lens = rng.integers(0, 5, n).astype(np.int32)
+    offs = np.concatenate([[0], np.cumsum(lens.astype(np.int64))[:-1]])
+    members = int(lens.sum())
+    fields = [(0, 8)] if fused else [(2, 2)]
+    assert _pack_raw(lens, offs, members, fields, fused=fused) == (members, 0)
+    bad_l, bad_o = lens.copy(), offs.copy()
+    bad_l[10] = -1                       # negative length
+    i = int(np.flatnonzero(lens)[-1])
+    bad_o[i] = members                   # non-empty segment past the end of the pool
+    j = int(np.flatnonzero(lens)[0])
+    bad_o[j] = -3                        # before its start
+    empty = int(np.flatnonzero(lens == 0)[0])
+    bad_o[empty] = 1 << 40               # an empty segment's offset is never read: valid
+    t, bad = _pack_raw(bad_l, bad_o, members, fields, fused=fused)
+    assert bad == 3
+
+
+def test_collection_pack_rejects_invalid_segments_host_and_device():
+    c = sk.Collection(wl.CLUSTER_SCHEMA, ly.PER_FIELD, CUDA)
+    with mc.execution_scope(mc.CUDA):
+        c.resize(1000)
+    lens, offs, pool = wl.cluster_inputs(1000, seed=4)
+    total = jagged.pack(c, "members", lens, offs, pool)
+
+    def state(coll):
+        with mc.execution_scope(mc.CUDA):
+            return coll.prefix_sums("members").tobytes(), coll.jagged_size("members")
+
+    before = state(c)
+    # host inputs: validated before anything is written (strong guarantee)
+    for bl, bo in ((np.where(np.arange(1000) == 7, -2, lens), offs), (lens, np.where(lens > 0, offs + pool.size, offs))):
+        with pytest.raises(BoundsError):
+            jagged.pack(c, "members", bl, bo, pool)
+        assert state(c) == before
+    # device inputs through the fused kernel: detected on the device, the vector is left empty
+    d_pool = DeviceArray.from_numpy(pool, CUDA)
+    bad_offs = offs.copy()
+    bad_offs[int(np.flatnonzero(lens)[0])] = pool.size
+    with pytest.raises(BoundsError):
+        jagged.pack(c, "members", DeviceArray.from_numpy(lens, CUDA), DeviceArray.from_numpy(bad_offs, CUDA), d_pool)
+    p, size = state(c)
+    assert size == 0 and not np.frombuffer(p, np.uint8).any()
+    # device inputs on a fresh collection (scan + gather path): validated first, nothing written
+    c2 = sk.Collection(wl.CLUSTER_SCHEMA, ly.PER_FIELD, CUDA)
+    with mc.execution_scope(mc.CUDA):
+        c2.resize(1000)
+    with pytest.raises(BoundsError):
+        jagged.pack(c2, "members", DeviceArray.from_numpy(lens, CUDA), DeviceArray.from_numpy(bad_offs, CUDA), d_pool)
+    assert c2.jagged_size("members") == 0
+    assert jagged.pack(c, "members", lens, offs, pool) == total
+
+
+def test_concurrent_fused_packs_on_two_streams():
+    """Two full-occupancy packs launched on two streams at once, repeatedly: the fused kernel never waits on a
+    CTA that might not be resident (no end-of-grid spin), so they cannot deadlock, and both stay exact."""
+    import torch
+
+    n = 2_000_000
+    ins = [wl.cluster_inputs(n, seed=s) for s in (21, 22)]
+    wants = [_expect_pool(lens, offs, pool) for lens, offs, pool in ins]
+    streams = [torch.cuda.Stream(device=0) for _ in range(2)]
+    bufs = []
+    for lens, offs, pool in ins:
+        T = int(lens.astype(np.int64).sum())
+        d = [DeviceArray.from_numpy(x, CUDA) for x in (lens, offs, pool)]
+        prefix = DeviceArray(n + 1, np.int32, CUDA)
+        out = DeviceArray(T, np.uint64, CUDA)
+        need = C.c_size_t(0)
+        nat.call("sk_jagged_scratch_bytes", n, C.byref(need))
+        scratch = DeviceArray(need.value, np.uint8, CUDA)
+        total = DeviceArray(2, np.int64, CUDA)
+        bufs.append((d, prefix, out, scratch, total, T, pool.size))
+    torch.cuda.synchronize()
+    for _ in range(20):
+        for (d, prefix, out, scratch, total, T, pm), st in zip(bufs, streams):
+            foff, fsz, dst = (C.c_int64 * 1)(0), (C.c_int32 * 1)(8), (C.c_void_p * 1)(out.ptr)
+            nat.call("sk_jagged_pack", n, d[0].ptr, TC["i32"], prefix.ptr, TC["i32"], d[1].ptr, d[2].ptr, pm, 8, 1,
+                     foff, fsz, dst, T, scratch.ptr, scratch.n, total.ptr, st.cuda_stream)
+    torch.cuda.synchronize()
+    for (d, prefix, out, scratch, total, T, pm), (pw, mw) in zip(bufs, wants):
+        assert prefix.numpy().tobytes() == pw.tobytes() and out.numpy().tobytes() == mw.tobytes()
+        for a in (*d, prefix, out, scratch, total):
+            a.free()
+
+
+def _expect_pool(lens, offs, pool):
+    P = np.concatenate([[0], np.cumsum(lens.astype(np.int64))]).astype(np.int32)
+    idx, _ = _gather_index(lens, offs)
+    return P, pool[idx]

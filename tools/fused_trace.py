@@ -20,12 +20,13 @@ prefix = DeviceArray(n + 1, np.int32, CUDA)
 need = C.c_size_t(0)
 nat.call("sk_jagged_scratch_bytes", n, C.byref(need))
 scratch = DeviceArray(need.value, np.uint8, CUDA)
-total = DeviceArray(1, np.int64, CUDA)
+total = DeviceArray(2, np.int64, CUDA)
 out = DeviceArray(T + 1000, np.uint64, CUDA)
 I32 = nat.TYPE_CODES["i32"]
 foff, fsz, dst = (C.c_int64 * 1)(0), (C.c_int32 * 1)(8), (C.c_void_p * 1)(out.ptr)
 for _ in range(6):
-    nat.call("sk_jagged_pack", n, d_lens.ptr, I32, prefix.ptr, I32, d_off.ptr, d_pool.ptr, 8, 1, foff, fsz, dst,
+    nat.call("sk_jagged_pack", n, d_lens.ptr, I32, prefix.ptr, I32, d_off.ptr, d_pool.ptr, pool.size, 8, 1, foff,
+             fsz, dst,
              T + 1000, scratch.ptr, scratch.n, total.ptr, nat.stream(0))
 buf = np.zeros(1024 * 8, np.uint64)
 nat.call("sk_jagged_trace", buf.ctypes.data, buf.nbytes)

@@ -1,6 +1,6 @@
 """Run one conversion job a few times (for ncu captures): python tools/profile_one.py JOB [reps]
 
-JOB in: obj8_a2p obj8_p2a sensor_fused sensor_a2p track_aosoa particle_a2p jagged
+JOB in: obj8_a2p obj8_p2a sensor_fused sensor_a2p sensor_calnoise track_aosoa particle_a2p jagged
 """
 
 import os
@@ -37,11 +37,19 @@ def job(name):
             (lambda: tr.copy_collection(a, p, {"async": True}))
     if name.startswith("sensor"):
         cells = 64 * 436 * 436
+        # real events (as bench.py config 2): random record bits would send the case-study
+        # arithmetic through its NaN/denormal paths
+        gen = sk.Collection(sensor.SENSOR_SCHEMA, ly.PER_FIELD, CUDA)
+        sensor.generate_events(gen, 436, 436, range(64), 0.002)
         a, p = coll(sensor.SENSOR_SCHEMA, ly.AOS, cells), coll(sensor.SENSOR_SCHEMA, ly.PER_FIELD, cells)
-        wl.fill_random_device(a.layout._struct_buf.ptr, cells * 30 // 8 * 8, 2, 0)
+        tr.copy_collection(a, gen)
+        gen.free()
         noise = DeviceArray(cells, np.float32, CUDA)
         if name == "sensor_fused":
             return lambda: sensor.transfer_calibrate(p, a, noise, sync=False)
+        if name == "sensor_calnoise":  # the standalone K5 kernels the drop-in behaviors launch
+            tr.copy_collection(p, a)
+            return lambda: (sensor.calibrate_collection(p, sync=False), sensor.noise_for_collection(p, noise, sync=False))
         return lambda: tr.copy_collection(p, a, {"async": True})
     if name == "particle_a2p":
         m = 50_000_000

@@ -28,7 +28,7 @@ nat.call("sk_jagged_scratch_bytes", n, C.byref(need))
 cap = T + 1000
 sbytes = -(-need.value // 256) * 256 + ((cap + 255) // 256 + 1) * 8
 scratch = DeviceArray(sbytes, np.uint8, CUDA)
-total = DeviceArray(1, np.int64, CUDA)
+total = DeviceArray(2, np.int64, CUDA)
 out = DeviceArray(cap, np.uint64, CUDA)
 out2 = DeviceArray(cap, np.uint32, CUDA)
 s = nat.stream(0)
@@ -49,7 +49,8 @@ def scatter():
 
 
 def pack():
-    nat.call("sk_jagged_pack", n, d_lens.ptr, I32, prefix.ptr, I32, d_off.ptr, d_pool.ptr, 8, NF, foff, fsz, dst,
+    nat.call("sk_jagged_pack", n, d_lens.ptr, I32, prefix.ptr, I32, d_off.ptr, d_pool.ptr, d_pool.nbytes // 8, 8, NF,
+             foff, fsz, dst,
              cap, scratch.ptr, scratch.n, total.ptr, s)
 
 
