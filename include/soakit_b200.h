@@ -121,6 +121,19 @@ int sk_memcpy_async(void* dst, const void* src, size_t nbytes, uintptr_t stream)
 /* Overlap-safe copy inside one allocation: the memmove contract of
    memcopy_with_context (memctx.py:314-316, 356-357; test_acceptance.py:558-583). */
 int sk_memmove_async(void* dst, const void* src, size_t nbytes, uintptr_t stream);
+/* Batched row moves of one layout splice (LayoutInstance insert / erase /
+   resize, layouts.py:298-367): every stream of a size tag shifts its tail and
+   zero-fills new rows in two launches, instead of one copy per plane. Each
+   op moves `bytes` from src to dst (memmove semantics: an op may overlap
+   itself); src == NULL zero-fills dst. Zero fills apply after every move has
+   read its source; distinct ops' destinations must not overlap. Device
+   memory only (host buffers are spliced on the host). */
+typedef struct sk_move {
+  void* dst;
+  const void* src;
+  uint64_t bytes;
+} sk_move;
+int sk_move_batch_async(const sk_move* ops, int count, uintptr_t stream);
 /* Enable NVLink peer access from `device` to `peer` (idempotent). */
 int sk_peer_enable(int device, int peer);
 

@@ -119,6 +119,7 @@ _SIGNATURES = {
     "sk_reco_free": [_P, _U],
     "sk_fill_random": [_P, _SZ, C.c_uint64, C.c_uint64, _U],
     "sk_compare_bytes": [_P, _P, _SZ, _P, _U],
+    "sk_move_batch_async": [_P, _I, _U],
     "sk_malloc_shareable": [_I, _SZ, C.POINTER(_P)],
     "sk_free_shareable": [_I, _P],
     "sk_ipc_handle_size": [C.POINTER(_SZ)],

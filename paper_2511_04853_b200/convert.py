@@ -211,8 +211,9 @@ def from_aosoa(a: Aosoa, coll, sync: bool = True) -> None:
     """Scatter AoSoA tiles back into a collection (casting to the leaf types)."""
     lay = coll.layout
     with lay.engine_ops():
-        lay.reserve(MAIN_TAG, a.n)
-        lay._set_sizes_for_engine({MAIN_TAG: a.n})
+        # through resize, not the engine's size hook: records of leaves the AoSoA does not carry start at
+        # zero and jagged prefix sums stay monotone (ADVICE r01)
+        coll.resize(a.n)
     coll._bump()
     if a.n:
         dev = _engine_device(a.info, lay.info)

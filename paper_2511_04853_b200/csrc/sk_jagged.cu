@@ -1026,6 +1026,7 @@ __global__ void __launch_bounds__(F_NT, 3) pack_fused_kernel(const __grid_consta
   };
   stamp(0);
 
+
   for (int round = 0;; ++round) {
     // the first block is the CTA's own index (CTAs are dispatched in index order, so a block only ever
     // waits on blocks whose CTAs run -- the assumption CUB's single-pass scan makes); later blocks by

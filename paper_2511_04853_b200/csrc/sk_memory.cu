@@ -1,6 +1,7 @@
 // Memory-context plumbing of libsoakit_b200: allocation, copies, memset,
 // memmove, streams/events, peer access, IPC. Replaces the mock device and the
 // default copier of the reference (memctx.py:115-143, 304-360).
+#include <algorithm>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -380,6 +381,59 @@ __global__ void fill_random_kernel(uint8_t* dst, size_t nbytes, uint64_t seed, u
     dst[nw * 8 + threadIdx.x] = static_cast<uint8_t>(splitmix64(seed, first + nw) >> (8 * threadIdx.x));
 }
 
+// ---- batched row moves of a layout splice (insert / erase / grow of every stream at once) ----
+// Pass 1 stages every move's source in one temporary (so a move may overlap itself and a zero fill may
+// cover another move's source), pass 2 writes the staged bytes to their destinations and applies the
+// zero fills. Work is cut into 64 KB chunks over all ops; 16-byte vectors when the addresses allow.
+constexpr int kMoveOps = 128;
+constexpr uint64_t kMoveChunk = 64 << 10;
+
+struct MoveBatch {
+  int count;
+  int pass;                 // 1: sources -> tmp; 2: tmp -> destinations, zero fills
+  uint8_t* tmp;
+  uint64_t chunk0[kMoveOps + 1];  // first chunk of op i (prefix over the ops active in this pass)
+  uint64_t tmp_off[kMoveOps];
+  sk_move op[kMoveOps];
+};
+
+__device__ __forceinline__ void copy_span(uint8_t* d, const uint8_t* s, uint64_t n) {
+  const int t = threadIdx.x;
+  if (((reinterpret_cast<uintptr_t>(d) | reinterpret_cast<uintptr_t>(s) | n) & 15) == 0) {
+    for (uint64_t i = t; i < n / 16; i += blockDim.x)
+      reinterpret_cast<uint4*>(d)[i] = reinterpret_cast<const uint4*>(s)[i];
+  } else {
+    for (uint64_t i = t; i < n; i += blockDim.x) d[i] = s[i];
+  }
+}
+
+__device__ __forceinline__ void zero_span(uint8_t* d, uint64_t n) {
+  const int t = threadIdx.x;
+  if (((reinterpret_cast<uintptr_t>(d) | n) & 15) == 0) {
+    for (uint64_t i = t; i < n / 16; i += blockDim.x) reinterpret_cast<uint4*>(d)[i] = make_uint4(0, 0, 0, 0);
+  } else {
+    for (uint64_t i = t; i < n; i += blockDim.x) d[i] = 0;
+  }
+}
+
+__global__ void __launch_bounds__(256) move_batch_kernel(const __grid_constant__ MoveBatch B) {
+  const uint64_t total = B.chunk0[B.count];
+  for (uint64_t c = blockIdx.x; c < total; c += gridDim.x) {
+    int i = 0;
+    while (B.chunk0[i + 1] <= c) ++i;  // <= 128 ops: a short scan
+    const sk_move& m = B.op[i];
+    const uint64_t off = (c - B.chunk0[i]) * kMoveChunk;
+    const uint64_t n = min(kMoveChunk, m.bytes - off);
+    if (B.pass == 1) {
+      copy_span(B.tmp + B.tmp_off[i] + off, static_cast<const uint8_t*>(m.src) + off, n);
+    } else if (m.src) {
+      copy_span(static_cast<uint8_t*>(m.dst) + off, B.tmp + B.tmp_off[i] + off, n);
+    } else {
+      zero_span(static_cast<uint8_t*>(m.dst) + off, n);
+    }
+  }
+}
+
 // mismatching bytes of a vs b (verification of full-size round trips on the
 // device: a 32 GB identity check must not cross PCIe)
 __global__ void compare_kernel(const uint8_t* a, const uint8_t* b, size_t n, unsigned long long* count) {
@@ -408,6 +462,55 @@ __global__ void compare_kernel(const uint8_t* a, const uint8_t* b, size_t n, uns
 }
 
 }  // namespace sk
+
+extern "C" int sk_move_batch_async(const sk_move* ops, int count, uintptr_t stream) {
+  if (count < 0 || (count && !ops)) return set_error(SK_ERR_INVALID, "bad op list");
+  cudaStream_t s;
+  int rc = stream_of(stream, &s);
+  if (rc) return rc;
+  int dev = 0;
+  SK_TRY(cudaGetDevice(&dev));
+  DeviceState* d = nullptr;
+  rc = device_state(dev, &d);
+  if (rc) return rc;
+  for (int base = 0; base < count; base += sk::kMoveOps) {
+    const int m = std::min(count - base, sk::kMoveOps);
+    sk::MoveBatch B;
+    memset(&B, 0, sizeof(B));
+    uint64_t staged = 0;
+    for (int i = 0; i < m; ++i) {
+      B.op[i] = ops[base + i];
+      if (B.op[i].src) {
+        B.tmp_off[i] = staged;
+        staged += (B.op[i].bytes + 255) & ~uint64_t(255);
+      }
+    }
+    if (staged) SK_TRY(cudaMallocAsync(reinterpret_cast<void**>(&B.tmp), staged, s));
+    for (int pass = staged ? 1 : 2; pass <= 2; ++pass) {
+      // the ops of this pass: moves in pass 1, everything in pass 2
+      sk::MoveBatch P = B;
+      P.pass = pass;
+      P.count = 0;
+      uint64_t chunks = 0;
+      for (int i = 0; i < m; ++i) {
+        if (pass == 1 && !B.op[i].src) continue;
+        if (!B.op[i].bytes) continue;
+        P.op[P.count] = B.op[i];
+        P.tmp_off[P.count] = B.tmp_off[i];
+        P.chunk0[P.count] = chunks;
+        chunks += (B.op[i].bytes + sk::kMoveChunk - 1) / sk::kMoveChunk;
+        ++P.count;
+      }
+      P.chunk0[P.count] = chunks;
+      if (!chunks) continue;
+      const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(chunks, static_cast<uint64_t>(d->sm_count) * 8));
+      sk::move_batch_kernel<<<grid, 256, 0, s>>>(P);
+      SK_TRY(cudaGetLastError());
+    }
+    if (staged) SK_TRY(cudaFreeAsync(B.tmp, s));
+  }
+  return SK_OK;
+}
 
 extern "C" int sk_compare_bytes(const void* a, const void* b, size_t nbytes, unsigned long long* mismatches,
                                 uintptr_t stream) {

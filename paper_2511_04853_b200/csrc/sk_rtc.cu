@@ -372,8 +372,10 @@ struct Compiled {
   bool ok = false;
   cudaLibrary_t lib = nullptr;
   cudaKernel_t kernel = nullptr;
-  int max_smem_set = 0;
-  std::vector<std::pair<int, int>> occ;  // smem -> CTAs per SM
+  // kernel attributes and occupancy are per device: a signature first launched on cuda:1 must set its
+  // dynamic shared memory limit there too
+  int max_smem_set[64] = {};
+  std::vector<std::pair<int64_t, int>> occ;  // (device << 32 | smem) -> CTAs per SM
 };
 
 static std::mutex g_mu;
@@ -447,6 +449,10 @@ int launch_specialized(const sk_conv_desc& d, const Plan& P, const DeviceState& 
   Spec spec;
   if (!generate(d, P, epi_fields, &spec)) return SK_OK;
   Compiled* c = nullptr;
+  int dev = 0;
+  SK_TRY(cudaGetDevice(&dev));
+  dev &= 63;
+  const int64_t occ_key = (static_cast<int64_t>(dev) << 32) | static_cast<int64_t>(P.smem_total);
   {
     std::lock_guard<std::mutex> lk(g_mu);
     auto it = g_cache->find(spec.key);
@@ -457,25 +463,28 @@ int launch_specialized(const sk_conv_desc& d, const Plan& P, const DeviceState& 
     }
     c = &it->second;
     if (!c->ok) return SK_OK;
-    if (P.smem_total > c->max_smem_set) {
-      if (cudaFuncSetAttribute(reinterpret_cast<const void*>(c->kernel), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               P.smem_total) != cudaSuccess) {
+    if (P.smem_total > c->max_smem_set[dev]) {
+      if (cudaKernelSetAttributeForDevice(c->kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, P.smem_total,
+                                          dev) != cudaSuccess) {
         cudaGetLastError();
         return SK_OK;
       }
-      c->max_smem_set = P.smem_total;
+      c->max_smem_set[dev] = P.smem_total;
     }
   }
   int per_sm = 0;
-  for (const auto& e : c->occ)
-    if (e.first == P.smem_total) per_sm = e.second;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    for (const auto& e : c->occ)
+      if (e.first == occ_key) per_sm = e.second;
+  }
   if (!per_sm) {
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, reinterpret_cast<const void*>(c->kernel), NT,
                                                       P.smem_total) != cudaSuccess || per_sm < 1)
       per_sm = 1;
     cudaGetLastError();
     std::lock_guard<std::mutex> lk(g_mu);
-    c->occ.push_back({P.smem_total, per_sm});
+    c->occ.push_back({occ_key, per_sm});
   }
   const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(static_cast<int64_t>(ds.sm_count) * per_sm, P.ntiles));
   void* args[] = {const_cast<Plan*>(&P)};

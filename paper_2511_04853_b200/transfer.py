@@ -244,6 +244,15 @@ class PreparedTransfer:
     storage; pageable-host endpoints cannot be captured (use pinned)."""
 
     def __init__(self, dst: Collection, src: Collection) -> None:
+        ends = (src.info.context, dst.info.context)
+        if memctx.HOST in ends:
+            raise TransferError("prepared transfers need pinned or device endpoints: pageable host memory "
+                                "cannot be captured into a CUDA graph")
+        if all(c == memctx.PINNED for c in ends):
+            # pinned <-> pinned byte copies run on the host (numpy), outside any stream: a graph would hold
+            # only part of the transfer (or nothing) and replay stale side data
+            raise TransferError("prepared transfers need a device endpoint; pinned <-> pinned copies run on the "
+                                "host and cannot be replayed from a CUDA graph")
         self.dst, self.src = dst, src
         self.spec = copy_collection(dst, src)  # eager warm-up; also resolves the spec
         self.device = _engine_device(dst, src)

@@ -344,3 +344,25 @@ def test_aosoa_to_planes_all_fields_vs_records(lanes, back_kind):
                     want = want.astype(np.float32).astype(np.float64)
             assert got.tobytes() == np.ascontiguousarray(want).tobytes(), nm
     a.free()
+
+
+def test_from_aosoa_grows_through_resize():
+    """records created by from_aosoa start at zero in the leaves the AoSoA does not carry, and a
+    jagged vector's prefix sums stay monotone (all records empty)."""
+    n = 10_007
+    parts = sk.Collection(sensor.PARTICLE_SCHEMA, ly.PER_FIELD, CUDA)
+    with mc.execution_scope(mc.CUDA):
+        parts.resize(5)
+    src = sk.Collection(sensor.PARTICLE_SCHEMA, ly.PER_FIELD, CUDA)
+    with mc.execution_scope(mc.CUDA):
+        src.resize(n)
+    fields = [sk.AosoaField("energy", "f32"), sk.AosoaField("origin", "u64")]
+    a = sk.to_aosoa(src, fields, 64)
+    sk.from_aosoa(a, parts)
+    with mc.execution_scope(mc.CUDA):
+        assert parts.size() == n
+        assert not parts.prefix_sums("sensors").any()
+        assert parts.jagged_size("sensors") == 0
+        assert not parts.column("x_variance").read().any()
+        assert not parts.column("noisy_count").read().any()
+    a.free()

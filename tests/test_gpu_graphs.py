@@ -76,3 +76,14 @@ def test_prepared_transfer_survives_staging_growth():
     for i in range(8):
         assert planes[f"f{i}#0"] == want[f"f{i}"][0].tobytes()
     prep.close()
+
+
+def test_prepare_refuses_host_only_pairs():
+    """pinned <-> pinned copies run on the host, outside the graph; a prepared transfer over them
+    would replay nothing (bulk / plane copies) or stale side data (Particle's jagged pools)."""
+    src = sk.Collection(sensor.PARTICLE_SCHEMA, ly.AOS, PINNED)
+    src.resize(10)
+    for kind in (ly.PER_FIELD, ly.AOS):
+        dst = sk.Collection(sensor.PARTICLE_SCHEMA, kind, PINNED)
+        with pytest.raises(sk.TransferError):
+            tr.prepare(dst, src)

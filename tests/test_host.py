@@ -263,3 +263,12 @@ def test_library_loads_and_reports_no_device_cleanly():
     assert st in (nat.SK_OK, nat.SK_ERR_NO_DEVICE, nat.SK_ERR_CUDA)
     if st != nat.SK_OK:
         assert n.value == 0 and lib.sk_last_error()
+
+
+def test_prepare_refuses_pageable_endpoints():
+    """A CUDA graph cannot capture pageable host copies: refused before anything runs."""
+    src = sk.Collection(wl.OBJ8_SCHEMA, ly.AOS, mc.ContextInfo.host())
+    src.resize(4)
+    dst = sk.Collection(wl.OBJ8_SCHEMA, ly.PER_FIELD, mc.ContextInfo.host())
+    with pytest.raises(sk.TransferError):
+        tr.prepare(dst, src)
