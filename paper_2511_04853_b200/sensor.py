@@ -199,11 +199,78 @@ def _noise_behavior(coll) -> DeviceArray:
     return noise_for_collection(coll)
 
 
+def _one_record(view) -> tuple[int, dict, int]:
+    """(device, plane addresses, record index) of a record view on a device collection."""
+    coll = view._coll
+    dev, planes = _device_planes(coll)
+    return dev, planes, view.index
+
+
+def _calibrate_object(view) -> None:
+    """Per-object form (detector/schemas.py:15-17). Host records: numpy scalar
+    arithmetic as in the reference; device records: K5 over that one record."""
+    if view._coll.layout.host_visible:
+        cal = view.calibration_data
+        view.energy = np.float32(cal.parameter_A) * np.float32(view.counts) + np.float32(cal.parameter_B)
+        return
+    dev, p, i = _one_record(view)
+    nat.call("sk_sensor_calibrate", 1, p[_COUNTS] + 8 * i, p[_A] + 4 * i, p[_B] + 4 * i, p[_ENERGY] + 4 * i,
+             nat.stream(dev))
+    nat.sync(dev)
+
+
+def _noise_object(view) -> np.float32:
+    """Per-object form (detector/schemas.py:20-26)."""
+    if view._coll.layout.host_visible:
+        cal = view.calibration_data
+        e = np.maximum(np.float32(view.energy), np.float32(0.0))
+        n = np.float32(cal.noise_A) * np.sqrt(e) + np.float32(cal.noise_B)
+        return n * np.float32(2.0) if cal.noisy else n
+    dev, p, i = _one_record(view)
+    out = DeviceArray(1, np.float32, memctx.ContextInfo.cuda(dev))
+    nat.call("sk_sensor_noise", 1, p[_ENERGY] + 4 * i, p[_NA] + 4 * i, p[_NB] + 4 * i, p[_NOISY] + i, out.ptr,
+             nat.stream(dev))
+    val = out.numpy()[0]
+    out.free()
+    return val
+
+
 if not bh.is_registered("sensor_funcs"):
     bh.register_bundle("sensor_funcs", [
+        bh.BehaviorFunction("calibrate_energy", bh.TARGET_OBJECT, _calibrate_object),
         bh.BehaviorFunction("calibrate_energy", bh.TARGET_COLLECTION, _calibrate_behavior),
+        bh.BehaviorFunction("get_noise", bh.TARGET_OBJECT, _noise_object),
         bh.BehaviorFunction("get_noise", bh.TARGET_COLLECTION, _noise_behavior),
     ])
+
+_EVENT_COLUMNS = ("type", "counts", "noisy", "parameter_A", "parameter_B", "noise_A", "noise_B")
+
+
+def fill_sensor_collection(coll, event) -> None:
+    """Load one event into a Sensor collection, reusing its size when it
+    matches (detector/reconstruct.py:142-154). `event` is the reference's
+    EventData (or any object/mapping with its seven columns). Host
+    collections are written through their columns as in the reference;
+    device collections take one host-to-device copy per plane (call it from
+    execution_scope("cuda"), like any device-side size change)."""
+    from .collection import _write_plane
+
+    get = (lambda k: event[k]) if isinstance(event, dict) else (lambda k: getattr(event, k))
+    spec = event.get("spec") if isinstance(event, dict) else getattr(event, "spec", None)
+    n = spec.n_sensors if spec is not None else len(get("type"))
+    if coll.size() != n:
+        coll.clear()
+        coll.resize(n)
+    lay = coll.layout
+    for name in _EVENT_COLUMNS:
+        leaf_path = name if name in ("type", "counts") else "calibration_data." + name
+        values = np.asarray(get(name))
+        if lay.host_visible:
+            coll.column(leaf_path).np[:] = values
+        else:
+            lay.check_writable()
+            _write_plane(lay, coll.plan.leaf(leaf_path), 0, 0, values)
+    coll._bump()
 
 SENSOR_SCHEMA = sc.Schema("Sensor", (
     sc.declare_per_item("type", SENSOR_TYPE),

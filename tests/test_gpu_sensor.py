@@ -146,3 +146,27 @@ def test_host_resident_collection_is_refused():
     host = sk.Collection(sensor.SENSOR_SCHEMA, ly.PER_FIELD, HOST)
     with pytest.raises(sk.AccessError):
         host.funcs.calibrate_energy()
+
+
+@pytest.mark.parametrize("ctx", ["host", "cuda"])
+def test_fill_sensor_collection_and_object_behaviors(ctx):
+    """fill_sensor_collection (reconstruct.py:142-154) on host and device collections, then the object-target
+    behaviors (detector/schemas.py:15-26): host records run the reference's scalar arithmetic, device records
+    run K5 over one record. Both equal the collection-level result."""
+    ev = R.generate_event(101, 37, seed=11, density=0.01)
+    info = mc.ContextInfo.host() if ctx == "host" else CUDA
+    c = sk.Collection(sensor.SENSOR_SCHEMA, ly.PER_FIELD, info)
+    scope = mc.HOST if ctx == "host" else mc.CUDA
+    with mc.execution_scope(scope):
+        sensor.fill_sensor_collection(c, ev)
+        assert c.size() == 101 * 37
+        for i in (0, 17, 3736):
+            c.record(i).funcs.calibrate_energy()
+        energy = c.column("energy").read()
+        noise_one = [c.record(i).funcs.get_noise() for i in (0, 17, 3736)]
+    want_e = R.calibrate(ev["counts"], ev["parameter_A"], ev["parameter_B"])
+    want_n = R.noise(want_e, ev["noise_A"], ev["noise_B"], ev["noisy"])
+    for k, i in enumerate((0, 17, 3736)):
+        assert energy[i].tobytes() == want_e[i].tobytes()
+        assert np.float32(noise_one[k]).tobytes() == want_n[i].tobytes()
+    assert not energy[1:17].any()  # only the records asked for were calibrated

@@ -272,3 +272,15 @@ def test_prepare_refuses_pageable_endpoints():
     dst = sk.Collection(wl.OBJ8_SCHEMA, ly.PER_FIELD, mc.ContextInfo.host())
     with pytest.raises(sk.TransferError):
         tr.prepare(dst, src)
+
+
+def test_move_collection_copies_then_clears_source():
+    """move_collection (transfer.py:119-124): copy, then clear the source under engine_ops; storage stays."""
+    src = sk.Collection(wl.CLUSTER_SCHEMA, ly.PER_FIELD, mc.ContextInfo.host())
+    src.resize(6)
+    src.column("seed").np[:] = np.arange(6, dtype=np.uint64) * 7
+    want = src.dump()
+    dst = sk.Collection(wl.CLUSTER_SCHEMA, ly.PER_FIELD, mc.ContextInfo.host())
+    assert tr.move_collection(dst, src) == "bulk-same-kind"
+    assert dst.dump() == want
+    assert src.size() == 0 and src.capacity() >= 6
