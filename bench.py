@@ -25,6 +25,7 @@ host cores instead, on rank 0 only.
 from __future__ import annotations
 
 import argparse
+import itertools
 import json
 import os
 import statistics
@@ -260,6 +261,35 @@ def run_ours(args) -> None:
     barrier()
     h2d_gbs = min_over_ranks(m * 32 * 3 / (l0.elapsed_ms(l1) / 1e3) / 1e9)
     host.free()
+    # the same through PAGEABLE host memory (the reference's default placement, ContextInfo.host()):
+    # the pipeline stages it through pinned buffers; a smaller bounded sample
+    mp_ = min(m, args.e2e_objects // 4)
+    page = sk.Collection(wl.OBJ8_SCHEMA, ly.AOS, mc.ContextInfo.host())
+    page.resize(mp_)
+    nat.memcpy(page.layout._struct_buf.ptr, aos.layout._struct_buf.ptr, mp_ * 32, dev)
+    nat.sync(dev)
+    tails_p = [dst.layout.plane_address(dst.plan.leaf(f"f{i}")) + (mp_ - 1) * 4 for i in range(8)]
+
+    def e2e_pageable():
+        tr.copy_collection(dst, page)
+        for i, p in enumerate(tails_p):
+            nat.memcpy(result.ctypes.data + 4 * i, p, 4, dev)
+        nat.sync(dev)
+
+    e2e_pageable()
+    q0, q1 = nat.Event(), nat.Event()
+    barrier()
+    q0.record(dev)
+    for _ in range(e2e_steps):
+        e2e_pageable()
+    q1.record(dev)
+    barrier()
+    pg_ms = max_over_ranks(q0.elapsed_ms(q1) / e2e_steps)
+    pageable = {"value": round(sum_over_ranks(mp_) * BYTES_PER_OBJECT / (pg_ms / 1e3) / 1e9, 2), "unit": UNIT,
+                "ms_per_step": round(pg_ms, 3), "h2d_bytes_per_step": mp_ * 32 * world,
+                "sample": f"{mp_} objects per rank in pageable host memory (numpy) -> device per_field via "
+                          "copy_collection, then D2H of the last converted record"}
+    page.free()
     dst.free()
 
     # ---- layout-changing peer pull (config 5b): rank r converts the AoS shard
@@ -347,12 +377,17 @@ def run_ours(args) -> None:
     if rank == 0 and world == 1 and not args.no_cpu:
         from oracle import cpu_baseline
 
-        cb = cpu_baseline.single_core(args.cpu_objects, budget_s=args.cpu_seconds)
-        cpu = {"value": round(cb["gbs"], 3), "unit": UNIT, "cores": 1, "kind": "port",
+        cb = cpu_baseline.reference_single_core(args.cpu_objects, budget_s=args.cpu_seconds)
+        if cb is not None:
+            what = ("soakit's own copy_collection(per_field, aos) on host collections (per-leaf-default, "
+                    "transfer.py:171-236) from baseline/_ref")
+        else:
+            cb = dict(cpu_baseline.single_core(args.cpu_objects, budget_s=args.cpu_seconds), kind="port")
+            what = "reference per-leaf numpy path (transfer.py:196-228) restated in oracle/cpu_baseline.py"
+        cpu = {"value": round(cb["gbs"], 3), "unit": UNIT, "cores": 1, "kind": cb["kind"],
                "objects_per_s": round(cb["objects_per_s"]),
-               "sample": f"{args.cpu_objects} Obj8 objects, reference per-leaf numpy path "
-                         f"(transfer.py:196-228) restated in oracle/cpu_baseline.py, mean of fastest of "
-                         f"{cb['reps']} reps; host: {os.cpu_count()} x {_cpu_info()}"}
+               "sample": f"{args.cpu_objects} Obj8 objects, {what}, mean of the fastest samples "
+                         f"(bench.py:214-215); host: {os.cpu_count()} x {_cpu_info()}"}
         if extra:
             # the reference's CPU path beside each extra config (one core, bounded samples)
             pc = cpu_baseline.per_config(budget_s=1.5)
@@ -403,7 +438,11 @@ def run_ours(args) -> None:
                 "h2d_link_gbs_measured": round(h2d_gbs, 1),
                 "frac_of_h2d_link": round(m * 32 * world / (e2e_ms / 1e3) / 1e9 / (h2d_gbs * world), 3),
                 "sample": f"{m} objects per rank in pinned host memory -> device per_field via copy_collection "
-                          "(chunked H2D | convert | on 3 streams), then D2H of the last converted record"},
+                          "(chunked H2D | convert | on 3 streams), then D2H of the last converted record",
+                "result_readback": "32 B per rank per step (the last converted record, 8 planes x 4 B) of the "
+                                   f"{m * 32} B converted: the converted planes stay in HBM, where the "
+                                   "application's next kernel reads them",
+                "pageable_host": pageable},
         "gpu_launches": args.steps,
         "clocks": clk,
         "cpu_baseline": cpu,
@@ -476,6 +515,94 @@ def verify_obj8_shard(aos, soa, n: int, lo: int, dev: int, rank: int) -> dict:
                                  "64 random) x 8 planes, byte-exact vs oracle/restate.splitmix_image",
             "full_round_trip": f"{n} records: planes -> AoS (K2) == input AoS, 0 of {n * 32} bytes differ "
                                "(sk_compare_bytes on the device)"}
+
+
+def config2_api_paths(a2, p2, h2, noise, cells, dev, peak, queued, timed) -> dict:
+    """Config 2 through the reference-facing API rather than the fused extension:
+    copy_collection + funcs.calibrate_energy() + funcs.get_noise() (the
+    reference's prepare phase, bench.py:174-178), batched and per event with the
+    reference's protocol (mean of the 10 fastest of 50 reps cycling 10 events,
+    bench.py:214-289), plus the K5 kernels alone against their roofline."""
+    import time
+
+    import numpy as np
+
+    import paper_2511_04853_b200 as sk
+    from paper_2511_04853_b200 import _native as nat
+    from paper_2511_04853_b200 import layouts as ly, memctx as mc, schema as sc, sensor, transfer as tr
+    from paper_2511_04853_b200.devarray import DeviceArray
+
+    def api_batch():  # pinned AoS -> device planes, then the two behaviors (separate K5 kernels)
+        tr.copy_collection(p2, h2)
+        with mc.execution_scope(mc.CUDA):
+            p2.funcs.calibrate_energy()
+            p2.funcs.get_noise().free()
+
+    ms_api = timed(api_batch, steps=3, warmup=1)
+
+    def api_device():  # the same three steps on device-resident AoS records
+        tr.copy_collection(p2, a2, {"async": True})
+        sensor.calibrate_collection(p2, sync=False)
+        sensor.noise_for_collection(p2, noise, sync=False)
+
+    ms_api_dev = queued(api_device, steps=10)
+    ms_cal = queued(lambda: sensor.calibrate_collection(p2, sync=False), steps=20)
+    ms_noise = queued(lambda: sensor.noise_for_collection(p2, noise, sync=False), steps=20)
+
+    # per event, the reference's protocol
+    ev = 436 * 436
+    pinned = mc.ContextInfo.pinned()
+    events = []
+    for e in range(10):
+        c = sk.Collection(sensor.SENSOR_SCHEMA, ly.AOS, pinned)
+        c.resize(ev)
+        nat.memcpy(c.layout._struct_buf.ptr, a2.layout._struct_buf.ptr + e * ev * 30, ev * 30, dev)
+        events.append(c)
+    nat.sync(dev)
+    d1 = sk.Collection(sensor.SENSOR_SCHEMA, ly.PER_FIELD, mc.ContextInfo.cuda(dev))
+    n1 = DeviceArray(ev, np.float32, mc.ContextInfo.cuda(dev))
+
+    def protocol(rep) -> float:
+        rep(0)
+        samples = []
+        for r in range(50):
+            t0 = time.perf_counter()
+            rep(r % 10)
+            samples.append(time.perf_counter() - t0)
+        return sum(sorted(samples)[:10]) / 10 * 1e3
+
+    def api_event(e):
+        tr.copy_collection(d1, events[e])
+        sensor.calibrate_collection(d1)
+        sensor.noise_for_collection(d1, n1)
+
+    ms_ev_api = protocol(api_event)
+    ms_ev_fused = protocol(lambda e: sensor.transfer_calibrate(d1, events[e], n1))
+    for c in events:
+        c.free()
+    d1.free()
+    n1.free()
+    return {
+        "api_pinned_e2e_ms": round(ms_api, 3),
+        "api_pinned_e2e_cells_per_s": round(cells / ms_api * 1e3),
+        "api_device_ms": round(ms_api_dev, 3),
+        "api_device_gbs": round(cells * 64 / ms_api_dev / 1e6, 1),
+        "k5_calibrate": {"ms": round(ms_cal, 4), "gbs": round(cells * 20 / ms_cal / 1e6, 1),
+                         "frac": round(cells * 20 / ms_cal / 1e6 / peak, 3),
+                         "bytes_per_cell": "20 (counts 8 + A 4 + B 4 read, energy 4 written)"},
+        "k5_noise": {"ms": round(ms_noise, 4), "gbs": round(cells * 17 / ms_noise / 1e6, 1),
+                     "frac": round(cells * 17 / ms_noise / 1e6 / peak, 3),
+                     "bytes_per_cell": "17 (energy 4 + nA 4 + nB 4 + noisy 1 read, noise 4 written)"},
+        "per_event_protocol": {
+            "api_ms": round(ms_ev_api, 4), "fused_ms": round(ms_ev_fused, 4),
+            "api_cells_per_s": round(ev / ms_ev_api * 1e3), "fused_cells_per_s": round(ev / ms_ev_fused * 1e3),
+            "note": "one 436x436 event per rep from pinned AoS: copy_collection + calibrate + noise (api) or "
+                    "transfer_calibrate (fused), host-synchronous; mean of the 10 fastest of 50 reps cycling "
+                    "10 events (bench.py:214-289)"},
+        "api_note": "api_*: copy_collection(per_field@cuda, aos) + funcs.calibrate_energy() + funcs.get_noise(), "
+                    "the reference's prepare phase (bench.py:174-178): one conversion launch plus the two K5 "
+                    "kernels, i.e. two more passes over the planes than the fused transfer_calibrate",
+    }
 
 
 def verify_aosoa_tiles(ao, n: int, fields, dev: int, seed: int = 4, samples: int = 32) -> str:
@@ -594,13 +721,33 @@ def run_extras(args, dev: int) -> dict:
     a1, p1 = coll(wl.OBJ8_SCHEMA, ly.AOS, n), coll(wl.OBJ8_SCHEMA, ly.PER_FIELD, n)
     wl.fill_random_device(a1.layout._struct_buf.ptr, n * 32, 1, dev)
     ms = queued(lambda: tr.copy_collection(p1, a1, {"async": True}), steps=20)
+    # cold L2: rotate over 4 input/output pairs (256 MB > the 126 MB L2), so no conversion finds its
+    # records or planes left in L2 by the previous one
+    sets = [(a1, p1)]
+    for k in range(3):
+        a, p = coll(wl.OBJ8_SCHEMA, ly.AOS, n), coll(wl.OBJ8_SCHEMA, ly.PER_FIELD, n)
+        wl.fill_random_device(a.layout._struct_buf.ptr, n * 32, 2 + k, dev)
+        sets.append((a, p))
+    turn = itertools.cycle(sets)
+
+    def cold():
+        a, p = next(turn)
+        tr.copy_collection(p, a, {"async": True})
+
+    ms_cold = queued(cold, steps=40)
     h1 = coll(wl.OBJ8_SCHEMA, ly.AOS, n, mc.ContextInfo.pinned())
     ms_h = timed(lambda: tr.copy_collection(p1, h1), steps=5)
     out["config1_obj8_1M"] = {"device_ms": round(ms, 4), "device_gbs": round(n * 64 / ms / 1e6, 1),
-                              "frac": round(n * 64 / ms / 1e6 / peak, 3), "pinned_h2d_e2e_ms": round(ms_h, 3),
-                              "e2e_gbs": round(n * 64 / ms_h / 1e6, 1)}
-    for c in (a1, p1, h1):
-        c.free()
+                              "frac": round(n * 64 / ms / 1e6 / peak, 3),
+                              "cold_l2_device_ms": round(ms_cold, 4),
+                              "cold_l2_frac": round(n * 64 / ms_cold / 1e6 / peak, 3),
+                              "pinned_h2d_e2e_ms": round(ms_h, 3), "e2e_gbs": round(n * 64 / ms_h / 1e6, 1),
+                              "note": "device_ms repeats one 64 MB pair (L2-resident: 64 MB < 126 MB L2); "
+                                      "cold_l2 rotates 4 pairs (256 MB) so every launch reads and writes HBM"}
+    for a, p in sets:
+        a.free()
+        p.free()
+    h1.free()
 
     # config 2: case study, 64 events x 190,096 cells generated on the device
     # (splitmix64, density 0.002), AoS (30 B) -> planes + energy + noise fused
@@ -624,6 +771,8 @@ def run_extras(args, dev: int) -> dict:
         "data": "64 events 436x436, seeds 0..63, density 0.002, generated on-device (bit-exact with "
                 "detector/events.py:85-133)"}
     out["config2_sensor_64x190096"]["parity"] = verify_sensor_events(p2, noise, dev, (0, 31, 63))
+    out["config2_sensor_64x190096"].update(config2_api_paths(a2, p2, h2, noise, cells, dev, peak, queued, timed))
+    out["config2_sensor_64x190096"]["parity_api_path"] = verify_sensor_events(p2, noise, dev, (5, 47))
     # the reference's second phase on the same events: reconstruct + transfer back (bench.py:180-184)
     from paper_2511_04853_b200 import sensor as sn
 
@@ -652,6 +801,18 @@ def run_extras(args, dev: int) -> dict:
         c3.resize(nc)
     members = int(lens.sum())
     ms_api = timed(lambda: jagged.pack(c3, "members", d_lens, d_off, d_pool), steps=10)
+    # the same call with the inputs in pinned and in pageable HOST memory: validation on the host, the
+    # H2D of lengths / offsets / pool and the pack, with the member total read back
+    pinned_in = []
+    for x in (lens, offsets, pool):
+        b = mc.allocate(mc.ContextInfo.pinned(), x.nbytes)
+        v = b._data.view(x.dtype)
+        v[:] = x
+        pinned_in.append((b, v))
+    ms_pinned = timed(lambda: jagged.pack(c3, "members", *(v for _, v in pinned_in)), steps=5, warmup=1)
+    ms_pageable = timed(lambda: jagged.pack(c3, "members", lens, offsets, pool), steps=3, warmup=1)
+    for b, _ in pinned_in:
+        mc.deallocate(b)
     # the same fused pack through the C-ABI (scan + gather, no host readback), device time
     import ctypes as C
 
@@ -678,6 +839,11 @@ def run_extras(args, dev: int) -> dict:
         "members": members, "device_ms": round(ms, 4), "members_per_s": round(members / ms * 1e3),
         "gbs": round(algo / ms / 1e6, 1), "frac": round(algo / ms / 1e6 / peak, 3),
         "api_ms": round(ms_api, 4),
+        "host_input_e2e": {"pinned_ms": round(ms_pinned, 3), "pageable_ms": round(ms_pageable, 3),
+                           "h2d_bytes": int(lens.nbytes + offsets.nbytes + pool.nbytes),
+                           "note": "jagged.pack(collection, lens, offsets, pool) with numpy inputs in pinned / "
+                                   "pageable host memory: host-side validation (collection.py:546 raises before "
+                                   "mutating), H2D of the inputs, the fused pack, member total read back"},
         "note": "device_ms: sk_jagged_pack (one fused kernel: block sums, prefixes, gather) queued on the device; "
                 "api_ms: jagged.pack on a "
                 "Collection, incl. the host readback of the member total that sizes the pool; source segments "
@@ -722,7 +888,13 @@ def run_reference(args) -> None:
 
     procs = os.cpu_count() or 1
     n = args.ref_objects
-    r = cpu_baseline.multi_core(n, args.steps, max(1, args.warmup), procs)
+    r = cpu_baseline.reference_multi_core(n, args.steps, max(1, args.warmup), procs)
+    if r is not None:
+        what = (f"soakit's own copy_collection(per_field, aos) (per-leaf-default, transfer.py:171-236) from "
+                f"baseline/_ref, one process per core, each owning 1/{procs} of the records")
+    else:
+        r = dict(cpu_baseline.multi_core(n, args.steps, max(1, args.warmup), procs), kind="port")
+        what = f"reference per-leaf numpy path (oracle/cpu_baseline.py) sharded over {procs} processes"
     times = r["step_seconds"]
     t = statistics.mean(times)
     value = n * BYTES_PER_OBJECT / t / 1e9
@@ -731,11 +903,12 @@ def run_reference(args) -> None:
         "warmup": args.warmup, "ms_per_step": round(t * 1e3, 3), "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "u8", "data": "synthetic (random Obj8 records)", "impl": "reference",
         "config": {"workload": WORKLOAD, "objects_per_step": n, "record_bytes": 32,
-                   "algorithmic_bytes_per_object": BYTES_PER_OBJECT},
-        "cpu_baseline": {"value": round(value, 3), "unit": UNIT, "cores": procs, "kind": "port",
-                         "sample": f"{n} Obj8 objects per step, reference per-leaf numpy path "
-                                   f"(oracle/cpu_baseline.py) sharded over {procs} processes; "
-                                   f"host: {_cpu_info()}"},
+                   "algorithmic_bytes_per_object": BYTES_PER_OBJECT,
+                   "sample_note": f"each step converts a bounded {n}-object sample of the 1e9-object workload "
+                                  "(the CPU would need minutes per full step); the metric is a rate (GB/s), "
+                                  "compared rate against rate with our arm"},
+        "cpu_baseline": {"value": round(value, 3), "unit": UNIT, "cores": procs, "kind": r["kind"],
+                         "sample": f"{n} Obj8 objects per step, {what}; host: {_cpu_info()}"},
         "e2e": {"value": round(value, 3), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)

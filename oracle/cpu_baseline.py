@@ -176,3 +176,90 @@ def per_config(budget_s: float = 2.0, seed: int = 3) -> dict:
         t = _rate(lambda: R.to_aosoa(trk, fields, 128), budget_s)
     out["config4_aosoa"] = {"sample": f"{n4} tracks", "objects_per_s": n4 / t, "gbs": n4 * 76 / t / 1e9}
     return out
+
+
+# ---- the reference package itself (baseline/_ref) ------------------------------------------
+
+def import_reference():
+    """soakit from the git-ignored install under baseline/_ref (it travels to the
+    GPU box); None when it is absent -- the callers then time the port above."""
+    import importlib
+    import sys
+
+    root = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "baseline", "_ref")
+    if not os.path.isdir(os.path.join(root, "soakit")):
+        return None
+    if root not in sys.path:
+        sys.path.append(root)
+    return importlib.import_module("soakit")
+
+
+def _soakit_pair(sk, n: int, seed: int):
+    """AoS source with random records and a per_field destination, both host
+    collections of the Obj8 schema (8 x f32/i32)."""
+    schema = sk.Schema("Obj8", tuple(sk.declare_per_item(f"f{i}", sk.F32 if i % 2 == 0 else sk.I32)
+                                     for i in range(8)))
+    src = sk.Collection(schema, "aos")
+    src.resize(n)
+    rng = np.random.default_rng(seed)
+    raw = src.layout._struct_buf._data
+    chunk = 1 << 24
+    for lo in range(0, n * 32, chunk):
+        hi = min(lo + chunk, n * 32)
+        raw[lo:hi] = rng.integers(0, 256, hi - lo, dtype=np.uint8)
+    return src, sk.Collection(schema, "per_field")
+
+
+def reference_single_core(n: int, budget_s: float = 12.0, seed: int = 1) -> dict | None:
+    """soakit's own copy_collection(per_field, aos) on host collections
+    (per-leaf-default, transfer.py:171-236), one core, reference protocol."""
+    sk = import_reference()
+    if sk is None:
+        return None
+    src, dst = _soakit_pair(sk, n, seed)
+    assert sk.transfer.copy_collection(dst, src) == "per-leaf-default"
+    t = _rate(lambda: sk.transfer.copy_collection(dst, src), budget_s)
+    return {"seconds": t, "objects_per_s": n / t, "gbs": n * 64 / t / 1e9, "kind": "reference"}
+
+
+def _ref_worker(span, seed, steps, start, done, out):
+    sk = import_reference()
+    src, dst = _soakit_pair(sk, span, seed)
+    sk.transfer.copy_collection(dst, src)  # warm-up, also sizes dst
+    for _ in range(steps):
+        start.wait()
+        sk.transfer.copy_collection(dst, src)
+        done.wait()
+    out.put(int(dst.size()))
+
+
+def reference_multi_core(n: int, steps: int, warmup: int, procs: int | None = None, seed: int = 1) -> dict | None:
+    """soakit's copy_collection on every host core: one process per core owns
+    a contiguous 1/procs shard (its own AoS and per_field collections); a step
+    is every shard converting once, timed by the parent between two barriers."""
+    if import_reference() is None:
+        return None
+    procs = procs or os.cpu_count() or 1
+    cuts = np.linspace(0, n, procs + 1).astype(np.int64)
+    ctx = mp.get_context("fork")
+    total = steps + warmup
+    start, done = ctx.Barrier(procs + 1), ctx.Barrier(procs + 1)
+    out = ctx.Queue()
+    workers = [ctx.Process(target=_ref_worker, args=(int(cuts[i + 1] - cuts[i]), seed + i, total, start, done, out))
+               for i in range(procs)]
+    for w in workers:
+        w.start()
+    times = []
+    try:
+        for k in range(total):
+            start.wait()
+            t0 = time.perf_counter()
+            done.wait()
+            if k >= warmup:
+                times.append(time.perf_counter() - t0)
+        converted = sum(out.get(timeout=60) for _ in workers)
+        assert converted == n
+    finally:
+        for w in workers:
+            w.join(timeout=60)
+    return {"step_seconds": times, "procs": procs, "n": n, "kind": "reference"}
