@@ -17,9 +17,12 @@
 // a double in ~0.1% of cases, which reaches the float32 variance only when the
 // double lies within 1e-16 of an f32 rounding boundary.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "sk_internal.cuh"
+
 
 namespace sk {
 namespace reco {
@@ -53,8 +56,11 @@ struct Args {
   uint8_t* state;
   uint8_t* consumed;
   int64_t* cand;
-  unsigned long long* counters;  // [0] ncand [1] nready [2] pending [3] unused [4] this round's first slot
+  // [0] ncand [1] nready (this round) [2] next pending list size [3] current pending list size
+  // [4] this round's first slot [5] pending seeds seen this round [6] rounds
+  unsigned long long* counters;
   int64_t* ready;
+  int32_t* list[2];  // candidates (by index into cand) still pending: this round's and the next one's
   Slot* slots;
   uint64_t* contrib;  // MAXC per slot
   unsigned long long* event_count;
@@ -114,17 +120,25 @@ __global__ void __launch_bounds__(NT) init_kernel(Args A) {
   for (unsigned j = threadIdx.x; j < m; j += NT) A.cand[s_base + j] = seeds[j];
 }
 
-// phase 1 of a round: which pending seeds are ready. One thread per
-// candidate, its 9x9 neighbourhood a row (9 independent loads) at a time;
-// the pending count and the ready appends are aggregated per warp.
-__global__ void ready_kernel(Args A) {
+__device__ __forceinline__ unsigned long long ctr(const Args& A, int k) { return A.counters[k]; }
+
+// phase 1 of a round, over the candidates still pending (a list that shrinks
+// every round): a candidate consumed meanwhile drops out; one with a pending
+// seed of higher priority within distance 4 goes to the next round's list;
+// the rest are ready. Its 9x9 neighbourhood is scanned a row (9 independent
+// loads) at a time; counts and appends are aggregated per warp. Every kernel
+// of a round returns at once when nothing is pending any more, so the host
+// queues rounds without checking in between.
+__global__ void __launch_bounds__(NT) ready_kernel(Args A, int parity) {
   const int lane = threadIdx.x & 31;
-  const int64_t ncand = static_cast<int64_t>(A.counters[0]);
+  const int64_t m = static_cast<int64_t>(ctr(A, 3));
+  const int32_t* cur = A.list[parity];
+  int32_t* nxt = A.list[parity ^ 1];
   const int64_t stride = static_cast<int64_t>(gridDim.x) * NT;
-  for (int64_t k0 = static_cast<int64_t>(blockIdx.x) * NT + (threadIdx.x & ~31); k0 < ncand; k0 += stride) {
-    const int64_t k = k0 + lane;
-    const int64_t c = k < ncand ? A.cand[k] : 0;
-    const bool pend = k < ncand && A.state[c] == PENDING;
+  for (int64_t i0 = static_cast<int64_t>(blockIdx.x) * NT + (threadIdx.x & ~31); i0 < m; i0 += stride) {
+    const int64_t i = i0 + lane;
+    const int64_t c = i < m ? A.cand[cur[i]] : 0;
+    const bool pend = i < m && A.state[c] == PENDING;
     bool ok = pend;
     if (pend) {
       const int64_t base = (c / A.n) * A.n, loc = c - base;
@@ -141,14 +155,20 @@ __global__ void ready_kernel(Args A) {
         }
       }
     }
+    const bool wait = pend && !ok;
     const unsigned pm = __ballot_sync(0xffffffffu, pend), rm = __ballot_sync(0xffffffffu, ok);
-    unsigned long long rb = 0;
+    const unsigned wm = __ballot_sync(0xffffffffu, wait);
+    unsigned long long rb = 0, wb = 0;
     if (lane == 0) {
-      if (pm) atomicAdd(&A.counters[2], static_cast<unsigned long long>(__popc(pm)));
+      if (pm) atomicAdd(&A.counters[5], static_cast<unsigned long long>(__popc(pm)));
       if (rm) rb = atomicAdd(&A.counters[1], static_cast<unsigned long long>(__popc(rm)));
+      if (wm) wb = atomicAdd(&A.counters[2], static_cast<unsigned long long>(__popc(wm)));
     }
     rb = __shfl_sync(0xffffffffu, rb, 0);
-    if (ok) A.ready[rb + __popc(rm & ((1u << lane) - 1u))] = c;
+    wb = __shfl_sync(0xffffffffu, wb, 0);
+    const unsigned below = (1u << lane) - 1u;
+    if (ok) A.ready[rb + __popc(rm & below)] = c;
+    if (wait) nxt[wb + __popc(wm & below)] = cur[i];
   }
 }
 
@@ -157,15 +177,15 @@ __global__ void ready_kernel(Args A) {
 // so the cell loads run in parallel; lane 0 then adds the contributors up in
 // the reference's row-major order (reconstruct.py:84-117), fetching each by
 // shuffle, so every sum is bit-identical to the sequential walk.
-__global__ void process_kernel(Args A) {
+__global__ void __launch_bounds__(NT) process_kernel(Args A) {
   const int lane = threadIdx.x & 31;
-  const int64_t nready = static_cast<int64_t>(A.counters[1]);
+  const int64_t nready = static_cast<int64_t>(ctr(A, 1));
   const int64_t nwarps = static_cast<int64_t>(gridDim.x) * (NT / 32);
   for (int64_t k = static_cast<int64_t>(blockIdx.x) * (NT / 32) + (threadIdx.x >> 5); k < nready; k += nwarps) {
     const int64_t s = A.ready[k];
     // slot = this round's first slot + the ready index (no shared particle counter); a skipped seed leaves
     // a hole that the ordering pass drops
-    const unsigned long long p = A.counters[4] + static_cast<unsigned long long>(k);
+    const unsigned long long p = ctr(A, 4) + static_cast<unsigned long long>(k);
     if (A.consumed[s]) {  // taken by an earlier particle: the reference skips it
       if (lane == 0) {
         A.state[s] = DECIDED;
@@ -257,12 +277,23 @@ __global__ void process_kernel(Args A) {
   }
 }
 
-// between rounds: the slots of the round just processed are taken, the
-// ready / pending counts start again
-__global__ void round_start_kernel(unsigned long long* counters) {
+// between rounds: the round's slots are taken, the next pending list becomes
+// current, a round that still saw pending seeds is counted
+__global__ void round_end_kernel(unsigned long long* counters) {
+  counters[6] += counters[5] != 0;
   counters[4] += counters[1];
+  counters[3] = counters[2];
   counters[1] = 0;
   counters[2] = 0;
+  counters[5] = 0;
+}
+
+// the pending list starts as every candidate
+__global__ void __launch_bounds__(NT) list_init_kernel(unsigned long long* counters, int32_t* list) {
+  const int64_t m = static_cast<int64_t>(counters[0]);
+  for (int64_t k = static_cast<int64_t>(blockIdx.x) * NT + threadIdx.x; k < m; k += static_cast<int64_t>(gridDim.x) * NT)
+    list[k] = static_cast<int32_t>(k);
+  if (blockIdx.x == 0 && threadIdx.x == 0) counters[3] = counters[0];
 }
 
 // order: bucket particles by event, then rank by priority inside the event
@@ -357,6 +388,7 @@ struct Handle {
   int64_t np = 0;      // particles
   int64_t nslots = 0;  // particle slots written, holes (skipped seeds) included
   void* ws = nullptr;
+  int32_t* lists = nullptr;  // the two pending lists
   Args A;
   std::vector<int64_t> counts;
 };
@@ -413,29 +445,32 @@ int sk_reco_run(int64_t w, int64_t h, int nevents, const float* energy, const fl
   unsigned long long ncand = 0;
   SK_TRY(cudaMemcpyAsync(&ncand, &A.counters[0], 8, cudaMemcpyDeviceToHost, s));
   SK_TRY(cudaStreamSynchronize(s));
-  // particle slots: at most one per seed
-  e = cudaMallocAsync(reinterpret_cast<void**>(&A.slots), std::max<size_t>(1, ncand) * sizeof(reco::Slot), s);
-  if (e == cudaSuccess)
-    e = cudaMallocAsync(reinterpret_cast<void**>(&A.contrib), std::max<size_t>(1, ncand) * reco::MAXC * 8, s);
+  // particle slots (at most one per seed) and the two pending lists
+  const size_t nc1 = std::max<size_t>(1, ncand);
+  e = cudaMallocAsync(reinterpret_cast<void**>(&A.slots), nc1 * sizeof(reco::Slot), s);
+  if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&A.contrib), nc1 * reco::MAXC * 8, s);
+  if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&H->lists), nc1 * 8, s);
   if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync(particle slots)");
-  // ready: one warp per 32 candidates; process: one warp per ready seed
+  A.list[0] = H->lists;
+  A.list[1] = A.list[0] + nc1;
   const int rgrid = std::max(1, std::min<int>(ds->sm_count * 8, static_cast<int>((ncand + reco::NT - 1) / reco::NT)));
   const int cgrid =
       std::max(1, std::min<int>(ds->sm_count * 8, static_cast<int>((ncand + reco::NT / 32 - 1) / (reco::NT / 32))));
-  int r = 0;
-  unsigned long long pending = ncand;
-  while (pending) {
-    // rounds per host check: 8 first (full events converge in ~6), then 4
-    for (int k = 0; k < (r ? 4 : 8); ++k, ++r) {
-      reco::round_start_kernel<<<1, 1, 0, s>>>(A.counters);
-      reco::ready_kernel<<<rgrid, reco::NT, 0, s>>>(A);
+  reco::list_init_kernel<<<rgrid, reco::NT, 0, s>>>(A.counters, A.list[0]);
+  // rounds are queued without a host check in between (a round with nothing pending returns at once):
+  // 8 (full events converge in ~6), then 4 more at a time until the pending list is empty
+  int launched = 0;
+  for (unsigned long long left = ncand; left;) {
+    for (int k = 0; k < (launched ? 4 : 8); ++k, ++launched) {
+      reco::ready_kernel<<<rgrid, reco::NT, 0, s>>>(A, launched & 1);
       reco::process_kernel<<<cgrid, reco::NT, 0, s>>>(A);
+      reco::round_end_kernel<<<1, 1, 0, s>>>(A.counters);
     }
     SK_TRY(cudaGetLastError());
-    SK_TRY(cudaMemcpyAsync(&pending, &A.counters[2], 8, cudaMemcpyDeviceToHost, s));
+    SK_TRY(cudaMemcpyAsync(&left, &A.counters[3], 8, cudaMemcpyDeviceToHost, s));
     SK_TRY(cudaStreamSynchronize(s));
   }
-  unsigned long long cnt[5] = {0, 0, 0, 0, 0};
+  unsigned long long cnt[8] = {0};
   SK_TRY(cudaMemcpyAsync(cnt, A.counters, sizeof(cnt), cudaMemcpyDeviceToHost, s));
   H->counts.assign(nevents, 0);
   std::vector<unsigned long long> ec(nevents > 0 ? nevents : 1);
@@ -449,7 +484,7 @@ int sk_reco_run(int64_t w, int64_t h, int nevents, const float* energy, const fl
   H->np = np;
   H->nslots = static_cast<int64_t>(cnt[4] + cnt[1]);  // slots of every round, holes included
   *nparticles = H->np;
-  if (rounds) *rounds = r;
+  if (rounds) *rounds = static_cast<int>(cnt[6]);
   *handle = H;
   return SK_OK;
 }
@@ -518,6 +553,7 @@ int sk_reco_free(void* handle, uintptr_t stream) {
   if (H->A.slots) cudaFreeAsync(H->A.slots, s);
   if (H->A.contrib) cudaFreeAsync(H->A.contrib, s);
   if (H->ws) cudaFreeAsync(H->ws, s);
+  if (H->lists) cudaFreeAsync(H->lists, s);
   delete H;
   return SK_OK;
 }

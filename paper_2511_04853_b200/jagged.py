@@ -100,6 +100,16 @@ def _check_host_segments(lens, offsets, members: int) -> None:
                           f"source pool of {members} members")
 
 
+def _validate_on_device(lens_d: DeviceArray, off_d: DeviceArray, members: int, dev: int) -> int:
+    """Records whose segment is negative or leaves the pool (sk_jagged_validate), read back."""
+    ws = _workspace(dev)
+    nat.call("sk_jagged_validate", lens_d.n, lens_d.ptr, nat.TYPE_CODES[_NP_CODE[lens_d.dtype]], off_d.ptr, members,
+             ws.total.ptr + 8, nat.stream(dev))
+    nat.memcpy(ws.host_total.ptr, ws.total.ptr + 8, 8, dev)
+    nat.sync(dev)
+    return int(ws.host_total._data.view(np.int64)[0])
+
+
 def _invalid_segments(bad: int) -> BoundsError:
     return BoundsError(f"{bad} segment(s) have a negative length or lie outside the source pool")
 
@@ -122,7 +132,9 @@ def pack(coll, path: str, lens, src_offsets, src_pool, member_stride: int | None
     lay = coll.layout
     dev = lay.device if lay.device is not None else 0
     keep: list = []
-    lens_d = _as_device(lens, None if isinstance(lens, DeviceArray) else np.int64, dev, keep)
+    host_lens = None if isinstance(lens, DeviceArray) else np.asarray(lens)
+    keep_type = host_lens is None or (host_lens.dtype in _NP_CODE and host_lens.dtype.kind in "iu")
+    lens_d = _as_device(lens, None if keep_type else np.int64, dev, keep)
     if lens_d.n != n:
         raise BoundsError(f"expected {n} segment lengths, got {lens_d.n}")
     off_d = _as_device(src_offsets, np.int64, dev, keep)
@@ -137,12 +149,19 @@ def pack(coll, path: str, lens, src_offsets, src_pool, member_stride: int | None
         raise KindError(f"member_offsets must name exactly the leaves {[lf.dotted for lf in leaves]}")
     pool_bytes = src_pool.nbytes if isinstance(src_pool, DeviceArray) else np.asarray(src_pool).nbytes
     members = pool_bytes // int(member_stride) if member_stride else 0
-    if not isinstance(lens, DeviceArray) and not isinstance(src_offsets, DeviceArray):
-        _check_host_segments(lens, src_offsets, members)
-        checked = True
-    else:
-        checked = False
     pool_d = _as_device(src_pool, None, dev, keep)
+    checked = False
+    if not isinstance(lens, DeviceArray) and not isinstance(src_offsets, DeviceArray):
+        # host inputs were copied to the device above: validate them there before anything is written
+        # (one small kernel instead of a numpy pass over every record; the reference raises before it
+        # mutates, collection.py:546)
+        bad = _validate_on_device(lens_d, off_d, members, dev)
+        if bad:
+            for t in keep:
+                t.free()
+            _check_host_segments(lens, src_offsets, members)  # names the first offending record
+            raise _invalid_segments(bad)
+        checked = True
 
     pleaf = plan.leaf(path + ".prefix_sum")
     pcode = pleaf.value_type.storage_code
@@ -194,12 +213,7 @@ def pack(coll, path: str, lens, src_offsets, src_pool, member_stride: int | None
         # overflow: the pools must grow first -- redo as scan, resize, gather
 
     if not checked:  # device inputs on the scan + gather path: validate before anything is written
-        ws = _workspace(dev)
-        nat.call("sk_jagged_validate", n, lens_d.ptr, nat.TYPE_CODES[_NP_CODE[lens_d.dtype]], off_d.ptr, members,
-                 ws.total.ptr + 8, nat.stream(dev))
-        nat.memcpy(ws.host_total.ptr, ws.total.ptr + 8, 8, dev)
-        nat.sync(dev)
-        bad = int(ws.host_total._data.view(np.int64)[0])
+        bad = _validate_on_device(lens_d, off_d, members, dev)
         if bad:
             for t in keep:
                 t.free()

@@ -1,5 +1,3 @@
-mkdir -p gpurun_out
-timeout 900 python bench.py --steps 10 --warmup 3 > gpurun_out/bench_r02a.json 2> gpurun_out/bench_r02a.err; echo rc=$?
-tail -5 gpurun_out/bench_r02a.err
-timeout 600 python bench.py --impl reference --steps 5 --warmup 3 > gpurun_out/bench_ref_r02a.json 2>gpurun_out/bench_ref_r02a.err; echo rc=$?
-tail -3 gpurun_out/bench_ref_r02a.err
+timeout 600 python -m pytest tests/test_gpu_reco.py -x -q 2>&1 | tail -2
+timeout 300 python tools/time_reco.py
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -s 60 -c 60 python tools/time_reco.py 2>&1 | grep -E "^\s+[a-z_:<>0-9, ]+\(|gpu__time" | paste - - | awk '{print $1, $NF}' | head -36
