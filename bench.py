@@ -216,8 +216,13 @@ def run_ours(args) -> None:
     local_ms = evs[0].elapsed_ms(evs[-1]) / args.steps
     ms = max_over_ranks(local_ms)
     value = n_total * BYTES_PER_OBJECT / (ms / 1e3) / 1e9
+    mine = n * BYTES_PER_OBJECT / (statistics.mean(per_launch) / 1e3) / 1e9  # this rank's HBM GB/s
     launch_ms = max_over_ranks(statistics.mean(per_launch))
     achieved = n * BYTES_PER_OBJECT / (launch_ms / 1e3) / 1e9  # per GPU, slowest rank's launch time
+    per_rank = [mine]
+    if world > 1:
+        per_rank = [None] * world
+        dist.all_gather_object(per_rank, mine)
 
     # parity of the timed output at full scale (the run fails on any mismatch)
     parity = verify_obj8_shard(aos, soa, n, lo, dev, rank)
@@ -431,6 +436,7 @@ def run_ours(args) -> None:
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": traffic,
                      "kernel": "sk::conv::convert_kernel (word-mode AoS->planes, TMA bulk in/out)",
+                     "per_rank_frac": [round(x / peak, 4) for x in per_rank],
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (torch copy, read+write)" if peaks else
                                     "fallback 6650 GB/s (B200_PROFILING.md)"},
         "e2e": {"value": round(e2e_value, 2), "unit": UNIT, "h2d_bytes_per_step": m * 32 * world,

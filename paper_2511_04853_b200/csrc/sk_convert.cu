@@ -599,6 +599,17 @@ static int copy_side(const sk_conv_desc& orig, bool dst, int64_t r0, int64_t row
   return SK_OK;
 }
 
+// Peer-device sides (NVLink through peer access or a CUDA IPC mapping) use the same TMA bulk copies as
+// local HBM: cp.async.bulk takes any global address, and the copy engine of the SM pulls the remote
+// lines over NVLink. SK_PEER_BULK=0 falls back to cooperative 16-byte loads/stores for peer sides.
+static bool peer_bulk() {
+  static const bool on = [] {
+    const char* e = getenv("SK_PEER_BULK");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 constexpr int64_t CHUNK_TARGET = 32ll << 20;  // bytes of the larger side per pipeline chunk
 constexpr int NSLOT = 2;
 
@@ -619,7 +630,8 @@ int run(const sk_conv_desc& d, int device, cudaStream_t s, int epi, float* extra
   auto plan_and_launch = [&](const sk_conv_desc& dk, float* extra_k, cudaStream_t st) -> int {
     Plan P;
     int grid = 1;
-    int r = make_plan(dk, *ds, src_loc != LOC_PEER, dst_loc != LOC_PEER, epi, &P, &grid);
+    int r = make_plan(dk, *ds, src_loc != LOC_PEER || peer_bulk(), dst_loc != LOC_PEER || peer_bulk(), epi, &P,
+                      &grid);
     if (r) return r;
     if (epi == EPI_SENSOR) {
       for (int k = 0; k < 7; ++k) P.epi_seg[k] = P.f[epi_fields[k]].dloc;

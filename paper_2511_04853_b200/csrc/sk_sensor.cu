@@ -22,28 +22,46 @@ __device__ __forceinline__ float noise_of(float e, float na, float nb, bool nois
   return sensor_noise(e, na, nb, noisy);
 }
 
+// Both kernels stream their planes with 16-byte accesses, U vector groups per
+// thread per step with every load issued before any arithmetic, so each warp
+// keeps U * (bytes per group) in flight (a grid-stride loop that loads one
+// group at a time left noise at 0.85 of the copy peak with half the warps idle).
+constexpr int U = 4;
+
 __global__ void __launch_bounds__(NT) calibrate_kernel(int64_t n, const uint64_t* __restrict__ counts,
                                                        const float* __restrict__ a, const float* __restrict__ b,
                                                        float* __restrict__ energy, bool vec) {
   const int64_t stride = static_cast<int64_t>(gridDim.x) * NT;
-  int64_t i = static_cast<int64_t>(blockIdx.x) * NT + threadIdx.x;
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * NT + threadIdx.x;
+  int64_t tail = 0;
   if (vec) {
     const int64_t nv = n / VEC;
-    for (; i < nv; i += stride) {
-      const float4 av = reinterpret_cast<const float4*>(a)[i];
-      const float4 bv = reinterpret_cast<const float4*>(b)[i];
-      const ulonglong2 c0 = reinterpret_cast<const ulonglong2*>(counts)[2 * i];
-      const ulonglong2 c1 = reinterpret_cast<const ulonglong2*>(counts)[2 * i + 1];
-      float4 e;
-      e.x = calib(c0.x, av.x, bv.x);
-      e.y = calib(c0.y, av.y, bv.y);
-      e.z = calib(c1.x, av.z, bv.z);
-      e.w = calib(c1.y, av.w, bv.w);
-      reinterpret_cast<float4*>(energy)[i] = e;
+    for (int64_t i0 = t; i0 < nv; i0 += U * stride) {
+      float4 av[U], bv[U];
+      ulonglong2 c0[U], c1[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t i = min(i0 + u * stride, nv - 1);  // clamped: in range, dropped at the store
+        av[u] = __ldcs(reinterpret_cast<const float4*>(a) + i);
+        bv[u] = __ldcs(reinterpret_cast<const float4*>(b) + i);
+        c0[u] = __ldcs(reinterpret_cast<const ulonglong2*>(counts) + 2 * i);
+        c1[u] = __ldcs(reinterpret_cast<const ulonglong2*>(counts) + 2 * i + 1);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t i = i0 + u * stride;
+        if (i >= nv) break;
+        float4 e;
+        e.x = calib(c0[u].x, av[u].x, bv[u].x);
+        e.y = calib(c0[u].y, av[u].y, bv[u].y);
+        e.z = calib(c1[u].x, av[u].z, bv[u].z);
+        e.w = calib(c1[u].y, av[u].w, bv[u].w);
+        reinterpret_cast<float4*>(energy)[i] = e;
+      }
     }
-    i = nv * VEC + (static_cast<int64_t>(blockIdx.x) * NT + threadIdx.x);
+    tail = nv * VEC;
   }
-  for (; i < n; i += stride) energy[i] = calib(counts[i], a[i], b[i]);
+  for (int64_t i = tail + t; i < n; i += stride) energy[i] = calib(counts[i], a[i], b[i]);
 }
 
 __global__ void __launch_bounds__(NT) noise_kernel(int64_t n, const float* __restrict__ energy,
@@ -51,24 +69,36 @@ __global__ void __launch_bounds__(NT) noise_kernel(int64_t n, const float* __res
                                                    const uint8_t* __restrict__ noisy, float* __restrict__ noise,
                                                    bool vec) {
   const int64_t stride = static_cast<int64_t>(gridDim.x) * NT;
-  int64_t i = static_cast<int64_t>(blockIdx.x) * NT + threadIdx.x;
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * NT + threadIdx.x;
+  int64_t tail = 0;
   if (vec) {
     const int64_t nv = n / VEC;
-    for (; i < nv; i += stride) {
-      const float4 e = reinterpret_cast<const float4*>(energy)[i];
-      const float4 av = reinterpret_cast<const float4*>(na)[i];
-      const float4 bv = reinterpret_cast<const float4*>(nb)[i];
-      const uint32_t q = reinterpret_cast<const uint32_t*>(noisy)[i];
-      float4 o;
-      o.x = noise_of(e.x, av.x, bv.x, q & 0xff);
-      o.y = noise_of(e.y, av.y, bv.y, (q >> 8) & 0xff);
-      o.z = noise_of(e.z, av.z, bv.z, (q >> 16) & 0xff);
-      o.w = noise_of(e.w, av.w, bv.w, q >> 24);
-      reinterpret_cast<float4*>(noise)[i] = o;
+    for (int64_t i0 = t; i0 < nv; i0 += U * stride) {
+      float4 e[U], av[U], bv[U];
+      uint32_t q[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t i = min(i0 + u * stride, nv - 1);
+        e[u] = __ldcs(reinterpret_cast<const float4*>(energy) + i);
+        av[u] = __ldcs(reinterpret_cast<const float4*>(na) + i);
+        bv[u] = __ldcs(reinterpret_cast<const float4*>(nb) + i);
+        q[u] = __ldcs(reinterpret_cast<const unsigned int*>(noisy) + i);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t i = i0 + u * stride;
+        if (i >= nv) break;
+        float4 o;
+        o.x = noise_of(e[u].x, av[u].x, bv[u].x, q[u] & 0xff);
+        o.y = noise_of(e[u].y, av[u].y, bv[u].y, (q[u] >> 8) & 0xff);
+        o.z = noise_of(e[u].z, av[u].z, bv[u].z, (q[u] >> 16) & 0xff);
+        o.w = noise_of(e[u].w, av[u].w, bv[u].w, q[u] >> 24);
+        reinterpret_cast<float4*>(noise)[i] = o;
+      }
     }
-    i = nv * VEC + (static_cast<int64_t>(blockIdx.x) * NT + threadIdx.x);
+    tail = nv * VEC;
   }
-  for (; i < n; i += stride) noise[i] = noise_of(energy[i], na[i], nb[i], noisy[i] != 0);
+  for (int64_t i = tail + t; i < n; i += stride) noise[i] = noise_of(energy[i], na[i], nb[i], noisy[i] != 0);
 }
 
 // ---- on-device event generation (detector/events.py:37-133) --------------------------
@@ -156,14 +186,22 @@ __global__ void __launch_bounds__(NT) gen_deposits_kernel(const __grid_constant_
 
 static bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
-static int grid_for(int64_t n, int* grid) {
+// one resident wave: every CTA streams its share with U groups in flight per thread
+template <typename K>
+static int grid_for(K kernel, int64_t n, int* grid) {
   int dev = 0;
   SK_TRY(cudaGetDevice(&dev));
   DeviceState* ds = nullptr;
   int rc = device_state(dev, &ds);
   if (rc) return rc;
-  const int64_t want = (n / VEC + NT - 1) / NT;
-  *grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, static_cast<int64_t>(ds->sm_count) * 8)));
+  static int occ[64] = {0};
+  int& o = occ[dev & 63];
+  if (!o) {
+    SK_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kernel, NT, 0));
+    o = std::max(o, 1);
+  }
+  const int64_t want = (n / VEC + static_cast<int64_t>(NT) * U - 1) / (static_cast<int64_t>(NT) * U);
+  *grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, static_cast<int64_t>(ds->sm_count) * o)));
   return SK_OK;
 }
 
@@ -179,7 +217,7 @@ int sk_sensor_calibrate(int64_t n, const uint64_t* counts, const float* a, const
   if (n < 0) return set_error(SK_ERR_INVALID, "negative count");
   if (n == 0) return SK_OK;
   int grid = 1, dev = 0;
-  int rc = sensor::grid_for(n, &grid);
+  int rc = sensor::grid_for(sensor::calibrate_kernel, n, &grid);
   if (rc) return rc;
   SK_TRY(cudaGetDevice(&dev));
   const bool vec = sensor::al16(counts) && sensor::al16(a) && sensor::al16(b) && sensor::al16(energy);
@@ -193,7 +231,7 @@ int sk_sensor_noise(int64_t n, const float* energy, const float* na, const float
   if (n < 0) return set_error(SK_ERR_INVALID, "negative count");
   if (n == 0) return SK_OK;
   int grid = 1, dev = 0;
-  int rc = sensor::grid_for(n, &grid);
+  int rc = sensor::grid_for(sensor::noise_kernel, n, &grid);
   if (rc) return rc;
   SK_TRY(cudaGetDevice(&dev));
   const bool vec = sensor::al16(energy) && sensor::al16(na) && sensor::al16(nb) &&

@@ -62,3 +62,44 @@ def test_cross_process_layout_changing_pull():
         res = dict(results)
     assert res["spec"] == "b200-convert"
     assert res["equal"]
+
+
+def _two_gpus() -> bool:
+    from paper_2511_04853_b200 import _native as nat
+
+    return nat.device_count() >= 2
+
+
+@pytest.mark.skipif(not _two_gpus(), reason="needs two GPUs in one process (the gpurun box has one)")
+@pytest.mark.parametrize("direction", ["pull", "push"])
+def test_in_process_peer_conversion(direction):
+    """LOC_PEER inside one process: the AoS records live on cuda:1 and the planes on cuda:0 (pull: the
+    kernel on cuda:0 reads cuda:1's HBM over NVLink with TMA bulk copies), or the reverse (push: K2 on
+    cuda:0 writes AoS records into cuda:1). Checked byte-exact against the oracle."""
+    import paper_2511_04853_b200 as sk
+    from oracle import restate as R
+    from paper_2511_04853_b200 import layouts as ly, memctx as mc, transfer as tr, workloads as wl
+
+    n = 2_000_003
+    recs = wl.obj8_records(n, seed=8)
+    host = sk.Collection(wl.OBJ8_SCHEMA, ly.AOS, mc.ContextInfo.host())
+    host.resize(n)
+    host.layout._struct_buf._data[: n * 32] = recs.view(np.uint8)
+    if direction == "pull":
+        far = sk.Collection(wl.OBJ8_SCHEMA, ly.AOS, mc.ContextInfo.cuda(1))
+        tr.copy_collection(far, host)
+        near = sk.Collection(wl.OBJ8_SCHEMA, ly.PER_FIELD, mc.ContextInfo.cuda(0))
+        assert tr.copy_collection(near, far) == "b200-convert"
+        back = sk.Collection(wl.OBJ8_SCHEMA, ly.PER_FIELD, mc.ContextInfo.host())
+        tr.copy_collection(back, near)
+        want = R.aos_to_planes(recs)
+        for i in range(8):
+            assert back.column(f"f{i}").np.tobytes() == want[f"f{i}"][0].tobytes()
+    else:
+        planes = sk.Collection(wl.OBJ8_SCHEMA, ly.PER_FIELD, mc.ContextInfo.cuda(0))
+        tr.copy_collection(planes, host)
+        far = sk.Collection(wl.OBJ8_SCHEMA, ly.AOS, mc.ContextInfo.cuda(1))
+        assert tr.copy_collection(far, planes) == "b200-convert"
+        back = sk.Collection(wl.OBJ8_SCHEMA, ly.AOS, mc.ContextInfo.host())
+        tr.copy_collection(back, far)
+        assert np.array(back.layout._struct_buf._data[: n * 32]).tobytes() == recs.tobytes()
