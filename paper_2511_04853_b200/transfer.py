@@ -189,6 +189,7 @@ def _cached_desc(dl, sl, n):
 def _convert_execute(dst: Collection, src: Collection, opts: Mapping[str, Any] | None = None) -> None:
     _match_sizes(dst, src)
     sl, dl = src.layout, dst.layout
+    memctx.pin_for_transfer(*sl.buffers(), *dl.buffers())
     n = sl.size(MAIN_TAG)
     dev = _engine_device(dst, src)
     desc = _cached_desc(dl, sl, n)
