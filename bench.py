@@ -443,7 +443,8 @@ def run_ours(args) -> None:
         "objects_per_s": round(n_total / (ms / 1e3)),
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": traffic,
-                     "kernel": "sk::conv::convert_kernel (word-mode AoS->planes, TMA bulk in/out)",
+                     "kernel": "sk::conv::convert_kernel_t<GenericTransform> (word-mode AoS->planes, TMA bulk "
+                               "in/out); traffic from profiles/r02_obj8_a2p.ncu-rep scaled to this launch",
                      "per_rank_frac": [round(x / peak, 4) for x in per_rank],
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (torch copy, read+write)" if peaks else
                                     "fallback 6650 GB/s (B200_PROFILING.md)"},
@@ -603,10 +604,12 @@ def config2_api_paths(a2, p2, h2, noise, cells, dev, peak, queued, timed) -> dic
         "api_device_gbs": round(cells * 64 / ms_api_dev / 1e6, 1),
         "k5_calibrate": {"ms": round(ms_cal, 4), "gbs": round(cells * 20 / ms_cal / 1e6, 1),
                          "frac": round(cells * 20 / ms_cal / 1e6 / peak, 3),
-                         "bytes_per_cell": "20 (counts 8 + A 4 + B 4 read, energy 4 written)"},
+                         "bytes_per_cell": "20 (counts 8 + A 4 + B 4 read, energy 4 written)",
+                         "roofline": _cfg_roofline("config2_k5_calibrate", cells * 20, ms_cal, cells, peak)},
         "k5_noise": {"ms": round(ms_noise, 4), "gbs": round(cells * 17 / ms_noise / 1e6, 1),
                      "frac": round(cells * 17 / ms_noise / 1e6 / peak, 3),
-                     "bytes_per_cell": "17 (energy 4 + nA 4 + nB 4 + noisy 1 read, noise 4 written)"},
+                     "bytes_per_cell": "17 (energy 4 + nA 4 + nB 4 + noisy 1 read, noise 4 written)",
+                     "roofline": _cfg_roofline("config2_k5_noise", cells * 17, ms_noise, cells, peak)},
         "per_event_protocol": {
             "api_ms": round(ms_ev_api, 4), "fused_ms": round(ms_ev_fused, 4),
             "api_cells_per_s": round(ev / ms_ev_api * 1e3), "fused_cells_per_s": round(ev / ms_ev_fused * 1e3),
@@ -665,6 +668,23 @@ def verify_sensor_events(coll, noise, dev: int, events) -> str:
         if got_e.tobytes() != energy.tobytes() or got_n.tobytes() != want_noise.tobytes():
             raise SystemExit(f"config 2: event {e} energy/noise differ from the oracle")
     return f"events {list(events)}: energy and noise bit-exact vs the oracle (generate_event + calibrate + noise)"
+
+
+def _cfg_roofline(key: str, algo_bytes: float, ms: float, units: float, peak: float) -> dict:
+    """roofline object of one config: algorithmic bytes per launch / launch time against the measured HBM
+    peak, plus the DRAM bytes per launch ncu saw for this kernel (profiles/ncu_traffic.json, scaled to
+    `units` of the workload's unit)."""
+    achieved = algo_bytes / (ms / 1e3) / 1e9
+    out = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+           "frac": round(achieved / peak, 4), "traffic": None}
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            e = json.load(f)["entries"][key]
+        out["traffic"] = round(e["dram_bytes_per_unit"] * units)
+        out["traffic_capture"] = e["capture"]
+    except (OSError, KeyError, ValueError):
+        pass
+    return out
 
 
 def _traffic(n: int):
@@ -757,7 +777,8 @@ def run_extras(args, dev: int) -> dict:
                               "cold_l2_frac": round(n * 64 / ms_cold / 1e6 / peak, 3),
                               "pinned_h2d_e2e_ms": round(ms_h, 3), "e2e_gbs": round(n * 64 / ms_h / 1e6, 1),
                               "note": "device_ms repeats one 64 MB pair (L2-resident: 64 MB < 126 MB L2); "
-                                      "cold_l2 rotates 4 pairs (256 MB) so every launch reads and writes HBM"}
+                                      "cold_l2 rotates 4 pairs (256 MB) so every launch reads and writes HBM",
+                              "roofline": _cfg_roofline("config1_obj8_1M", n * 64, ms_cold, n, peak)}
     for a, p in sets:
         a.free()
         p.free()
@@ -784,6 +805,7 @@ def run_extras(args, dev: int) -> dict:
         "event_generation_ms": round(ms_gen, 3), "event_generation_cells_per_s": round(cells / ms_gen * 1e3),
         "data": "64 events 436x436, seeds 0..63, density 0.002, generated on-device (bit-exact with "
                 "detector/events.py:85-133)"}
+    out["config2_sensor_64x190096"]["roofline"] = _cfg_roofline("config2_sensor_fused", cells * 64, ms, cells, peak)
     out["config2_sensor_64x190096"]["parity"] = verify_sensor_events(p2, noise, dev, (0, 31, 63))
     out["config2_sensor_64x190096"].update(config2_api_paths(a2, p2, h2, noise, cells, dev, peak, queued, timed))
     out["config2_sensor_64x190096"]["parity_api_path"] = verify_sensor_events(p2, noise, dev, (5, 47))
@@ -862,7 +884,8 @@ def run_extras(args, dev: int) -> dict:
                 "api_ms: jagged.pack on a "
                 "Collection, incl. the host readback of the member total that sizes the pool; source segments "
                 "in shuffled order with slack, so ~125 MB of 32 B sectors are read for 92 MB of payload",
-        "parity": "whole prefix (1,000,001 x i32) and pool byte-exact vs oracle/restate.jagged_pack"}
+        "parity": "whole prefix (1,000,001 x i32) and pool byte-exact vs oracle/restate.jagged_pack",
+        "roofline": _cfg_roofline("config3_jagged_1M", algo, ms, 1, peak)}
     c3.free()
     for d in (d_lens, d_off, d_pool, prefix, scratch, total, pool_out):
         d.free()
@@ -877,6 +900,7 @@ def run_extras(args, dev: int) -> dict:
     ms = queued(lambda: sk.to_aosoa(a4, fields, 128, out=ao, sync=False), steps=10)
     out["config4_aosoa_100M"] = {"ms": round(ms, 3), "gbs": round(n4 * 76 / ms / 1e6, 1),
                                  "frac": round(n4 * 76 / ms / 1e6 / peak, 3), "objects_per_s": round(n4 / ms * 1e3)}
+    out["config4_aosoa_100M"]["roofline"] = _cfg_roofline("config4_aosoa_100M", n4 * 76, ms, n4, peak)
     out["config4_aosoa_100M"]["parity"] = verify_aosoa_tiles(ao, n4, fields, dev)
     ao.free()
     # the other tile widths SURVEY 8d names (T = 32, 64): same bytes per object

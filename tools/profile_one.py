@@ -1,6 +1,6 @@
 """Run one conversion job a few times (for ncu captures): python tools/profile_one.py JOB [reps]
 
-JOB in: obj8_a2p obj8_p2a sensor_fused sensor_a2p sensor_calnoise track_aosoa particle_a2p jagged
+JOB in: obj8_a2p obj8_p2a obj8_1m sensor_fused sensor_a2p sensor_calnoise track_aosoa particle_a2p jagged
 """
 
 import os
@@ -31,9 +31,10 @@ def coll(schema, kind, n):
 def job(name):
     n = 100_000_000
     if name.startswith("obj8"):
+        n = 1_000_000 if name == "obj8_1m" else n  # config 1
         a, p = coll(wl.OBJ8_SCHEMA, ly.AOS, n), coll(wl.OBJ8_SCHEMA, ly.PER_FIELD, n)
         wl.fill_random_device(a.layout._struct_buf.ptr, n * 32, 1, 0)
-        return (lambda: tr.copy_collection(p, a, {"async": True})) if name == "obj8_a2p" else \
+        return (lambda: tr.copy_collection(p, a, {"async": True})) if name != "obj8_p2a" else \
             (lambda: tr.copy_collection(a, p, {"async": True}))
     if name.startswith("sensor"):
         cells = 64 * 436 * 436
