@@ -555,6 +555,15 @@ def config2_api_paths(a2, p2, h2, noise, cells, dev, peak, queued, timed) -> dic
 
     ms_api = timed(api_batch, steps=3, warmup=1)
 
+    def api_fused():  # the same reference-API sequence with the fusion option: one HBM pass
+        tr.copy_collection(p2, h2, {"fuse": "sensor_funcs"})
+        with mc.execution_scope(mc.CUDA):
+            p2.funcs.calibrate_energy()
+            p2.funcs.get_noise()
+
+    ms_api_fused = timed(api_fused, steps=3, warmup=1)
+    ms_api_fused_dev = queued(lambda: tr.copy_collection(p2, a2, {"async": True, "fuse": "sensor_funcs"}), steps=10)
+
     def api_device():  # the same three steps on device-resident AoS records
         tr.copy_collection(p2, a2, {"async": True})
         sensor.calibrate_collection(p2, sync=False)
@@ -592,6 +601,14 @@ def config2_api_paths(a2, p2, h2, noise, cells, dev, peak, queued, timed) -> dic
         sensor.noise_for_collection(d1, n1)
 
     ms_ev_api = protocol(api_event)
+
+    def api_fused_event(e):
+        tr.copy_collection(d1, events[e], {"fuse": "sensor_funcs"})
+        with mc.execution_scope(mc.CUDA):
+            d1.funcs.calibrate_energy()
+            d1.funcs.get_noise()
+
+    ms_ev_api_fused = protocol(api_fused_event)
     ms_ev_fused = protocol(lambda e: sensor.transfer_calibrate(d1, events[e], n1))
     for c in events:
         c.free()
@@ -602,6 +619,9 @@ def config2_api_paths(a2, p2, h2, noise, cells, dev, peak, queued, timed) -> dic
         "api_pinned_e2e_cells_per_s": round(cells / ms_api * 1e3),
         "api_device_ms": round(ms_api_dev, 3),
         "api_device_gbs": round(cells * 64 / ms_api_dev / 1e6, 1),
+        "api_fused_option_pinned_e2e_ms": round(ms_api_fused, 3),
+        "api_fused_option_device_ms": round(ms_api_fused_dev, 3),
+        "api_fused_option_device_gbs": round(cells * 64 / ms_api_fused_dev / 1e6, 1),
         "k5_calibrate": {"ms": round(ms_cal, 4), "gbs": round(cells * 20 / ms_cal / 1e6, 1),
                          "frac": round(cells * 20 / ms_cal / 1e6 / peak, 3),
                          "bytes_per_cell": "20 (counts 8 + A 4 + B 4 read, energy 4 written)",
@@ -611,14 +631,17 @@ def config2_api_paths(a2, p2, h2, noise, cells, dev, peak, queued, timed) -> dic
                      "bytes_per_cell": "17 (energy 4 + nA 4 + nB 4 + noisy 1 read, noise 4 written)",
                      "roofline": _cfg_roofline("config2_k5_noise", cells * 17, ms_noise, cells, peak)},
         "per_event_protocol": {
-            "api_ms": round(ms_ev_api, 4), "fused_ms": round(ms_ev_fused, 4),
+            "api_ms": round(ms_ev_api, 4), "api_fused_option_ms": round(ms_ev_api_fused, 4),
+            "fused_ms": round(ms_ev_fused, 4),
             "api_cells_per_s": round(ev / ms_ev_api * 1e3), "fused_cells_per_s": round(ev / ms_ev_fused * 1e3),
             "note": "one 436x436 event per rep from pinned AoS: copy_collection + calibrate + noise (api) or "
                     "transfer_calibrate (fused), host-synchronous; mean of the 10 fastest of 50 reps cycling "
                     "10 events (bench.py:214-289)"},
         "api_note": "api_*: copy_collection(per_field@cuda, aos) + funcs.calibrate_energy() + funcs.get_noise(), "
                     "the reference's prepare phase (bench.py:174-178): one conversion launch plus the two K5 "
-                    "kernels, i.e. two more passes over the planes than the fused transfer_calibrate",
+                    "kernels, i.e. two more passes over the planes than the fused transfer_calibrate; "
+                    "api_fused_option_*: the same three calls with copy_collection(..., {'fuse': 'sensor_funcs'}), "
+                    "which runs the fused K1+K5 pass and leaves the behaviors nothing to do",
     }
 
 

@@ -191,11 +191,42 @@ def reconstruct_from_collection(sensors, width: int, height: int, out=None, even
     return out
 
 
+def fused_transfer(dst, src, opts=None) -> None:
+    """copy_collection(dst, src, {"fuse": "sensor_funcs"}): the AoS -> planes
+    conversion computes the calibrated energy and the noise in the same HBM
+    pass (K1+K5, transfer_calibrate). dst remembers the noise column for the
+    current content, so the reference's prepare sequence -- copy_collection,
+    funcs.calibrate_energy(), funcs.get_noise() (bench.py:174-178) -- costs
+    one pass: calibrate_energy() finds the energy already calibrated and
+    get_noise() returns the column (the same device array until dst's next
+    transfer; free() it and the next fused transfer allocates another). Any
+    change to dst (a size change, a transfer, a write through the API) bumps
+    its epoch and drops the markers."""
+    noise = getattr(dst, "_fused_noise", (None, None))[1]
+    if noise is None or not noise.buffer.live or noise.n != src.size():
+        if noise is not None:
+            noise.free()
+        noise = None
+    noise = transfer_calibrate(dst, src, noise, sync=not (opts or {}).get("async"))
+    dst._fused_noise = (dst._epoch + 1, noise)  # copy_collection bumps the epoch once more after us
+    dst._fused_calibrated = dst._epoch + 1
+
+
+def _fresh(coll, attr: str) -> bool:
+    mark = getattr(coll, attr, None)
+    stamp = mark[0] if isinstance(mark, tuple) else mark
+    return stamp is not None and stamp == coll._epoch
+
+
 def _calibrate_behavior(coll) -> None:
+    if _fresh(coll, "_fused_calibrated"):
+        return  # energy is a pure function of counts, A and B: the fused pass already wrote it
     calibrate_collection(coll)
 
 
 def _noise_behavior(coll) -> DeviceArray:
+    if _fresh(coll, "_fused_noise") and coll._fused_noise[1].buffer.live:
+        return coll._fused_noise[1]
     return noise_for_collection(coll)
 
 

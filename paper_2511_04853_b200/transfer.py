@@ -187,6 +187,16 @@ def _cached_desc(dl, sl, n):
 
 
 def _convert_execute(dst: Collection, src: Collection, opts: Mapping[str, Any] | None = None) -> None:
+    fuse = (opts or {}).get("fuse")
+    if fuse is not None:
+        # copy_collection(dst, src, {"fuse": "sensor_funcs"}): the conversion also runs the bundle's
+        # collection behaviors in the same pass (sensor.fused_transfer); unknown bundles are refused
+        from . import sensor
+
+        if fuse != "sensor_funcs":
+            raise TransferError(f"no fused conversion for behavior bundle {fuse!r}")
+        sensor.fused_transfer(dst, src, opts)
+        return
     _match_sizes(dst, src)
     sl, dl = src.layout, dst.layout
     memctx.pin_for_transfer(*sl.buffers(), *dl.buffers())

@@ -170,3 +170,28 @@ def test_fill_sensor_collection_and_object_behaviors(ctx):
         assert energy[i].tobytes() == want_e[i].tobytes()
         assert np.float32(noise_one[k]).tobytes() == want_n[i].tobytes()
     assert not energy[1:17].any()  # only the records asked for were calibrated
+
+
+def test_fused_option_through_copy_collection():
+    """copy_collection(dst, src, {"fuse": "sensor_funcs"}) + funcs.calibrate_energy() + funcs.get_noise():
+    the reference's prepare sequence in one HBM pass, same bytes as the separate path and the reference."""
+    g = golden("sensor_64x64_s3.npz")
+    n = int(g["w"] * g["h"])
+    host = aos_collection(sensor.SENSOR_SCHEMA, g["aos"], n, PINNED)
+    dev = sk.Collection(sensor.SENSOR_SCHEMA, ly.PER_FIELD, CUDA)
+    assert tr.copy_collection(dev, host, {"fuse": "sensor_funcs"}) == "b200-convert"
+    with mc.execution_scope(mc.CUDA):
+        dev.funcs.calibrate_energy()
+        noise = dev.funcs.get_noise()
+        assert noise is dev.funcs.get_noise()  # the fused column, no second kernel
+        energy = dev.column("energy").read()
+    assert energy.tobytes() == g["energy"].tobytes()
+    assert noise.numpy().tobytes() == g["noise"].tobytes()
+    # a later plain transfer drops the fused marker: the behaviors run their kernels again
+    tr.copy_collection(dev, host)
+    with mc.execution_scope(mc.CUDA):
+        assert not dev.column("energy").read().any()  # the AoS records carry energy 0
+        dev.funcs.calibrate_energy()
+        assert dev.column("energy").read().tobytes() == g["energy"].tobytes()
+    with pytest.raises(sk.TransferError):
+        tr.copy_collection(dev, host, {"fuse": "particle_funcs"})
