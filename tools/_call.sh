@@ -1,1 +1,3 @@
-timeout 900 python -m pytest tests/test_gpu_sensor.py tests/test_gpu_graphs.py tests/test_gpu_convert.py -x -q 2>&1 | tail -3
+for t in memcheck racecheck synccheck; do
+  timeout 1500 compute-sanitizer --tool $t python tools/sanitize_paths.py > gpurun_out/san_$t.log 2>&1; echo "$t rc=$?"; tail -2 gpurun_out/san_$t.log
+done

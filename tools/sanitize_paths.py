@@ -74,4 +74,24 @@ for m in (3, 1001):
         sk.from_aosoa(ao, tp)
         sk.from_aosoa(ao, ta)
         ao.free()
+# round 2: segment validation (fused and validate + scan + gather), batched device splices, K5 alone with
+# ragged tails, the device compare
+J._pack_raw(np.array([3, -1, 2, 0], np.int32), np.array([0, 0, 100, 1 << 40], np.int64), 5, [(0, 8)])
+J._pack_raw(np.array([3, 1, 2], np.int32), np.array([0, 4, 9], np.int64), 8, [(2, 2)], fused=False)
+with mc.execution_scope(mc.CUDA):
+    parts.insert_records(3, 5)
+    parts.erase_records(1, 4)
+    parts.resize(len(parts) + 37)
+    sensor.calibrate_collection(p)
+    sensor.noise_for_collection(p, noise)
+for m in (1, 7, 4099):
+    c = sk.Collection(sensor.SENSOR_SCHEMA, ly.PER_FIELD, CUDA)
+    sensor.generate_events(c, m, 1, range(1), 0.0)
+    sensor.calibrate_collection(c)
+    sensor.noise_for_collection(c)
+import ctypes  # noqa: E402
+from paper_2511_04853_b200 import _native as nat  # noqa: E402
+cnt = DeviceArray(1, np.uint64, CUDA)
+nat.call("sk_compare_bytes", a.layout._struct_buf.ptr, a.layout._struct_buf.ptr + 3, 1001, cnt.ptr, nat.stream(0))
+nat.sync(0)
 print("sanitize paths done", len(parts))
