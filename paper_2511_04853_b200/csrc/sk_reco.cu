@@ -198,18 +198,19 @@ __global__ void __launch_bounds__(NT) process_kernel(Args A) {
     const int64_t y = sy + lane / 5 - 2, x = sx + lane % 5 - 2;
     const bool inwin = lane < 25 && y >= 0 && y < A.h && x >= 0 && x < A.w;
     const int64_t f = base + y * A.w + x;
-    bool take = false;
-    float e32 = 0.0f, r32 = 0.0f;
-    int t = 0;
-    bool noisy = false;
-    if (inwin && !A.consumed[f]) {
-      r32 = A.ratio[f];
-      take = r32 > 2.0f;
-    }
-    if (take) {
-      e32 = A.energy[f];
-      t = A.type[f] & 3;
-      noisy = A.noisy[f] != 0;
+    // every load of the window cell at once (one memory round trip, not three dependent ones); values of
+    // cells that are not taken are discarded
+    const int64_t fc = inwin ? f : s;
+    const uint8_t used = A.consumed[fc];
+    float r32 = A.ratio[fc], e32 = A.energy[fc];
+    int t = A.type[fc] & 3;
+    bool noisy = A.noisy[fc] != 0;
+    const bool take = inwin && !used && r32 > 2.0f;
+    if (!take) {
+      r32 = 0.0f;
+      e32 = 0.0f;
+      t = 0;
+      noisy = false;
     }
     __syncwarp();  // every lane has read `consumed` before any marks it
     if (take) {
@@ -220,29 +221,37 @@ __global__ void __launch_bounds__(NT) process_kernel(Args A) {
     const int nc = __popc(mask);
     const double lx = static_cast<double>(x), ly = static_cast<double>(y);
     // reconstruct.py:84-117, same operation order (no FMA: -fmad=false)
+    // contributors only (set bits of the warp-uniform mask, ascending = row-major); the per-type sums
+    // are selected with constant indices so they stay in registers (a runtime index put them in local
+    // memory)
     double e64[4] = {0, 0, 0, 0}, sig64[4] = {0, 0, 0, 0};
     int cnt[4] = {0, 0, 0, 0};
     double sw = 0, swx = 0, swy = 0;
-    for (int i = 0; i < 25; ++i) {
+    for (unsigned m = mask; m; m &= m - 1) {
+      const int i = __ffs(m) - 1;
       const float ei = __shfl_sync(0xffffffffu, e32, i), ri = __shfl_sync(0xffffffffu, r32, i);
       const int ti = __shfl_sync(0xffffffffu, t, i);
       const int ni = __shfl_sync(0xffffffffu, static_cast<int>(noisy), i);
       const double xi = __shfl_sync(0xffffffffu, lx, i), yi = __shfl_sync(0xffffffffu, ly, i);
-      if (!((mask >> i) & 1u)) continue;
       const double e = static_cast<double>(ei);
-      e64[ti] = __dadd_rn(e64[ti], e);
-      sig64[ti] = __dadd_rn(sig64[ti], static_cast<double>(ri));
-      if (ni) ++cnt[ti];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if (ti == q) {
+          e64[q] = __dadd_rn(e64[q], e);
+          sig64[q] = __dadd_rn(sig64[q], static_cast<double>(ri));
+          cnt[q] += ni;
+        }
+      }
       sw = __dadd_rn(sw, e);
       swx = __dadd_rn(swx, __dmul_rn(e, xi));
       swy = __dadd_rn(swy, __dmul_rn(e, yi));
     }
     const double xbar = __ddiv_rn(swx, sw), ybar = __ddiv_rn(swy, sw);
     double vx = 0, vy = 0;
-    for (int i = 0; i < 25; ++i) {
+    for (unsigned m = mask; m; m &= m - 1) {
+      const int i = __ffs(m) - 1;
       const float ei = __shfl_sync(0xffffffffu, e32, i);
       const double xi = __shfl_sync(0xffffffffu, lx, i), yi = __shfl_sync(0xffffffffu, ly, i);
-      if (!((mask >> i) & 1u)) continue;
       const double e = static_cast<double>(ei);
       const double dx = __dsub_rn(xi, xbar), dy = __dsub_rn(yi, ybar);
       vx = __dadd_rn(vx, __dmul_rn(e, __dmul_rn(dx, dx)));
@@ -254,6 +263,7 @@ __global__ void __launch_bounds__(NT) process_kernel(Args A) {
     if (lane == 0) {
       Slot& S = A.slots[p];
       float c32[4];
+#pragma unroll
       for (int q = 0; q < 4; ++q) {
         c32[q] = __double2float_rn(e64[q]);
         S.ec[q] = c32[q];
