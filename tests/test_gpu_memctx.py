@@ -94,3 +94,44 @@ def test_migration_round_trip_keeps_contents():
     for info in (CUDA, PINNED, CUDA, HOST):
         c.update_memory_context_info(info)
     assert c.dump() == ref
+
+
+@pytest.mark.parametrize("nops", [1, 7, 300])
+def test_copy_rows_batched_moves_and_fills_vs_numpy(nops):
+    """memctx.copy_rows -> sk_move_batch_async: random self-overlapping moves and zero fills over many
+    buffers (300 ops crosses the 128-op batch), every move reading its source before any fill lands; the
+    same ops applied to host twins with numpy are the oracle."""
+    rng = np.random.default_rng(nops)
+    nbuf = min(nops, 40)
+    sizes = rng.integers(64, 200_000, nbuf)
+    dev = [mc.allocate(CUDA, int(n)) for n in sizes]
+    host = [mc.allocate(HOST, int(n)) for n in sizes]
+    for d, h in zip(dev, host):
+        h._data[:] = rng.integers(0, 256, h.length_bytes, dtype=np.uint8)
+        mc.memcopy_with_context(d, 0, h, 0, h.length_bytes)
+    # disjoint destinations per buffer: split each buffer into slices, one op per slice
+    ops_d, ops_h = [], []
+    per = max(1, nops // nbuf)
+    for b in range(nbuf):
+        cuts = np.sort(rng.choice(np.arange(1, sizes[b]), size=min(per * 2, sizes[b] - 1), replace=False))
+        edges = [0, *cuts.tolist(), int(sizes[b])]
+        for lo, hi in zip(edges[::2], edges[1::2]):
+            n = hi - lo
+            if n <= 0 or len(ops_d) >= nops:
+                continue
+            if rng.random() < 0.3:
+                ops_d.append(mc.RowOp(dev[b], lo, None, 0, n))
+                ops_h.append(mc.RowOp(host[b], lo, None, 0, n))
+            else:
+                src = int(rng.integers(0, sizes[b] - n + 1))  # may overlap its own destination
+                ops_d.append(mc.RowOp(dev[b], lo, dev[b], src, n))
+                ops_h.append(mc.RowOp(host[b], lo, host[b], src, n))
+    mc.copy_rows(ops_d)
+    mc.copy_rows(ops_h)
+    for d, h in zip(dev, host):
+        out = mc.allocate(HOST, d.length_bytes)
+        mc.memcopy_with_context(out, 0, d, 0, d.length_bytes)
+        assert np.array_equal(out._data, h._data)
+        mc.deallocate(out)
+    for buf in dev + host:
+        mc.deallocate(buf)

@@ -1,3 +1,4 @@
-timeout 600 python -m pytest tests/test_gpu_reco.py -x -q 2>&1 | tail -2
-SK_RECO_TRACE=1 timeout 300 python tools/time_reco.py 2>&1 | tail -1
-timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --cache-control none -s 60 -c 30 python tools/time_reco.py 2>&1 | grep -E "^\s+[a-z_:<>0-9, ]+\(|gpu__time" | paste - - | awk '{print $1, $NF}' | sed -n 9,22p
+timeout 600 python -m pytest tests/test_gpu_memctx.py -x -q 2>&1 | tail -2
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -2
+SK_BENCH_DEVICE=0 SK_BENCH_BACKEND=gloo timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29534 bench.py --gpus 4 --steps 3 --warmup 3 --objects 200000000 --e2e-objects 8000000 --no-extra > gpurun_out/bench_n4_sim.json 2> gpurun_out/bench_n4_sim.err; echo n4 rc=$?
+tail -c 600 gpurun_out/bench_n4_sim.json
