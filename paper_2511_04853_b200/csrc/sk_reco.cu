@@ -173,117 +173,139 @@ __global__ void __launch_bounds__(NT) ready_kernel(Args A, int parity) {
 }
 
 // phase 2 of a round: process the ready seeds (pairwise disjoint windows).
-// One warp per seed: lane l < 25 examines window cell (l / 5 - 2, l % 5 - 2),
-// so the cell loads run in parallel; lane 0 then adds the contributors up in
-// the reference's row-major order (reconstruct.py:84-117), fetching each by
-// shuffle, so every sum is bit-identical to the sequential walk.
-__global__ void __launch_bounds__(NT) process_kernel(Args A) {
-  const int lane = threadIdx.x & 31;
+// A warp takes 32 ready seeds at a time in two steps:
+//  1. for each of them in turn, lane l < 25 examines window cell
+//     (l / 5 - 2, l % 5 - 2): every load in one round trip, the taken cells
+//     marked consumed, the contributor list written, and the cell values kept
+//     in shared memory;
+//  2. lane j adds up seed j's contributors in the reference's row-major order
+//     (reconstruct.py:84-117), f64 and no FMA, so every sum is bit-identical to
+//     the sequential walk -- 32 particles' sums side by side instead of one
+//     warp replaying one particle's serial sums.
+constexpr int PNT = 128;             // process threads per CTA
+constexpr int PW = PNT / 32;         // warps per CTA
+constexpr unsigned SKIPPED = ~0u;    // window mask of a seed consumed before its turn
+
+struct WinSmem {
+  float e[32][25], r[32][25];
+  uint8_t t[32][25], nz[32][25];
+  unsigned mask[32];
+};
+
+__global__ void __launch_bounds__(PNT) process_kernel(Args A) {
+  __shared__ WinSmem W[PW];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  WinSmem& S = W[wid];
   const int64_t nready = static_cast<int64_t>(ctr(A, 1));
-  const int64_t nwarps = static_cast<int64_t>(gridDim.x) * (NT / 32);
-  for (int64_t k = static_cast<int64_t>(blockIdx.x) * (NT / 32) + (threadIdx.x >> 5); k < nready; k += nwarps) {
-    const int64_t s = A.ready[k];
-    // slot = this round's first slot + the ready index (no shared particle counter); a skipped seed leaves
-    // a hole that the ordering pass drops
-    const unsigned long long p = ctr(A, 4) + static_cast<unsigned long long>(k);
-    if (A.consumed[s]) {  // taken by an earlier particle: the reference skips it
-      if (lane == 0) {
-        A.state[s] = DECIDED;
-        A.slots[p].event = -1;
-      }
-      continue;
-    }
-    const int64_t ev = s / A.n, base = ev * A.n, loc = s - base;
-    const int64_t sy = loc / A.w, sx = loc - sy * A.w;
-    const int64_t y = sy + lane / 5 - 2, x = sx + lane % 5 - 2;
-    const bool inwin = lane < 25 && y >= 0 && y < A.h && x >= 0 && x < A.w;
-    const int64_t f = base + y * A.w + x;
-    // every load of the window cell at once (one memory round trip, not three dependent ones); values of
-    // cells that are not taken are discarded
-    const int64_t fc = inwin ? f : s;
-    const uint8_t used = A.consumed[fc];
-    float r32 = A.ratio[fc], e32 = A.energy[fc];
-    int t = A.type[fc] & 3;
-    bool noisy = A.noisy[fc] != 0;
-    const bool take = inwin && !used && r32 > 2.0f;
-    if (!take) {
-      r32 = 0.0f;
-      e32 = 0.0f;
-      t = 0;
-      noisy = false;
-    }
-    __syncwarp();  // every lane has read `consumed` before any marks it
-    if (take) {
-      A.consumed[f] = 1;
-      if (f != s && A.state[f] == PENDING) A.state[f] = DECIDED;  // a consumed seed is always skipped
-    }
-    const unsigned mask = __ballot_sync(0xffffffffu, take);
-    const int nc = __popc(mask);
-    const double lx = static_cast<double>(x), ly = static_cast<double>(y);
-    // reconstruct.py:84-117, same operation order (no FMA: -fmad=false)
-    // contributors only (set bits of the warp-uniform mask, ascending = row-major); the per-type sums
-    // are selected with constant indices so they stay in registers (a runtime index put them in local
-    // memory)
-    double e64[4] = {0, 0, 0, 0}, sig64[4] = {0, 0, 0, 0};
-    int cnt[4] = {0, 0, 0, 0};
-    double sw = 0, swx = 0, swy = 0;
-    for (unsigned m = mask; m; m &= m - 1) {
-      const int i = __ffs(m) - 1;
-      const float ei = __shfl_sync(0xffffffffu, e32, i), ri = __shfl_sync(0xffffffffu, r32, i);
-      const int ti = __shfl_sync(0xffffffffu, t, i);
-      const int ni = __shfl_sync(0xffffffffu, static_cast<int>(noisy), i);
-      const double xi = __shfl_sync(0xffffffffu, lx, i), yi = __shfl_sync(0xffffffffu, ly, i);
-      const double e = static_cast<double>(ei);
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        if (ti == q) {
-          e64[q] = __dadd_rn(e64[q], e);
-          sig64[q] = __dadd_rn(sig64[q], static_cast<double>(ri));
-          cnt[q] += ni;
+  const unsigned long long slot0 = ctr(A, 4);
+  // seeds per warp batch: spread over every warp of the grid (the window step is serial per warp)
+  const int64_t nwarps = static_cast<int64_t>(gridDim.x) * PW;
+  const int64_t per = max(static_cast<int64_t>(1), min(static_cast<int64_t>(32), (nready + nwarps - 1) / nwarps));
+  const int64_t stride = nwarps * per;
+  for (int64_t k0 = (static_cast<int64_t>(blockIdx.x) * PW + wid) * per; k0 < nready; k0 += stride) {
+    const int nb = static_cast<int>(min(per, nready - k0));
+    for (int j = 0; j < nb; ++j) {  // 1. windows, one seed at a time
+      const int64_t s = A.ready[k0 + j];
+      const unsigned long long p = slot0 + static_cast<unsigned long long>(k0 + j);
+      const int64_t base = (s / A.n) * A.n, loc = s - base;
+      const int64_t sy = loc / A.w, sx = loc - sy * A.w;
+      const int64_t y = sy + lane / 5 - 2, x = sx + lane % 5 - 2;
+      const bool inwin = lane < 25 && y >= 0 && y < A.h && x >= 0 && x < A.w;
+      const int64_t f = inwin ? base + y * A.w + x : s;
+      const uint8_t used = A.consumed[f];
+      const float r32 = A.ratio[f], e32 = A.energy[f];
+      const uint8_t t = A.type[f] & 3, nz = A.noisy[f] != 0;
+      // lane 12 is the seed itself (window centre): consumed by an earlier particle -> skipped
+      if (__shfl_sync(0xffffffffu, used, 12)) {
+        if (lane == 0) {
+          A.state[s] = DECIDED;
+          A.slots[p].event = -1;
+          S.mask[j] = SKIPPED;
         }
+        continue;
       }
-      sw = __dadd_rn(sw, e);
-      swx = __dadd_rn(swx, __dmul_rn(e, xi));
-      swy = __dadd_rn(swy, __dmul_rn(e, yi));
+      const bool take = inwin && !used && r32 > 2.0f;
+      __syncwarp();  // every lane has read `consumed` before any marks it
+      if (take) {
+        A.consumed[f] = 1;
+        if (f != s && A.state[f] == PENDING) A.state[f] = DECIDED;  // a consumed seed is always skipped
+      }
+      const unsigned mask = __ballot_sync(0xffffffffu, take);
+      if (take) {  // contributor list, row-major: rank of this lane among the taken ones
+        A.contrib[p * MAXC + __popc(mask & ((1u << lane) - 1u))] = static_cast<uint64_t>(f - base);
+      }
+      if (lane < 25) {
+        S.e[j][lane] = e32;
+        S.r[j][lane] = r32;
+        S.t[j][lane] = t;
+        S.nz[j][lane] = nz;
+      }
+      if (lane == 0) S.mask[j] = mask;
     }
-    const double xbar = __ddiv_rn(swx, sw), ybar = __ddiv_rn(swy, sw);
-    double vx = 0, vy = 0;
-    for (unsigned m = mask; m; m &= m - 1) {
-      const int i = __ffs(m) - 1;
-      const float ei = __shfl_sync(0xffffffffu, e32, i);
-      const double xi = __shfl_sync(0xffffffffu, lx, i), yi = __shfl_sync(0xffffffffu, ly, i);
-      const double e = static_cast<double>(ei);
-      const double dx = __dsub_rn(xi, xbar), dy = __dsub_rn(yi, ybar);
-      vx = __dadd_rn(vx, __dmul_rn(e, __dmul_rn(dx, dx)));
-      vy = __dadd_rn(vy, __dmul_rn(e, __dmul_rn(dy, dy)));
-    }
-    if (take) {  // contributor list, row-major: rank of this lane among the taken ones
-      A.contrib[p * MAXC + __popc(mask & ((1u << lane) - 1u))] = static_cast<uint64_t>(f - base);
-    }
-    if (lane == 0) {
-      Slot& S = A.slots[p];
+    __syncwarp();
+    // 2. sums, lane j for seed j
+    if (lane < nb && S.mask[lane] != SKIPPED) {
+      const int j = lane;
+      const int64_t s = A.ready[k0 + j];
+      const unsigned long long p = slot0 + static_cast<unsigned long long>(k0 + j);
+      const int64_t ev = s / A.n, loc = s - ev * A.n;
+      const int64_t sy = loc / A.w, sx = loc - sy * A.w;
+      const unsigned mask = S.mask[j];
+      double e64[4] = {0, 0, 0, 0}, sig64[4] = {0, 0, 0, 0};
+      int cnt[4] = {0, 0, 0, 0};
+      double sw = 0, swx = 0, swy = 0;
+      for (unsigned m = mask; m; m &= m - 1) {
+        const int i = __ffs(m) - 1;
+        const double e = static_cast<double>(S.e[j][i]);
+        const double ri = static_cast<double>(S.r[j][i]);
+        const int ti = S.t[j][i], ni = S.nz[j][i];
+        const double xi = static_cast<double>(sx + i % 5 - 2), yi = static_cast<double>(sy + i / 5 - 2);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          if (ti == q) {
+            e64[q] = __dadd_rn(e64[q], e);
+            sig64[q] = __dadd_rn(sig64[q], ri);
+            cnt[q] += ni;
+          }
+        }
+        sw = __dadd_rn(sw, e);
+        swx = __dadd_rn(swx, __dmul_rn(e, xi));
+        swy = __dadd_rn(swy, __dmul_rn(e, yi));
+      }
+      const double xbar = __ddiv_rn(swx, sw), ybar = __ddiv_rn(swy, sw);
+      double vx = 0, vy = 0;
+      for (unsigned m = mask; m; m &= m - 1) {
+        const int i = __ffs(m) - 1;
+        const double e = static_cast<double>(S.e[j][i]);
+        const double dx = __dsub_rn(static_cast<double>(sx + i % 5 - 2), xbar);
+        const double dy = __dsub_rn(static_cast<double>(sy + i / 5 - 2), ybar);
+        vx = __dadd_rn(vx, __dmul_rn(e, __dmul_rn(dx, dx)));
+        vy = __dadd_rn(vy, __dmul_rn(e, __dmul_rn(dy, dy)));
+      }
+      Slot& P = A.slots[p];
       float c32[4];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         c32[q] = __double2float_rn(e64[q]);
-        S.ec[q] = c32[q];
-        S.sig[q] = __double2float_rn(sig64[q]);
-        S.nc[q] = static_cast<uint8_t>(cnt[q]);
+        P.ec[q] = c32[q];
+        P.sig[q] = __double2float_rn(sig64[q]);
+        P.nc[q] = static_cast<uint8_t>(cnt[q]);
       }
-      S.energy = __double2float_rn(__dadd_rn(
+      P.energy = __double2float_rn(__dadd_rn(
           __dadd_rn(__dadd_rn(static_cast<double>(c32[0]), static_cast<double>(c32[1])), static_cast<double>(c32[2])),
           static_cast<double>(c32[3])));
-      S.x = __double2float_rn(xbar);
-      S.y = __double2float_rn(ybar);
-      S.xvar = __double2float_rn(__ddiv_rn(vx, sw));
-      S.yvar = __double2float_rn(__ddiv_rn(vy, sw));
-      S.nsens = nc;
-      S.event = static_cast<int32_t>(ev);
-      S.origin = loc;
-      S.key_e = A.energy[s];
+      P.x = __double2float_rn(xbar);
+      P.y = __double2float_rn(ybar);
+      P.xvar = __double2float_rn(__ddiv_rn(vx, sw));
+      P.yvar = __double2float_rn(__ddiv_rn(vy, sw));
+      P.nsens = __popc(mask);
+      P.event = static_cast<int32_t>(ev);
+      P.origin = loc;
+      P.key_e = A.energy[s];
       atomicAdd(&A.event_count[ev], 1ull);
       A.state[s] = DECIDED;
     }
+    __syncwarp();  // the window buffers are reused by the next batch
   }
 }
 
@@ -464,8 +486,9 @@ int sk_reco_run(int64_t w, int64_t h, int nevents, const float* energy, const fl
   A.list[0] = H->lists;
   A.list[1] = A.list[0] + nc1;
   const int rgrid = std::max(1, std::min<int>(ds->sm_count * 8, static_cast<int>((ncand + reco::NT - 1) / reco::NT)));
-  const int cgrid =
-      std::max(1, std::min<int>(ds->sm_count * 8, static_cast<int>((ncand + reco::NT / 32 - 1) / (reco::NT / 32))));
+  // process: one warp per 32 ready seeds
+  const int cgrid = std::max(1, std::min<int>(ds->sm_count * 8,
+                                              static_cast<int>((ncand + reco::PNT - 1) / reco::PNT)));
   reco::list_init_kernel<<<rgrid, reco::NT, 0, s>>>(A.counters, A.list[0]);
   // rounds are queued without a host check in between (a round with nothing pending returns at once):
   // 8 (full events converge in ~6), then 4 more at a time until the pending list is empty
@@ -473,7 +496,7 @@ int sk_reco_run(int64_t w, int64_t h, int nevents, const float* energy, const fl
   for (unsigned long long left = ncand; left;) {
     for (int k = 0; k < (launched ? 4 : 8); ++k, ++launched) {
       reco::ready_kernel<<<rgrid, reco::NT, 0, s>>>(A, launched & 1);
-      reco::process_kernel<<<cgrid, reco::NT, 0, s>>>(A);
+      reco::process_kernel<<<cgrid, reco::PNT, 0, s>>>(A);
       reco::round_end_kernel<<<1, 1, 0, s>>>(A.counters);
     }
     SK_TRY(cudaGetLastError());

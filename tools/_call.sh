@@ -1,3 +1,1 @@
-timeout 1500 python -m pytest tests -m gpu -q 2>&1 | tail -2
-timeout 900 python bench.py > gpurun_out/bench_r02_final.json 2> gpurun_out/bench_r02_final.err; echo bench rc=$?
-timeout 900 python bench.py --impl reference > gpurun_out/bench_ref_r02_final.json 2> gpurun_out/bench_ref_r02_final.err; echo ref rc=$?
+timeout 900 python -m pytest tests/test_gpu_reco.py tests/test_gpu_sensor.py -x -q 2>&1 | tail -2
