@@ -15,6 +15,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import struct
 
 import numpy as np
 
@@ -274,7 +275,112 @@ if not bh.is_registered("sensor_funcs"):
         bh.BehaviorFunction("get_noise", bh.TARGET_COLLECTION, _noise_behavior),
     ])
 
+PARTICLE_AOS_DTYPE = np.dtype([
+    ("energy", "<f4"), ("x", "<f4"), ("y", "<f4"), ("origin", "<u8"), ("x_variance", "<f4"),
+    ("y_variance", "<f4"), ("significance", "<f4", (4,)), ("E_contribution", "<f4", (4,)), ("noisy_count", "u1", (4,)),
+])
+
+
+def export_particles_from_collection(coll, stage=None) -> tuple[np.ndarray, list]:
+    """The external AoS form of a particle collection (detector/baselines.py:104-120):
+    the packed particle records (PARTICLE_AOS_DTYPE, baselines.py:37-49) and one
+    sensor-index array per particle. A device-resident collection is converted
+    to packed records on the B200 (K2) and comes back in one copy per buffer;
+    `stage` (a pinned AoS Particle collection) is reused across calls when given."""
+    from .collection import Collection
+    from .transfer import copy_collection
+
+    if stage is None:
+        stage = Collection(PARTICLE_SCHEMA, ly.AOS, memctx.ContextInfo.pinned())
+    copy_collection(stage, coll)
+    n = stage.size()
+    lay = stage.layout
+    recs = np.array(lay._struct_buf._data[: n * PARTICLE_AOS_DTYPE.itemsize].view(PARTICLE_AOS_DTYPE))
+    pool = np.array(lay._plane_view(stage.plan.leaf("sensors.value"), 0))
+    bounds = np.array(lay._plane_view(stage.plan.leaf("sensors.prefix_sum"), 0)).astype(np.int64)
+    return recs, (np.split(pool, bounds[1:-1]) if n else [])
+
+
 _EVENT_COLUMNS = ("type", "counts", "noisy", "parameter_A", "parameter_B", "noise_A", "noise_B")
+
+# SKEV event files (detector/events.py:27-29, 147-197): a 32-byte header, then the seven input columns
+# one after another -- already the per_field image, so loading is one copy per column
+_SKEV_MAGIC, _SKEV_VERSION = b"SKEV", 1
+_SKEV_HEADER = struct.Struct("<4sHHIIQd")
+_SKEV_DTYPES = (np.dtype("u1"), np.dtype("<u8"), np.dtype("u1"), np.dtype("<f4"), np.dtype("<f4"),
+                np.dtype("<f4"), np.dtype("<f4"))
+
+
+def _leaf_of(name: str) -> str:
+    return name if name in ("type", "counts") else "calibration_data." + name
+
+
+def load_events(paths, coll) -> list[tuple[int, int, int, float]]:
+    """Read SKEV event files into a Sensor collection, event-major, energy
+    zeroed (the reference's load_event + fill_sensor_collection per event,
+    events.py:165-197, reconstruct.py:142-154). Every file must hold the same
+    grid. The columns go straight into the planes: a host copy for host
+    collections, one host-to-device copy per column for device collections
+    (call it from execution_scope("cuda") for those). Returns each file's
+    (width, height, seed, density). Errors follow the reference: ValueError for
+    a truncated file, a wrong magic or version, or trailing bytes."""
+    from .collection import _write_plane
+
+    paths = [str(p) for p in paths]
+    raws, specs = [], []
+    for path in paths:
+        raw = np.fromfile(path, dtype=np.uint8)
+        if raw.size < _SKEV_HEADER.size:
+            raise ValueError(f"{path}: truncated event file")
+        magic, version, _, w, h, seed, density = _SKEV_HEADER.unpack_from(raw.tobytes()[: _SKEV_HEADER.size])
+        if magic != _SKEV_MAGIC:
+            raise ValueError(f"{path}: not an event file")
+        if version != _SKEV_VERSION:
+            raise ValueError(f"{path}: unsupported event file version {version}")
+        n = w * h
+        end = _SKEV_HEADER.size + n * sum(dt.itemsize for dt in _SKEV_DTYPES)
+        if end > raw.size:
+            raise ValueError(f"{path}: truncated event file")
+        if end != raw.size:
+            raise ValueError(f"{path}: trailing bytes after event data")
+        if specs and (w, h) != specs[0][:2]:
+            raise ValueError(f"{path}: grid {w}x{h} differs from {specs[0][0]}x{specs[0][1]}")
+        raws.append(raw)
+        specs.append((w, h, seed, density))
+    n = specs[0][0] * specs[0][1] if specs else 0
+    total = n * len(paths)
+    if coll.size() != total:
+        coll.clear()
+        coll.resize(total)
+    lay = coll.layout
+    lay.check_writable()
+    for e, raw in enumerate(raws):
+        off = _SKEV_HEADER.size
+        for name, dt in zip(_EVENT_COLUMNS, _SKEV_DTYPES):
+            col = raw[off : off + n * dt.itemsize].view(dt)
+            off += n * dt.itemsize
+            _write_plane(lay, coll.plan.leaf(_leaf_of(name)), 0, e * n, col)
+        _write_plane(lay, coll.plan.leaf("energy"), 0, e * n, np.zeros(n, np.float32))
+    coll._bump()
+    return specs
+
+
+def save_events(coll, paths, specs) -> None:
+    """Write each event of a Sensor collection (event-major, grids given by
+    specs = [(width, height, seed, density)]) as a SKEV file (events.py:147-162)."""
+    from .collection import _read_plane
+
+    lay = coll.layout
+    lay.check_readable()
+    first = 0
+    for path, (w, h, seed, density) in zip(paths, specs):
+        n = w * h
+        with open(path, "wb") as f:
+            f.write(_SKEV_HEADER.pack(_SKEV_MAGIC, _SKEV_VERSION, 0, w, h, seed, density))
+            for name, dt in zip(_EVENT_COLUMNS, _SKEV_DTYPES):
+                col = _read_plane(lay, coll.plan.leaf(_leaf_of(name)), 0, first, first + n)
+                f.write(np.ascontiguousarray(col).astype(dt).tobytes())
+        first += n
 
 
 def fill_sensor_collection(coll, event) -> None:

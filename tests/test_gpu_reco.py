@@ -82,3 +82,27 @@ def test_event_without_deposits_has_no_particles():
         dev.funcs.calibrate_energy()
     parts = sensor.reconstruct_from_collection(dev, 32, 32)
     assert len(parts) == 0 and parts.jagged_size("sensors") == 0
+
+
+@pytest.mark.parametrize("name", ["particles_64x64_s3.npz", "particles_160x120_s21.npz"])
+def test_export_particles_matches_reference_struct(name):
+    """export_particles_from_collection (detector/baselines.py:104-120): the GPU reconstruction's particles as
+    the reference's packed PARTICLE_AOS_DTYPE records + per-particle sensor lists, through K2 and one D2H."""
+    g = golden(name)
+    w, h = int(g["w"]), int(g["h"])
+    ev = R.generate_event(w, h, seed=int(g["seed"]), density=float(g["density"]))
+    cells = sk.Collection(sensor.SENSOR_SCHEMA, ly.PER_FIELD, CUDA)
+    sensor.generate_events(cells, w, h, [int(g["seed"])], float(g["density"]))
+    sensor.calibrate_collection(cells)
+    parts = sensor.reconstruct_from_collection(cells, w, h)
+    recs, sens = sensor.export_particles_from_collection(parts)
+    m = g["energy"].size
+    want = np.empty(m, sensor.PARTICLE_AOS_DTYPE)
+    for k in FIELDS + ARRAYS:
+        want[k] = g[k]
+    assert recs.dtype == sensor.PARTICLE_AOS_DTYPE and recs.tobytes() == want.tobytes()
+    cuts = np.concatenate([[0], np.cumsum(g["sensor_lens"].astype(np.int64))])
+    assert len(sens) == m
+    for i in range(m):
+        assert sens[i].tobytes() == g["sensors"][cuts[i]:cuts[i + 1]].tobytes()
+    del ev

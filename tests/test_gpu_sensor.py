@@ -195,3 +195,27 @@ def test_fused_option_through_copy_collection():
         assert dev.column("energy").read().tobytes() == g["energy"].tobytes()
     with pytest.raises(sk.TransferError):
         tr.copy_collection(dev, host, {"fuse": "particle_funcs"})
+
+
+def test_skev_files_into_a_device_collection(tmp_path):
+    """SKEV event files (the reference's format, events.py:147-197) loaded straight into device planes, then
+    the case-study kernel: same energies and noises as the oracle on the same events."""
+    specs = [(64, 64, 3, 0.01), (64, 64, 4, 0.01)]
+    host = sk.Collection(sensor.SENSOR_SCHEMA, ly.PER_FIELD, HOST)
+    paths = [tmp_path / f"{i}.skev" for i in range(2)]
+    gen = sk.Collection(sensor.SENSOR_SCHEMA, ly.PER_FIELD, CUDA)
+    sensor.generate_events(gen, 64, 64, [3, 4], 0.01)
+    tr.copy_collection(host, gen)
+    sensor.save_events(host, paths, specs)
+    dev = sk.Collection(sensor.SENSOR_SCHEMA, ly.PER_FIELD, CUDA)
+    with mc.execution_scope(mc.CUDA):
+        assert sensor.load_events(paths, dev) == specs
+        dev.funcs.calibrate_energy()
+        noise = dev.funcs.get_noise().numpy()
+        energy = dev.column("energy").read()
+    for i, seed in enumerate((3, 4)):
+        ev = R.generate_event(64, 64, seed=seed, density=0.01)
+        e = R.calibrate(ev["counts"], ev["parameter_A"], ev["parameter_B"])
+        sl = slice(i * 4096, (i + 1) * 4096)
+        assert energy[sl].tobytes() == e.tobytes()
+        assert noise[sl].tobytes() == R.noise(e, ev["noise_A"], ev["noise_B"], ev["noisy"]).tobytes()

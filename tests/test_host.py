@@ -284,3 +284,36 @@ def test_move_collection_copies_then_clears_source():
     assert tr.move_collection(dst, src) == "bulk-same-kind"
     assert dst.dump() == want
     assert src.size() == 0 and src.capacity() >= 6
+
+
+def test_skev_event_files_round_trip_with_the_reference(tmp_path):
+    """load_events / save_events speak the reference's SKEV format (events.py:147-197) both ways."""
+    from skhelp import import_soakit
+
+    soakit = import_soakit()
+    if soakit is None:
+        pytest.skip("soakit (the reference package) is not installed")
+    from soakit.detector import events as ev
+
+    specs = [ev.EventSpec(37, 11, 5, 0.01), ev.EventSpec(37, 11, 6, 0.02)]
+    paths = [tmp_path / f"e{i}.skev" for i in range(2)]
+    for sp, p in zip(specs, paths):
+        ev.save_event(ev.generate_event(sp), p)
+    coll = sk.Collection(sensor.SENSOR_SCHEMA, ly.PER_FIELD, mc.ContextInfo.host())
+    got = sensor.load_events(paths, coll)
+    assert got == [(37, 11, 5, 0.01), (37, 11, 6, 0.02)]
+    for i, (sp, p) in enumerate(zip(specs, paths)):
+        want = ev.load_event(p)
+        sl = slice(i * 407, (i + 1) * 407)
+        for name in ("type", "counts", "noisy", "parameter_A", "parameter_B", "noise_A", "noise_B"):
+            leaf = name if name in ("type", "counts") else "calibration_data." + name
+            assert coll.column(leaf).np[sl].tobytes() == getattr(want, name).tobytes(), name
+    assert not coll.column("energy").np.any()
+    out = [tmp_path / f"o{i}.skev" for i in range(2)]
+    sensor.save_events(coll, out, got)
+    for a, b in zip(paths, out):
+        assert a.read_bytes() == b.read_bytes()
+    bad = tmp_path / "bad.skev"
+    bad.write_bytes(paths[0].read_bytes() + b"x")
+    with pytest.raises(ValueError):
+        sensor.load_events([bad], coll)
