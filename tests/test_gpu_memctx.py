@@ -135,3 +135,26 @@ def test_copy_rows_batched_moves_and_fills_vs_numpy(nops):
         mc.deallocate(out)
     for buf in dev + host:
         mc.deallocate(buf)
+
+
+def test_large_pageable_buffers_are_pinned_once_and_released():
+    """memctx.pin_for_transfer: a >= 8 MB pageable host buffer taking part in a device copy is page-locked
+    once; deallocation (or garbage collection) unregisters it."""
+    import weakref
+
+    n = 16 << 20
+    host = mc.allocate(HOST, n)
+    host._data[:] = 7
+    dev = mc.allocate(CUDA, n)
+    mc.memcopy_with_context(dev, 0, host, 0, n)
+    assert isinstance(host._keep, weakref.finalize) and host._keep.alive
+    fin = host._keep
+    mc.memcopy_with_context(host, 0, dev, 0, n)  # reused, not registered twice
+    assert host._keep is fin
+    mc.deallocate(host)
+    assert not fin.alive
+    small = mc.allocate(HOST, 4096)
+    mc.memcopy_with_context(small, 0, dev, 0, 4096)
+    assert small._keep is None  # below the threshold: stays pageable
+    for b in (small, dev):
+        mc.deallocate(b)
