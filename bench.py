@@ -645,6 +645,48 @@ def config2_api_paths(a2, p2, h2, noise, cells, dev, peak, queued, timed) -> dic
     }
 
 
+def soakit_plugin_paths(a2, cells, dev, timed, noise_ref):
+    """Config 2's prepare phase through soakit itself (baseline/_ref) with the plugin installed: soakit's
+    copy_collection(per_field@cuda, aos@pinned) -> b200-convert, then soakit's coll.funcs.calibrate_energy() /
+    get_noise() (the reference's bench.py:174-178 with cuda for mockdev). None when soakit is absent."""
+    import numpy as np
+
+    from oracle import cpu_baseline
+    from paper_2511_04853_b200 import _native as nat
+
+    soakit = cpu_baseline.import_reference()
+    if soakit is None:
+        return None
+    from paper_2511_04853_b200 import soakit_plugin
+
+    soakit_plugin.install()
+    from soakit.detector import schemas as ds
+
+    host = soakit.Collection(ds.SENSOR_SCHEMA, "aos", soakit_plugin.pinned_info())
+    host.resize(cells)
+    nat.memcpy(host.layout._struct_buf._data.ctypes.data, a2.layout._struct_buf.ptr, cells * 30, dev)
+    nat.sync(dev)
+    devc = soakit.Collection(ds.SENSOR_SCHEMA, "per_field", soakit_plugin.cuda_info(dev))
+
+    def prepare():
+        soakit.transfer.copy_collection(devc, host)
+        with soakit.memctx.execution_scope("cuda"):
+            devc.funcs.calibrate_energy()
+            return devc.funcs.get_noise()
+
+    ms = timed(prepare, steps=3, warmup=1)
+    noise = prepare()
+    # the same events through this package's own route: both noises must be the same bytes
+    if np.asarray(noise).tobytes() != noise_ref.numpy().tobytes():
+        raise SystemExit("config 2 through soakit: noise differs from the package route")
+    return {"prepare_ms": round(ms, 3), "cells_per_s": round(cells / ms * 1e3),
+            "h2d_gbs": round(cells * 30 / ms / 1e6, 1), "parity": "noise byte-equal to the package route",
+            "note": "soakit 0.1.0 itself (baseline/_ref) + soakit_plugin.install(): copy_collection(per_field@cuda, "
+                    "aos@pinned) + funcs.calibrate_energy() + funcs.get_noise(), 64 events per call. get_noise() "
+                    "returns the reference's type, a fresh host numpy array, so each call also moves 49 MB of "
+                    "noise into pageable memory; the package route (api_pinned_e2e_ms) keeps it on the device"}
+
+
 def verify_aosoa_tiles(ao, n: int, fields, dev: int, seed: int = 4, samples: int = 32) -> str:
     """First, last and random AoSoA tiles vs oracle/restate.to_aosoa over the
     Track records restated from the splitmix image (seed 4, word 0)."""
@@ -832,6 +874,9 @@ def run_extras(args, dev: int) -> dict:
     out["config2_sensor_64x190096"]["parity"] = verify_sensor_events(p2, noise, dev, (0, 31, 63))
     out["config2_sensor_64x190096"].update(config2_api_paths(a2, p2, h2, noise, cells, dev, peak, queued, timed))
     out["config2_sensor_64x190096"]["parity_api_path"] = verify_sensor_events(p2, noise, dev, (5, 47))
+    sp = soakit_plugin_paths(a2, cells, dev, timed, noise)
+    if sp is not None:
+        out["config2_sensor_64x190096"]["through_soakit"] = sp
     # the reference's second phase on the same events: reconstruct + transfer back (bench.py:180-184)
     from paper_2511_04853_b200 import sensor as sn
 
