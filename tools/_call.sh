@@ -1,1 +1,1 @@
-timeout 900 python bench.py --steps 5 --warmup 3 --no-cpu > gpurun_out/bench_sp.json 2> gpurun_out/bench_sp.err; echo rc=$?; tail -3 gpurun_out/bench_sp.err
+timeout 300 python tools/reco_host.py 2>&1 | head -50
