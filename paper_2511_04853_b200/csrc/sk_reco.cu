@@ -60,7 +60,7 @@ struct Args {
   // [4] this round's first slot [5] pending seeds seen this round [6] rounds
   unsigned long long* counters;
   int64_t* ready;
-  int32_t* list[2];  // candidates (by index into cand) still pending: this round's and the next one's
+  int64_t* list[2];  // seeds (cell indices) still pending: this round's list and the next one's
   Slot* slots;
   uint64_t* contrib;  // MAXC per slot
   unsigned long long* event_count;
@@ -132,12 +132,12 @@ __device__ __forceinline__ unsigned long long ctr(const Args& A, int k) { return
 __global__ void __launch_bounds__(NT) ready_kernel(Args A, int parity) {
   const int lane = threadIdx.x & 31;
   const int64_t m = static_cast<int64_t>(ctr(A, 3));
-  const int32_t* cur = A.list[parity];
-  int32_t* nxt = A.list[parity ^ 1];
+  const int64_t* cur = A.list[parity];
+  int64_t* nxt = A.list[parity ^ 1];
   const int64_t stride = static_cast<int64_t>(gridDim.x) * NT;
   for (int64_t i0 = static_cast<int64_t>(blockIdx.x) * NT + (threadIdx.x & ~31); i0 < m; i0 += stride) {
     const int64_t i = i0 + lane;
-    const int64_t c = i < m ? A.cand[cur[i]] : 0;
+    const int64_t c = i < m ? cur[i] : 0;  // cells, not candidate indices: one dependent load less
     const bool pend = i < m && A.state[c] == PENDING;
     bool ok = pend;
     if (pend) {
@@ -168,7 +168,7 @@ __global__ void __launch_bounds__(NT) ready_kernel(Args A, int parity) {
     wb = __shfl_sync(0xffffffffu, wb, 0);
     const unsigned below = (1u << lane) - 1u;
     if (ok) A.ready[rb + __popc(rm & below)] = c;
-    if (wait) nxt[wb + __popc(wm & below)] = cur[i];
+    if (wait) nxt[wb + __popc(wm & below)] = c;
   }
 }
 
@@ -320,11 +320,12 @@ __global__ void round_end_kernel(unsigned long long* counters) {
   counters[5] = 0;
 }
 
-// the pending list starts as every candidate
-__global__ void __launch_bounds__(NT) list_init_kernel(unsigned long long* counters, int32_t* list) {
+// the pending list starts as every candidate (their cells)
+__global__ void __launch_bounds__(NT) list_init_kernel(unsigned long long* counters, const int64_t* cand,
+                                                       int64_t* list) {
   const int64_t m = static_cast<int64_t>(counters[0]);
   for (int64_t k = static_cast<int64_t>(blockIdx.x) * NT + threadIdx.x; k < m; k += static_cast<int64_t>(gridDim.x) * NT)
-    list[k] = static_cast<int32_t>(k);
+    list[k] = cand[k];
   if (blockIdx.x == 0 && threadIdx.x == 0) counters[3] = counters[0];
 }
 
@@ -420,7 +421,7 @@ struct Handle {
   int64_t np = 0;      // particles
   int64_t nslots = 0;  // particle slots written, holes (skipped seeds) included
   void* ws = nullptr;
-  int32_t* lists = nullptr;  // the two pending lists
+  int64_t* lists = nullptr;  // the two pending lists
   Args A;
   std::vector<int64_t> counts;
 };
@@ -481,7 +482,7 @@ int sk_reco_run(int64_t w, int64_t h, int nevents, const float* energy, const fl
   const size_t nc1 = std::max<size_t>(1, ncand);
   e = cudaMallocAsync(reinterpret_cast<void**>(&A.slots), nc1 * sizeof(reco::Slot), s);
   if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&A.contrib), nc1 * reco::MAXC * 8, s);
-  if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&H->lists), nc1 * 8, s);
+  if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&H->lists), nc1 * 16, s);
   if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync(particle slots)");
   A.list[0] = H->lists;
   A.list[1] = A.list[0] + nc1;
@@ -489,7 +490,7 @@ int sk_reco_run(int64_t w, int64_t h, int nevents, const float* energy, const fl
   // process: one warp per 32 ready seeds
   const int cgrid = std::max(1, std::min<int>(ds->sm_count * 8,
                                               static_cast<int>((ncand + reco::PNT - 1) / reco::PNT)));
-  reco::list_init_kernel<<<rgrid, reco::NT, 0, s>>>(A.counters, A.list[0]);
+  reco::list_init_kernel<<<rgrid, reco::NT, 0, s>>>(A.counters, A.cand, A.list[0]);
   // rounds are queued without a host check in between (a round with nothing pending returns at once):
   // 8 (full events converge in ~6), then 4 more at a time until the pending list is empty
   int launched = 0;
