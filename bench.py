@@ -404,6 +404,14 @@ def run_ours(args) -> None:
         if extra:
             # the reference's CPU path beside each extra config (one core, bounded samples)
             pc = cpu_baseline.per_config(budget_s=1.5)
+            for key, val in (cpu_baseline.reference_per_config(budget_s=1.5) or {}).items():
+                pc[key] = val  # configs 1-3 through soakit itself when baseline/_ref is present
+            if "config2_reconstruct" in pc and "config2_reconstruct_64_events" in extra:
+                r = pc["config2_reconstruct"]
+                extra["config2_reconstruct_64_events"]["cpu_reference_1core"] = {
+                    k: (round(v, 3) if isinstance(v, float) else v) for k, v in r.items()}
+                extra["config2_reconstruct_64_events"]["gpu_over_cpu_1core"] = round(
+                    extra["config2_reconstruct_64_events"]["events_per_s"] / r["events_per_s"], 1)
             pairs = {"config1_obj8_1M": ("config1_obj8", "device_gbs"),
                      "config2_sensor_64x190096": ("config2_sensor", "device_gbs"),
                      "config3_jagged_1M": ("config3_jagged", "gbs"),
@@ -411,8 +419,8 @@ def run_ours(args) -> None:
             for key, (ck, gkey) in pairs.items():
                 if key in extra and ck in pc:
                     c = pc[ck]
-                    extra[key]["cpu_port_1core"] = {k: (round(v, 3) if isinstance(v, float) else v)
-                                                    for k, v in c.items()}
+                    label = "cpu_reference_1core" if c.get("kind") == "reference" else "cpu_port_1core"
+                    extra[key][label] = {k: (round(v, 3) if isinstance(v, float) else v) for k, v in c.items()}
                     extra[key]["gpu_over_cpu_1core"] = round(extra[key][gkey] / c["gbs"], 1)
 
     if rank != 0:

@@ -263,3 +263,75 @@ def reference_multi_core(n: int, steps: int, warmup: int, procs: int | None = No
         for w in workers:
             w.join(timeout=60)
     return {"step_seconds": times, "procs": procs, "n": n, "kind": "reference"}
+
+
+def reference_per_config(budget_s: float = 2.0, seed: int = 3) -> dict | None:
+    """Configs 1-3 through soakit itself (baseline/_ref), one core, on bounded
+    samples, timed with the reference protocol:
+    1: copy_collection(per_field, aos) of 1M Obj8 on the host (per-leaf-default);
+    2: one 436x436 event: fill_sensor_collection into a host AoS collection
+       (untimed), copy_collection(per_field@mockdev, aos@host) +
+       calibrate_collection + noise_for_collection inside execution_scope("mockdev");
+    3: Collection.jagged_fill of 100K clusters from per-object segments.
+    Config 4 (AoSoA/cast) has no reference path: the port's figure stays.
+    None when soakit is absent."""
+    sk = import_reference()
+    if sk is None:
+        return None
+    from soakit.detector import events as ev
+    from soakit.detector import reconstruct as rc
+    from soakit.detector import schemas as ds
+
+    rng = np.random.default_rng(seed)
+    out = {}
+    n1 = 1_000_000
+    src, dst = _soakit_pair(sk, n1, seed)
+    t = _rate(lambda: sk.transfer.copy_collection(dst, src), budget_s)
+    out["config1_obj8"] = {"sample": f"{n1} objects, soakit copy_collection(per_field, aos)",
+                           "objects_per_s": n1 / t, "gbs": n1 * 64 / t / 1e9}
+
+    event = ev.generate_event(ev.EventSpec(436, 436, 0, 0.002))
+    host_pf = sk.Collection(ds.SENSOR_SCHEMA, "per_field")
+    rc.fill_sensor_collection(host_pf, event)
+    host = sk.Collection(ds.SENSOR_SCHEMA, "aos")
+    sk.transfer.copy_collection(host, host_pf)
+    cells = host.size()
+    sk.memctx.configure_mockdev(capacity_bytes=1 << 30)
+    dev = sk.Collection(ds.SENSOR_SCHEMA, "per_field", sk.memctx.ContextInfo.mockdev())
+
+    def case_study():
+        sk.transfer.copy_collection(dev, host)
+        with sk.memctx.execution_scope("mockdev"):
+            ds.calibrate_collection(dev)
+            ds.noise_for_collection(dev)
+
+    t = _rate(case_study, budget_s)
+    out["config2_sensor"] = {"sample": f"1 event, {cells} cells, soakit per-leaf AoS@host -> per_field@mockdev "
+                                       "+ calibrate + noise", "cells_per_s": cells / t, "gbs": cells * 64 / t / 1e9}
+
+    # the second phase of the case study (bench.py:180-184): reconstruct one calibrated event
+    with sk.memctx.execution_scope("mockdev"):
+        energy = dev.column("energy").read().copy()
+        noise = ds.noise_for_collection(dev)
+        stype = dev.column("type").read().copy()
+        noisy = dev.column("calibration_data.noisy").read().copy()
+    t = _rate(lambda: rc.reconstruct_arrays(energy, noise, stype, noisy, 436, 436), budget_s)
+    out["config2_reconstruct"] = {"sample": "1 event 436x436, soakit reconstruct_arrays",
+                                  "events_per_s": 1.0 / t, "ms_per_event": t * 1e3}
+
+    n3 = 100_000
+    lens = rng.integers(0, 21, n3)
+    pool = rng.integers(0, 1 << 62, int(lens.sum()), dtype=np.uint64)
+    cuts = np.concatenate([[0], np.cumsum(lens)])
+    order = rng.permutation(n3)
+    segments = [pool[cuts[i]:cuts[i + 1]] for i in order]  # per-object vectors in shuffled memory order
+    schema = sk.Schema("Cluster", (sk.declare_per_item("seed", sk.U64), sk.declare_jagged("members", sk.I32, sk.U64)))
+    coll = sk.Collection(schema, "per_field")
+    coll.resize(n3)
+    members = int(lens.sum())
+    t = _rate(lambda: coll.jagged_fill("members", segments), budget_s)
+    out["config3_jagged"] = {"sample": f"{n3} clusters, {members} members, soakit Collection.jagged_fill",
+                             "members_per_s": members / t, "gbs": (n3 * 16 + members * 16) / t / 1e9}
+    for v in out.values():
+        v["kind"] = "reference"
+    return out

@@ -1,3 +1,1 @@
-timeout 900 python -m pytest tests/test_gpu_reco.py -x -q 2>&1 | tail -2
-timeout 300 python tools/time_reco.py
-timeout 300 python tools/time_reco.py
+timeout 900 python bench.py --steps 5 --warmup 3 > gpurun_out/bench_rc.json 2> gpurun_out/bench_rc.err; echo rc=$?; tail -2 gpurun_out/bench_rc.err
