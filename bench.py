@@ -895,11 +895,18 @@ def run_extras(args, dev: int) -> dict:
     host_parts = sk.Collection(sensor.PARTICLE_SCHEMA, ly.PER_FIELD, mc.ContextInfo.pinned())
     ms_rt = timed(lambda: (sn.reconstruct_from_collection(p2, 436, 436, out=parts, events=64, noise=noise),
                            tr.copy_collection(host_parts, parts)), steps=3, warmup=1)
+    # ... and the reference's export of the result (bench.py:180-184 -> baselines.py:104-120): K2 into packed
+    # particle records on the device, one D2H per buffer, the records + per-particle sensor lists on the host
+    stage = sk.Collection(sensor.PARTICLE_SCHEMA, ly.AOS, mc.ContextInfo.pinned())
+    ms_ex = timed(lambda: (sn.reconstruct_from_collection(p2, 436, 436, out=parts, events=64, noise=noise),
+                           sn.export_particles_from_collection(parts, stage)), steps=3, warmup=1)
     out["config2_reconstruct_64_events"] = {
         "ms": round(ms_r, 3), "events_per_s": round(64 / ms_r * 1e3), "particles": len(parts),
         "rounds": parts.reco_rounds, "with_transfer_back_ms": round(ms_rt, 3),
-        "note": "round-synchronous parallel greedy, same particles/order as reconstruct_arrays"}
-    for c in (a2, p2, h2, gen, parts, host_parts):
+        "with_export_ms": round(ms_ex, 3),
+        "note": "round-synchronous parallel greedy, same particles/order as reconstruct_arrays; with_export: "
+                "+ export_particles_from_collection (PARTICLE_AOS_DTYPE records and sensor lists on the host)"}
+    for c in (a2, p2, h2, gen, parts, host_parts, stage):
         c.free()
     noise.free()
 
