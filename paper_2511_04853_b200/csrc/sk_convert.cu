@@ -210,8 +210,15 @@ int make_plan(const sk_conv_desc& d, const DeviceState& ds, bool in_bulk_ok, boo
   // the fused case study (30 B Sensor records -> planes + energy + noise) measured best at 40 KB tiles on real
   // events (tools/time_sensor.py: 123 us vs 128.5 us at 48 KB; 36 and 44 KB are worse -- the record-group
   // rounding of R matters more than the size)
-  const int tile_bytes = tun.tile_set ? tun.tile_bytes : d.nfields > 12 ? 32768 : epi == EPI_SENSOR ? 40960
-                                                                                                  : tun.tile_bytes;
+  // odd-stride packed records into planes (Sensor, 30 B: record groups of 2) measured best with 64 KB tiles,
+  // which the smem budget turns into one CTA per SM with 4 stages: 0.85 -> 0.93 of the copy peak
+  // (tools/time_paths.py, tools/time_sensor.py); the reverse direction and even strides lose with them
+  const bool odd_a2p = d.src_kind == SK_KIND_AOS && d.dst_kind == SK_KIND_PLANES && d.src_stride % 4 != 0;
+  const int tile_bytes = tun.tile_set           ? tun.tile_bytes
+                         : d.nfields > 12       ? 32768
+                         : epi == EPI_SENSOR    ? 40960
+                         : odd_a2p              ? 65536
+                                                : tun.tile_bytes;
   int64_t R = (static_cast<int64_t>(tile_bytes) * 1000 / rec_sum) / g * g;
   R = std::max<int64_t>(R, g);
   R = std::min<int64_t>(R, std::max<int64_t>(g, 4096));

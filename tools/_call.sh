@@ -1,1 +1,2 @@
-timeout 900 python bench.py --steps 5 --warmup 3 > gpurun_out/bench_rc.json 2> gpurun_out/bench_rc.err; echo rc=$?; tail -2 gpurun_out/bench_rc.err
+for t in 65536 81920 98304; do SK_TILE_BYTES=$t timeout 300 python tools/time_sensor.py | head -1; done
+for t in 16384 24576 40960; do SK_TILE_BYTES=$t timeout 300 python tools/time_paths.py 2>&1 | grep particle | sed "s/^/tile=$t /"; done

@@ -47,3 +47,24 @@ for rep in range(3):
     res.append(e0.elapsed_ms(e1) / 10)
 print(os.environ.get("SK_TILE_BYTES", "default"), os.environ.get("SK_CTAS", "-"),
       [round(x * 1e3, 1) for x in res], "us; GB/s", round(cells * 64 / min(res) / 1e6))
+
+
+def queued(fn, reps=10):
+    for _ in range(3):
+        fn()
+    nat.sync(0)
+    e0, e1 = nat.Event(), nat.Event()
+    nat.call("sk_fill_random", busy.ptr, busy.n, 1, 0, nat.stream(0))
+    e0.record(0)
+    for _ in range(reps):
+        fn()
+    e1.record(0)
+    nat.sync(0)
+    return e0.elapsed_ms(e1) / reps
+
+
+# the same real events through the plain conversion (no case-study epilogue), both directions
+for name, fn in (("a2p", lambda: tr.copy_collection(p, a, {"async": True})),
+                 ("p2a", lambda: tr.copy_collection(a, p, {"async": True}))):
+    ms = queued(fn)
+    print(f"plain {name}: {ms * 1e3:.1f} us, {cells * 60 / ms / 1e6:.0f} GB/s ({cells * 60 / ms / 1e6 / 6546.9:.3f})")
