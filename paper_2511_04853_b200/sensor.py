@@ -297,8 +297,8 @@ def export_particles_from_collection(coll, stage=None) -> tuple[np.ndarray, list
     lay = stage.layout
     recs = np.array(lay._struct_buf._data[: n * PARTICLE_AOS_DTYPE.itemsize].view(PARTICLE_AOS_DTYPE))
     pool = np.array(lay._plane_view(stage.plan.leaf("sensors.value"), 0))
-    bounds = np.array(lay._plane_view(stage.plan.leaf("sensors.prefix_sum"), 0)).astype(np.int64)
-    return recs, (np.split(pool, bounds[1:-1]) if n else [])
+    b = np.array(lay._plane_view(stage.plan.leaf("sensors.prefix_sum"), 0)).astype(np.int64).tolist()
+    return recs, [pool[b[i]:b[i + 1]] for i in range(n)]  # views of one pool (np.split is slower)
 
 
 _EVENT_COLUMNS = ("type", "counts", "noisy", "parameter_A", "parameter_B", "noise_A", "noise_B")
