@@ -422,6 +422,10 @@ def run_ours(args) -> None:
                     label = "cpu_reference_1core" if c.get("kind") == "reference" else "cpu_port_1core"
                     extra[key][label] = {k: (round(v, 3) if isinstance(v, float) else v) for k, v in c.items()}
                     extra[key]["gpu_over_cpu_1core"] = round(extra[key][gkey] / c["gbs"], 1)
+            if "config3_jagged_1M" in extra and pc.get("config3_jagged", {}).get("kind") == "reference":
+                jf = extra["config3_jagged_1M"]["jagged_fill"]  # the same call on both sides
+                jf["over_reference_jagged_fill_1core"] = round(
+                    jf["members_per_s"] / pc["config3_jagged"]["members_per_s"], 1)
 
     if rank != 0:
         if world > 1:
@@ -932,6 +936,13 @@ def run_extras(args, dev: int) -> dict:
     ms_pageable = timed(lambda: jagged.pack(c3, "members", lens, offsets, pool), steps=3, warmup=1)
     for b, _ in pinned_in:
         mc.deallocate(b)
+    # the reference's own API: Collection.jagged_fill(path, segments) with one numpy vector per record
+    # (collection.py:537-556), the vectors being views into the shuffled source pool
+    segments = [pool[o:o + k] for o, k in zip(offsets.tolist(), lens.tolist())]
+    ms_fill = timed(lambda: c3.jagged_fill("members", segments), steps=5, warmup=2)
+    with mc.execution_scope(mc.CUDA):
+        fill_p, fill_m = c3.prefix_sums("members"), c3.column("members").read()
+    del segments
     # the same fused pack through the C-ABI (scan + gather, no host readback), device time
     import ctypes as C
 
@@ -954,10 +965,18 @@ def run_extras(args, dev: int) -> dict:
     want_p, want_m = restate.jagged_pack(lens, offsets, pool, np.int32)
     if prefix.numpy().tobytes() != want_p.tobytes() or pool_out.numpy()[:members].tobytes() != want_m.tobytes():
         raise SystemExit("config 3: packed prefix/pool differ from the oracle")
+    if np.asarray(fill_p).tobytes() != want_p.tobytes() or np.asarray(fill_m).tobytes() != want_m.tobytes():
+        raise SystemExit("config 3: jagged_fill prefix/pool differ from the oracle")
     out["config3_jagged_1M"] = {
         "members": members, "device_ms": round(ms, 4), "members_per_s": round(members / ms * 1e3),
         "gbs": round(algo / ms / 1e6, 1), "frac": round(algo / ms / 1e6 / peak, 3),
         "api_ms": round(ms_api, 4),
+        "jagged_fill": {"ms": round(ms_fill, 3), "members_per_s": round(members / ms_fill * 1e3),
+                        "gbs": round(algo / ms_fill / 1e6, 2),
+                        "note": "Collection.jagged_fill('members', segments), segments = 1M numpy views into the "
+                                "shuffled host pool (the reference's call, collection.py:537-556): threaded C "
+                                "packing into pinned staging, one H2D, the fused pack; prefix and pool checked "
+                                "byte-exact vs the oracle"},
         "host_input_e2e": {"pinned_ms": round(ms_pinned, 3), "pageable_ms": round(ms_pageable, 3),
                            "h2d_bytes": int(lens.nbytes + offsets.nbytes + pool.nbytes),
                            "note": "jagged.pack(collection, lens, offsets, pool) with numpy inputs in pinned / "

@@ -16,7 +16,10 @@ host-resident collections are staged through device temporaries.
 
 from __future__ import annotations
 
+import contextlib
 import ctypes as C
+import os
+import threading
 from typing import Mapping
 
 import numpy as np
@@ -61,6 +64,49 @@ class _Workspace:
 
 
 _workspaces: dict[int, _Workspace] = {}
+
+# jagged_fill stages its packed segments here (pinned, so the H2D runs at link speed);
+# larger fills use a one-off pageable buffer instead of pinning that much for good
+FILL_STAGING_BYTES = int(os.environ.get("SOAKIT_FILL_STAGING_BYTES", str(1 << 30)))
+
+
+class _FillStaging:
+    """One grow-only pinned host area per device for Collection.jagged_fill.
+    A fill holds it from packing until its H2D copies have landed (pack() syncs
+    before it returns); a concurrent fill on the same device that finds it
+    busy packs into pageable memory instead of waiting."""
+
+    def __init__(self) -> None:
+        self.lock = threading.Lock()
+        self.buf = None
+
+    def alloc(self, nbytes: int):
+        if nbytes > FILL_STAGING_BYTES:
+            return bytearray(nbytes)
+        have = self.buf.length_bytes if self.buf is not None else 0
+        if have < nbytes:
+            if self.buf is not None:
+                memctx.deallocate(self.buf)
+                self.buf = None
+            self.buf = memctx.allocate(memctx.ContextInfo.pinned(), max(nbytes, 2 * have, 1 << 20))
+        return np.frombuffer(self.buf._data, np.uint8, nbytes)
+
+
+_fill_staging: dict[int, _FillStaging] = {}
+
+
+@contextlib.contextmanager
+def fill_staging(dev: int):
+    """Yield an alloc(nbytes) callable for _segpack.pack_segments, or None when
+    this device's staging area is in use by another thread."""
+    st = _fill_staging.setdefault(dev, _FillStaging())
+    if not st.lock.acquire(blocking=False):
+        yield None
+        return
+    try:
+        yield st.alloc
+    finally:
+        st.lock.release()
 
 
 def _workspace(dev: int) -> _Workspace:

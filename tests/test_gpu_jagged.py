@@ -30,7 +30,8 @@ def _read(coll, path):
 
 @pytest.mark.parametrize("label", list(ITYPES))
 @pytest.mark.parametrize("ctx", ["cuda", "host"])
-def test_jagged_fill_matches_reference(label, ctx):
+@pytest.mark.parametrize("form", ["arrays", "lists"])  # arrays take _segpack, lists the np.asarray path
+def test_jagged_fill_matches_reference(label, ctx, form):
     g = golden("jagged.npz")
     lens = g[f"{label}:lens"]
     pool = g[f"{label}:pool_in"]
@@ -40,7 +41,8 @@ def test_jagged_fill_matches_reference(label, ctx):
     with mc.execution_scope(mc.CUDA if ctx == "cuda" else mc.HOST):
         c.resize(n)
         cuts = np.concatenate([[0], np.cumsum(lens.astype(np.int64))])
-        c.jagged_fill("members", [pool[cuts[i]:cuts[i + 1]] for i in range(n)])
+        segs = [pool[cuts[i]:cuts[i + 1]] for i in range(n)]
+        c.jagged_fill("members", segs if form == "arrays" else [s.tolist() for s in segs])
     if ctx == "cuda":
         p, m = _read(c, "members")
     else:
