@@ -266,8 +266,9 @@ int sk_sensor_generate(int64_t w, int64_t h, const uint64_t* seeds, int nevents,
 
 /* Particle reconstruction (reconstruct_arrays, detector/reconstruct.py:53-136)
    over nevents calibrated events of w x h cells (energy/noise/type/noisy
-   planes, event-major). Round-synchronous parallel greedy: same particles in
-   the same order as the reference's sequential seed walk. Returns an opaque
+   planes, event-major). Round-synchronous parallel greedy over the seeds'
+   blocker lists: same particles in the same order as the reference's
+   sequential seed walk. Returns an opaque
    handle with the particles and per-event counts; sk_reco_write then writes
    them in reference order into per-field planes (slot planes of the 4-wide
    arrays as separate pointers), the per-particle contributor counts and
@@ -277,6 +278,8 @@ int sk_reco_run(int64_t w, int64_t h, int nevents, const float* energy,
                 const float* noise, const uint8_t* type, const uint8_t* noisy,
                 int device, uintptr_t stream, void** handle, int64_t* nparticles,
                 int* rounds);
+/* Particles and contributor cells (the total of the per-particle sensor lists) of a run. */
+int sk_reco_sizes(void* handle, int64_t* nparticles, int64_t* ncontributors);
 int sk_reco_event_counts(void* handle, int64_t* counts);
 int sk_reco_write(void* handle, float* energy, float* x, float* y, uint64_t* origin,
                   float* x_variance, float* y_variance, float* const* significance,

@@ -113,6 +113,7 @@ _SIGNATURES = {
     "sk_sensor_generate": [_I64, _I64, C.POINTER(C.c_uint64), _I, _I64, C.POINTER(C.c_double), _P, _P, _P, _P, _P,
                            _P, _P, _P, _U],
     "sk_reco_run": [_I64, _I64, _I, _P, _P, _P, _P, _I, _U, C.POINTER(_P), C.POINTER(_I64), C.POINTER(_I)],
+    "sk_reco_sizes": [_P, C.POINTER(_I64), C.POINTER(_I64)],
     "sk_reco_event_counts": [_P, C.POINTER(_I64)],
     "sk_reco_write": [_P, _P, _P, _P, _P, _P, _P, C.POINTER(_P), C.POINTER(_P), C.POINTER(_P), _P, _P,
                       C.POINTER(_P), _U],

@@ -4,21 +4,36 @@
 // (ratio > 5) in descending energy / ascending index; an unconsumed seed takes
 // the unconsumed ratio > 2 cells of its grid-clipped 5x5 window. The walk is
 // sequential, but two seeds interact only when their windows overlap
-// (Chebyshev distance <= 4). Round-synchronous parallel greedy reproduces it
-// exactly: in a round, a pending seed is READY when no pending seed of higher
-// priority lies within distance 4; ready seeds have pairwise disjoint windows
-// and every seed that could have affected them is already decided, so they are
-// processed concurrently with the same outcome as the sequential walk. A seed
-// consumed by another is decided (skipped) at once. Per-particle sums run in
-// one thread in the reference's order (f64, row-major contributors), so the
-// attributes are bit-identical; particles are finally ordered by priority.
-// The one approximation: the reference squares deviations with Python's
-// `x ** 2` (glibc pow) and this kernel with x * x; they differ by <= 1 ulp of
-// a double in ~0.1% of cases, which reaches the float32 variance only when the
-// double lies within 1e-16 of an f32 rounding boundary.
+// (Chebyshev distance <= 4). So the walk is a dependency graph: a seed's
+// BLOCKERS are the candidates of higher priority within distance 4, and a
+// seed may be processed as soon as every blocker is decided (processed, or
+// consumed by another particle) -- with exactly the sequential walk's outcome,
+// because every seed that could touch its window is then final and no seed of
+// lower priority can touch it first (it would have this seed as a blocker).
+//
+//  1. tile_kernel: one CTA per 32x32 cell tile of an event stages energy and
+//     noise of the tile plus a 4-cell halo in shared memory, marks the
+//     candidates and writes each one's blocker list (offsets inside its 9x9
+//     neighbourhood) -- the only 81-cell scan of the whole run.
+//  2. pass_kernel, repeated: over the candidates still pending, one thread per
+//     candidate walks its blocker list from where the last pass stopped; a
+//     candidate whose blockers are all decided is processed by its warp right
+//     away (window, contributors, sums), one that still waits goes to the next
+//     pass's list. Processing publishes its cell flags with release ordering
+//     and readers check them with acquire ordering, so a pass also resolves
+//     chains whose blockers finish earlier in the same launch.
+//
+// Per-particle sums run in one thread in the reference's order (f64, no FMA,
+// row-major contributors), so the attributes are bit-identical; particles are
+// finally ordered by priority per event. The one approximation: the reference
+// squares deviations with Python's `x ** 2` (glibc pow) and this kernel with
+// x * x; profiles/r02_pow_check.md shows no f32 variance of the benchmark
+// events differs.
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <mutex>
+#include <string>
 #include <vector>
 
 #include "sk_internal.cuh"
@@ -30,20 +45,35 @@ namespace reco {
 constexpr int NT = 256;
 constexpr int MAXC = 25;  // contributors per particle (5x5 window)
 
-enum : uint8_t { NONE = 0, PENDING = 1, DECIDED = 2 };
+// per-cell flags
+constexpr uint8_t PENDING = 1;   // a candidate not decided yet
+constexpr uint8_t CONSUMED = 2;  // taken by a particle (a consumed candidate is decided)
 
-__device__ __forceinline__ int64_t imax64(int64_t a, int64_t b) { return a > b ? a : b; }
-__device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
+constexpr int KB = 48;                 // blocker offsets kept per candidate
+constexpr uint32_t OVERFLOW = ~0u;     // more blockers than KB: the pass scans the 9x9 neighbourhood instead
+
+struct Cand {          // 64 B
+  int64_t cell;        // cell index (event-major)
+  uint32_t n;          // blockers, or OVERFLOW
+  uint32_t cur;        // blockers [0, cur) are known to be decided
+  uint8_t off[KB];     // (dy + 4) * 9 + (dx + 4), row-major
+};
+static_assert(sizeof(Cand) == 64, "Cand is one 64-byte record");
 
 struct Slot {  // one reconstructed particle, before ordering
   float energy, x, y, xvar, yvar;
   float sig[4], ec[4];
   uint8_t nc[4];
   int32_t nsens;
-  int32_t event;
+  int32_t event;   // -1: a seed found consumed at its turn (a hole)
   int64_t origin;  // seed flat index inside its event
   float key_e;     // priority: energy desc, then origin asc
 };
+
+// [0] candidates [1] ready seeds of this round [2] next round's list size [3] this round's list size
+// [4] slots taken [5] CTAs finished in the current kernel [6] rounds that saw work [7] contributors
+constexpr int C_NCAND = 0, C_READY = 1, C_NEXT = 2, C_CUR = 3, C_SLOTS = 4, C_DONE = 5, C_PASSES = 6,
+              C_CONTRIB = 7;
 
 struct Args {
   int64_t w, h, n;  // n = cells per event
@@ -52,284 +82,477 @@ struct Args {
   const float* noise;
   const uint8_t* type;
   const uint8_t* noisy;
-  float* ratio;
-  uint8_t* state;
-  uint8_t* consumed;
-  int64_t* cand;
-  // [0] ncand [1] nready (this round) [2] next pending list size [3] current pending list size
-  // [4] this round's first slot [5] pending seeds seen this round [6] rounds
-  unsigned long long* counters;
-  int64_t* ready;
-  int64_t* list[2];  // seeds (cell indices) still pending: this round's list and the next one's
+  uint8_t* flags;
+  Cand* cand;
+  int64_t cand_cap;
+  int64_t* list[2];  // candidates (indices into cand) still pending
+  int64_t* ready;    // this round's ready seeds (cells)
   Slot* slots;
   uint64_t* contrib;  // MAXC per slot
+  int64_t slot_cap;
+  unsigned long long* counters;
   unsigned long long* event_count;
 };
 
-__device__ __forceinline__ bool higher(const Args& A, int64_t q, int64_t c) {
-  const float eq = A.energy[q], ec = A.energy[c];
-  return eq > ec || (eq == ec && q < c);  // argsort(-energy, stable) over ascending candidates
-}
+// ---- 1. tiles: flags, candidates and their blockers ------------------------------------
 
-constexpr int SEED_CAP = 2048;  // seeds a CTA collects in smem before one global append
+constexpr int TX = 56, TY = 32, HALO = 4, HX = TX + 2 * HALO, HY = TY + 2 * HALO;  // HX = 64: two lane chunks
 
-// ratio / state / consumed for every cell, and the seed (candidate) list. A CTA
-// streams one contiguous range of cells (4 independent loads in flight per
-// thread), collects its seeds in smem and appends them with ONE global atomic
-// (a counter shared by the grid serialises at hundreds of thousands of atomics).
-__global__ void __launch_bounds__(NT) init_kernel(Args A) {
-  __shared__ int64_t seeds[SEED_CAP];
-  __shared__ unsigned s_n;
-  __shared__ unsigned long long s_base;
-  if (threadIdx.x == 0) s_n = 0;
-  __syncthreads();
-  const int64_t total = A.n * A.nevents;
-  const int64_t chunk = ((total + gridDim.x - 1) / gridDim.x + 4 * NT - 1) / (4 * NT) * (4 * NT);
-  const int64_t start = static_cast<int64_t>(blockIdx.x) * chunk, end = min(total, start + chunk);
-  for (int64_t c0 = start; c0 < end; c0 += 4 * NT) {
-    float e[4], nz[4];
+// One CTA per tile. Each candidate's 81-cell neighbourhood is scanned by one
+// warp (lane l looks at cells l, l + 32, l + 64 of the 9x9 square, row-major),
+// the blockers collected with three ballots. Candidates without blockers are
+// ready for the first round, the others start the first pending list. Index
+// math inside an event is 32-bit (events hold fewer than 2^31 cells).
+__global__ void __launch_bounds__(NT, 4) tile_kernel(Args A, int tiles_x, int tiles_per_event) {
+  __shared__ float se[HY * HX];
+  __shared__ uint8_t sc[HY * HX];
+  __shared__ uint16_t cl[TX * TY];   // the tile's candidates (halo index)
+  __shared__ uint16_t cls[TX * TY];  // their list (bit 15) and position in it
+  __shared__ int s_cnt[NT / 32];
+  __shared__ int s_nl[2];
+  __shared__ unsigned long long s_base, s_lb[2];
+  const int ev = blockIdx.x / tiles_per_event;
+  const int tile = blockIdx.x - ev * tiles_per_event;
+  const int ty0 = (tile / tiles_x) * TY, tx0 = (tile % tiles_x) * TX;
+  const int w = static_cast<int>(A.w), h = static_cast<int>(A.h);
+  const int64_t base = static_cast<int64_t>(ev) * A.n;
+  const float* E = A.energy + base;
+  const float* NZ = A.noise + base;
+  uint8_t* F = A.flags + base;
+  if (threadIdx.x < 2) s_nl[threadIdx.x] = 0;
+  // a warp loads whole halo rows (HX = 2 x 32 lanes), all of its rows in flight at once
+  constexpr int RPW = HY / (NT / 32);  // rows per warp
+  static_assert(HY % (NT / 32) == 0 && HX == 64, "tile shape");
+  const int lane0 = threadIdx.x & 31, wid0 = threadIdx.x >> 5;
+  float e[RPW][2], nz[RPW][2];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int64_t i = c0 + u * NT + threadIdx.x;
-      e[u] = i < end ? A.energy[i] : 0.0f;
-      nz[u] = i < end ? A.noise[i] : 1.0f;
+  for (int r = 0; r < RPW; ++r) {
+    const int y = ty0 - HALO + wid0 + r * (NT / 32);
+#pragma unroll
+    for (int ch = 0; ch < 2; ++ch) {
+      const int x = tx0 - HALO + ch * 32 + lane0;
+      const bool in = y >= 0 && y < h && x >= 0 && x < w;
+      e[r][ch] = in ? E[y * w + x] : 0.0f;
+      nz[r][ch] = in ? NZ[y * w + x] : 1.0f;
     }
+  }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int64_t i = c0 + u * NT + threadIdx.x;
-      if (i < end) {
-        const float r = __fdiv_rn(e[u], nz[u]);  // numpy f32 division (IEEE)
-        A.ratio[i] = r;
-        A.consumed[i] = 0;
-        const bool seed = r > 5.0f;
-        A.state[i] = seed ? PENDING : NONE;
-        if (seed) {
-          const unsigned pos = atomicAdd(&s_n, 1u);
-          if (pos < SEED_CAP)
-            seeds[pos] = i;
-          else
-            A.cand[atomicAdd(&A.counters[0], 1ull)] = i;  // an unusually dense range: straight to global
-        }
+  for (int r = 0; r < RPW; ++r) {
+    const int hy = wid0 + r * (NT / 32), y = ty0 - HALO + hy;
+#pragma unroll
+    for (int ch = 0; ch < 2; ++ch) {
+      const int hx = ch * 32 + lane0, x = tx0 - HALO + hx;
+      const bool in = y >= 0 && y < h && x >= 0 && x < w;
+      const bool cand = in && __fdiv_rn(e[r][ch], nz[r][ch]) > 5.0f;  // numpy f32 division; NaN: no candidate
+      if (in && hy >= HALO && hy < HALO + TY && hx >= HALO && hx < HALO + TX)
+        F[y * w + x] = cand ? PENDING : 0;  // read by the rounds (later launches)
+      se[hy * HX + hx] = e[r][ch];
+      sc[hy * HX + hx] = cand;
+    }
+  }
+  __syncthreads();
+  // compact the tile's candidates (row-major order) into cl
+  constexpr int PER = TX * TY / NT;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int mine = 0;
+#pragma unroll
+  for (int k = 0; k < PER; ++k) {
+    const int j = threadIdx.x * PER + k, iy = j / TX, ix = j - iy * TX;
+    mine += sc[(iy + HALO) * HX + ix + HALO];
+  }
+  int incl = mine;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  if (lane == 31) s_cnt[wid] = incl;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int t = 0;
+    for (int k = 0; k < NT / 32; ++k) {
+      const int v = s_cnt[k];
+      s_cnt[k] = t;
+      t += v;
+    }
+    s_base = t ? atomicAdd(&A.counters[C_NCAND], static_cast<unsigned long long>(t)) : 0ull;
+    s_lb[0] = static_cast<unsigned long long>(t);
+  }
+  __syncthreads();
+  const int total = static_cast<int>(s_lb[0]);
+  if (!total) return;
+  {
+    int pos = s_cnt[wid] + incl - mine;
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      const int j = threadIdx.x * PER + k, iy = j / TX, ix = j - iy * TX;
+      const int hc = (iy + HALO) * HX + ix + HALO;
+      if (sc[hc]) cl[pos++] = static_cast<uint16_t>(hc);
+    }
+  }
+  __syncthreads();
+  // this lane's three cells of the 9x9 square: offset in the halo tile (0 for lanes past the square or
+  // at its centre, which then never count), and whether it precedes the centre in cell order
+  int d[3];
+  bool valid[3], before[3];
+#pragma unroll
+  for (int r = 0; r < 3; ++r) {
+    const int j = lane + 32 * r;
+    valid[r] = j < 81 && j != 40;
+    before[r] = j < 40;  // a smaller cell index in the same event
+    d[r] = valid[r] ? (j / 9 - 4) * HX + (j % 9 - 4) : 0;
+  }
+  const unsigned lt = (1u << lane) - 1u;
+  const int64_t cap = A.cand_cap;
+  for (int q = wid; q < total; q += NT / 32) {
+    const int hc = cl[q];
+    const float ec = se[hc];
+    unsigned m[3];
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      const float eq = se[hc + d[r]];
+      m[r] = __ballot_sync(0xffffffffu, valid[r] & (sc[hc + d[r]] != 0) & ((eq > ec) | ((eq == ec) & before[r])));
+    }
+    const int c0 = __popc(m[0]), c1 = __popc(m[1]);
+    const int n = c0 + c1 + __popc(m[2]);
+    const int64_t kk = static_cast<int64_t>(s_base) + q;
+    if (kk < cap) {
+      Cand& R = A.cand[kk];
+      const int p0 = __popc(m[0] & lt), p1 = c0 + __popc(m[1] & lt), p2 = c0 + c1 + __popc(m[2] & lt);
+      if (((m[0] >> lane) & 1u) && p0 < KB) R.off[p0] = static_cast<uint8_t>(lane);
+      if (((m[1] >> lane) & 1u) && p1 < KB) R.off[p1] = static_cast<uint8_t>(lane + 32);
+      if (((m[2] >> lane) & 1u) && p2 < KB) R.off[p2] = static_cast<uint8_t>(lane + 64);
+      if (lane == 0) {
+        const int iy = hc / HX - HALO, ix = hc % HX - HALO;
+        const longlong2 head = make_longlong2(base + (ty0 + iy) * w + tx0 + ix,
+                                              static_cast<long long>(n <= KB ? static_cast<uint32_t>(n) : OVERFLOW));
+        *reinterpret_cast<longlong2*>(&R) = head;  // cell, n, cur = 0
+        const int which = n ? 1 : 0;  // 0: no blockers, ready for the first round
+        cls[q] = static_cast<uint16_t>(atomicAdd(&s_nl[which], 1) | (which << 15));
       }
     }
   }
   __syncthreads();
-  const unsigned m = min(s_n, static_cast<unsigned>(SEED_CAP));
-  if (threadIdx.x == 0) s_base = m ? atomicAdd(&A.counters[0], static_cast<unsigned long long>(m)) : 0ull;
+  if (threadIdx.x < 2) {
+    const int c = s_nl[threadIdx.x];
+    s_lb[threadIdx.x] = c ? atomicAdd(&A.counters[threadIdx.x ? C_CUR : C_READY], static_cast<unsigned long long>(c))
+                          : 0ull;
+  }
   __syncthreads();
-  for (unsigned j = threadIdx.x; j < m; j += NT) A.cand[s_base + j] = seeds[j];
+  for (int q = threadIdx.x; q < total; q += NT) {  // no blockers: ready for the first round (cells);
+    const int64_t kk = static_cast<int64_t>(s_base) + q;  // the others: the first pending list (records)
+    if (kk >= cap) continue;
+    const int which = cls[q] >> 15, li = cls[q] & 0x7fff;
+    if (which) {
+      A.list[0][s_lb[1] + li] = kk;
+    } else {
+      const int hc = cl[q], iy = hc / HX - HALO, ix = hc % HX - HALO;
+      A.ready[s_lb[0] + li] = base + (ty0 + iy) * w + tx0 + ix;
+    }
+  }
 }
 
-__device__ __forceinline__ unsigned long long ctr(const Args& A, int k) { return A.counters[k]; }
+// ---- 2. rounds: check, then process ---------------------------------------------------------
+//
+// check_kernel: one thread per candidate of the pending list walks its blocker
+// list from where the last round stopped (8 blocker flags in flight); a
+// candidate consumed meanwhile drops out, one with a pending blocker goes to
+// the next list, the rest are ready. process_kernel then processes the ready
+// seeds, whose windows are pairwise disjoint, spread over every warp of the
+// grid. Kernel boundaries order the two, so plain loads and stores suffice.
+// The last CTA out of each kernel does the round's bookkeeping, so the host
+// queues rounds without looking in between (an empty round returns at once).
+constexpr int PNT = 128;
+constexpr int PW = PNT / 32;
 
-// phase 1 of a round, over the candidates still pending (a list that shrinks
-// every round): a candidate consumed meanwhile drops out; one with a pending
-// seed of higher priority within distance 4 goes to the next round's list;
-// the rest are ready. Its 9x9 neighbourhood is scanned a row (9 independent
-// loads) at a time; counts and appends are aggregated per warp. Every kernel
-// of a round returns at once when nothing is pending any more, so the host
-// queues rounds without checking in between.
-__global__ void __launch_bounds__(NT) ready_kernel(Args A, int parity) {
+struct WinSmem {  // window values of 32 seeds of one warp
+  float e[32][25], r[32][25];
+  uint8_t t[32][25], nz[32][25];
+  unsigned mask[32];
+  int64_t seed[32];
+  int64_t slot[32];
+  int ev[32], sy[32], sx[32];  // the seed's event and position in it
+};
+
+// seed j's particle from its window values, into its slot: f64 sums in the reference's row-major
+// contributor order, no FMA, rounded once to f32 (reconstruct.py:84-117)
+__device__ void particle_sums(const Args& A, const WinSmem& S, int j) {
+  const int64_t s = S.seed[j];
+  const int ev = S.ev[j], sy = S.sy[j], sx = S.sx[j];
+  const int64_t loc = static_cast<int64_t>(sy) * A.w + sx;
+  const unsigned mask = S.mask[j];
+  double e64[4] = {0, 0, 0, 0}, sig64[4] = {0, 0, 0, 0};
+  int cnt[4] = {0, 0, 0, 0};
+  double sw = 0, swx = 0, swy = 0;
+  for (unsigned m = mask; m; m &= m - 1) {
+    const int i = __ffs(m) - 1;
+    const double e = static_cast<double>(S.e[j][i]);
+    const double ri = static_cast<double>(S.r[j][i]);
+    const int ti = S.t[j][i], ni = S.nz[j][i];
+    const double xi = static_cast<double>(sx + i % 5 - 2), yi = static_cast<double>(sy + i / 5 - 2);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (ti == q) {
+        e64[q] = __dadd_rn(e64[q], e);
+        sig64[q] = __dadd_rn(sig64[q], ri);
+        cnt[q] += ni;
+      }
+    }
+    sw = __dadd_rn(sw, e);
+    swx = __dadd_rn(swx, __dmul_rn(e, xi));
+    swy = __dadd_rn(swy, __dmul_rn(e, yi));
+  }
+  const double xbar = __ddiv_rn(swx, sw), ybar = __ddiv_rn(swy, sw);
+  double vx = 0, vy = 0;
+  for (unsigned m = mask; m; m &= m - 1) {
+    const int i = __ffs(m) - 1;
+    const double e = static_cast<double>(S.e[j][i]);
+    const double dx = __dsub_rn(static_cast<double>(sx + i % 5 - 2), xbar);
+    const double dy = __dsub_rn(static_cast<double>(sy + i / 5 - 2), ybar);
+    vx = __dadd_rn(vx, __dmul_rn(e, __dmul_rn(dx, dx)));
+    vy = __dadd_rn(vy, __dmul_rn(e, __dmul_rn(dy, dy)));
+  }
+  Slot& P = A.slots[S.slot[j]];
+  float c32[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    c32[q] = __double2float_rn(e64[q]);
+    P.ec[q] = c32[q];
+    P.sig[q] = __double2float_rn(sig64[q]);
+    P.nc[q] = static_cast<uint8_t>(cnt[q]);
+  }
+  P.energy = __double2float_rn(__dadd_rn(
+      __dadd_rn(__dadd_rn(static_cast<double>(c32[0]), static_cast<double>(c32[1])), static_cast<double>(c32[2])),
+      static_cast<double>(c32[3])));
+  P.x = __double2float_rn(xbar);
+  P.y = __double2float_rn(ybar);
+  P.xvar = __double2float_rn(__ddiv_rn(vx, sw));
+  P.yvar = __double2float_rn(__ddiv_rn(vy, sw));
+  P.nsens = __popc(mask);
+  P.event = static_cast<int32_t>(ev);
+  P.origin = loc;
+  P.key_e = A.energy[s];
+}
+
+__device__ __forceinline__ bool higher(const Args& A, int64_t q, int64_t c) {
+  const float eq = A.energy[q], ec = A.energy[c];
+  return eq > ec || (eq == ec && q < c);
+}
+
+// a candidate with more than KB blockers: any pending candidate of higher priority in its 9x9 neighbourhood?
+__device__ bool scan_blocked(const Args& A, int64_t c) {
+  const int64_t base = (c / A.n) * A.n, loc = c - base;
+  const int64_t cy = loc / A.w, cx = loc - cy * A.w;
+  for (int64_t y = max(static_cast<int64_t>(0), cy - 4); y <= min(A.h - 1, cy + 4); ++y)
+    for (int64_t x = max(static_cast<int64_t>(0), cx - 4); x <= min(A.w - 1, cx + 4); ++x) {
+      const int64_t q = base + y * A.w + x;
+      if (q != c && (A.flags[q] & PENDING) && higher(A, q, c)) return true;
+    }
+  return false;
+}
+
+// true in the one CTA that finishes last (every other CTA of the grid is done)
+__device__ __forceinline__ bool last_cta(unsigned long long* done) {
+  __shared__ bool s_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = atomicAdd(done, 1ull) == gridDim.x - 1;
+  }
+  __syncthreads();
+  return s_last;
+}
+
+__global__ void __launch_bounds__(NT) check_kernel(Args A, int parity) {
   const int lane = threadIdx.x & 31;
-  const int64_t m = static_cast<int64_t>(ctr(A, 3));
+  const int64_t m = static_cast<int64_t>(A.counters[C_CUR]);
   const int64_t* cur = A.list[parity];
   int64_t* nxt = A.list[parity ^ 1];
   const int64_t stride = static_cast<int64_t>(gridDim.x) * NT;
   for (int64_t i0 = static_cast<int64_t>(blockIdx.x) * NT + (threadIdx.x & ~31); i0 < m; i0 += stride) {
     const int64_t i = i0 + lane;
-    const int64_t c = i < m ? cur[i] : 0;  // cells, not candidate indices: one dependent load less
-    const bool pend = i < m && A.state[c] == PENDING;
+    const bool have = i < m;
+    const int64_t k = have ? cur[i] : 0;
+    Cand& R = A.cand[k];
+    const longlong2 head = have ? *reinterpret_cast<const longlong2*>(&R) : make_longlong2(0, 0);
+    const int64_t c = head.x;
+    const bool pend = have && (A.flags[c] & PENDING);
     bool ok = pend;
     if (pend) {
-      const int64_t base = (c / A.n) * A.n, loc = c - base;
-      const int64_t cy = loc / A.w, cx = loc - cy * A.w;
-      const int64_t x0 = imax64(0, cx - 4), x1 = imin64(A.w - 1, cx + 4);
-      for (int64_t y = imax64(0, cy - 4); ok && y <= imin64(A.h - 1, cy + 4); ++y) {
-        uint8_t st[9];
+      const uint32_t n = static_cast<uint32_t>(static_cast<uint64_t>(head.y) & 0xffffffffu);
+      if (n == OVERFLOW) {
+        ok = !scan_blocked(A, c);
+      } else {
+        uint32_t j = static_cast<uint32_t>(static_cast<uint64_t>(head.y) >> 32);
+        const uint32_t j0 = j;
+        while (j < n) {  // 8 blocker flags in flight at a time, stop at the first pending one
+          const uint32_t j8 = j & ~7u;
+          const uint64_t ow = *reinterpret_cast<const uint64_t*>(&R.off[j8]);
+          uint8_t st[8];
 #pragma unroll
-        for (int d = 0; d < 9; ++d) st[d] = x0 + d <= x1 ? A.state[base + y * A.w + x0 + d] : NONE;
+          for (int u = 0; u < 8; ++u) {
+            const uint32_t idx = j8 + u;
+            const int o = static_cast<int>((ow >> (8 * u)) & 0xff);
+            const int64_t q = c + static_cast<int64_t>(o / 9 - 4) * A.w + (o % 9 - 4);
+            st[u] = (idx >= j && idx < n) ? A.flags[q] : 0;
+          }
+          uint32_t hit = n;
 #pragma unroll
-        for (int d = 0; d < 9; ++d) {
-          const int64_t q = base + y * A.w + x0 + d;
-          if (st[d] == PENDING && q != c && higher(A, q, c)) ok = false;
+          for (int u = 7; u >= 0; --u)
+            if (st[u] & PENDING) hit = j8 + u;
+          if (hit < n) {
+            ok = false;
+            j = hit;
+            break;
+          }
+          j = j8 + 8;
         }
+        if (!ok && j != j0) R.cur = j;
       }
     }
     const bool wait = pend && !ok;
-    const unsigned pm = __ballot_sync(0xffffffffu, pend), rm = __ballot_sync(0xffffffffu, ok);
-    const unsigned wm = __ballot_sync(0xffffffffu, wait);
-    unsigned long long rb = 0, wb = 0;
-    if (lane == 0) {
-      if (pm) atomicAdd(&A.counters[5], static_cast<unsigned long long>(__popc(pm)));
-      if (rm) rb = atomicAdd(&A.counters[1], static_cast<unsigned long long>(__popc(rm)));
-      if (wm) wb = atomicAdd(&A.counters[2], static_cast<unsigned long long>(__popc(wm)));
-    }
-    rb = __shfl_sync(0xffffffffu, rb, 0);
-    wb = __shfl_sync(0xffffffffu, wb, 0);
+    const unsigned wm = __ballot_sync(0xffffffffu, wait), rm = __ballot_sync(0xffffffffu, ok);
     const unsigned below = (1u << lane) - 1u;
+    unsigned long long wb = 0, rb = 0;
+    if (lane == 0) {
+      if (wm) wb = atomicAdd(&A.counters[C_NEXT], static_cast<unsigned long long>(__popc(wm)));
+      if (rm) rb = atomicAdd(&A.counters[C_READY], static_cast<unsigned long long>(__popc(rm)));
+    }
+    wb = __shfl_sync(0xffffffffu, wb, 0);
+    rb = __shfl_sync(0xffffffffu, rb, 0);
+    if (wait) nxt[wb + __popc(wm & below)] = k;
     if (ok) A.ready[rb + __popc(rm & below)] = c;
-    if (wait) nxt[wb + __popc(wm & below)] = c;
+  }
+  if (last_cta(&A.counters[C_DONE]) && threadIdx.x == 0) {
+    A.counters[C_PASSES] += m != 0;
+    A.counters[C_CUR] = A.counters[C_NEXT];
+    A.counters[C_NEXT] = 0;
+    A.counters[C_DONE] = 0;
   }
 }
 
-// phase 2 of a round: process the ready seeds (pairwise disjoint windows).
-// A warp takes 32 ready seeds at a time in two steps:
-//  1. for each of them in turn, lane l < 25 examines window cell
-//     (l / 5 - 2, l % 5 - 2): every load in one round trip, the taken cells
-//     marked consumed, the contributor list written, and the cell values kept
-//     in shared memory;
-//  2. lane j adds up seed j's contributors in the reference's row-major order
-//     (reconstruct.py:84-117), f64 and no FMA, so every sum is bit-identical to
-//     the sequential walk -- 32 particles' sums side by side instead of one
-//     warp replaying one particle's serial sums.
-constexpr int PNT = 128;             // process threads per CTA
-constexpr int PW = PNT / 32;         // warps per CTA
-constexpr unsigned SKIPPED = ~0u;    // window mask of a seed consumed before its turn
-
-struct WinSmem {
-  float e[32][25], r[32][25];
-  uint8_t t[32][25], nz[32][25];
-  unsigned mask[32];
-};
-
+// A warp takes up to 32 ready seeds at a time: for each in turn, lane l < 25
+// examines window cell (l / 5 - 2, l % 5 - 2) -- every load in one round trip,
+// the taken cells marked consumed, the contributor list written, the values
+// kept in shared memory -- then lane j adds up seed j's contributors.
 __global__ void __launch_bounds__(PNT) process_kernel(Args A) {
   __shared__ WinSmem W[PW];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   WinSmem& S = W[wid];
-  const int64_t nready = static_cast<int64_t>(ctr(A, 1));
-  const unsigned long long slot0 = ctr(A, 4);
+  const int64_t nready = static_cast<int64_t>(A.counters[C_READY]);
+  const int64_t slot0 = static_cast<int64_t>(A.counters[C_SLOTS]);
+  const int w = static_cast<int>(A.w), h = static_cast<int>(A.h);
   // seeds per warp batch: spread over every warp of the grid (the window step is serial per warp)
   const int64_t nwarps = static_cast<int64_t>(gridDim.x) * PW;
   const int64_t per = max(static_cast<int64_t>(1), min(static_cast<int64_t>(32), (nready + nwarps - 1) / nwarps));
   const int64_t stride = nwarps * per;
   for (int64_t k0 = (static_cast<int64_t>(blockIdx.x) * PW + wid) * per; k0 < nready; k0 += stride) {
     const int nb = static_cast<int>(min(per, nready - k0));
-    for (int j = 0; j < nb; ++j) {  // 1. windows, one seed at a time
-      const int64_t s = A.ready[k0 + j];
-      const unsigned long long p = slot0 + static_cast<unsigned long long>(k0 + j);
-      const int64_t base = (s / A.n) * A.n, loc = s - base;
-      const int64_t sy = loc / A.w, sx = loc - sy * A.w;
-      const int64_t y = sy + lane / 5 - 2, x = sx + lane % 5 - 2;
-      const bool inwin = lane < 25 && y >= 0 && y < A.h && x >= 0 && x < A.w;
-      const int64_t f = inwin ? base + y * A.w + x : s;
-      const uint8_t used = A.consumed[f];
-      const float r32 = A.ratio[f], e32 = A.energy[f];
-      const uint8_t t = A.type[f] & 3, nz = A.noisy[f] != 0;
-      // lane 12 is the seed itself (window centre): consumed by an earlier particle -> skipped
-      if (__shfl_sync(0xffffffffu, used, 12)) {
-        if (lane == 0) {
-          A.state[s] = DECIDED;
-          A.slots[p].event = -1;
-          S.mask[j] = SKIPPED;
+    // lane j owns seed j of the batch: one load and one 64-bit division each, shared by shuffles
+    const int64_t my_s = lane < nb ? A.ready[k0 + lane] : 0;
+    const int64_t my_ev = my_s / A.n;
+    const int my_loc = static_cast<int>(my_s - my_ev * A.n);
+    const int my_sy = my_loc / w;
+    const int my_sx = my_loc - my_sy * w;
+    const int dy = lane / 5 - 2, dx = lane % 5 - 2;
+    constexpr int G = 4;  // windows whose loads are in flight together (the windows are disjoint)
+    for (int j0 = 0; j0 < nb; j0 += G) {
+      float e[G], z[G];
+      uint8_t fl[G], ty[G], nzv[G];
+      int64_t fc[G];
+      bool inw[G];
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        const int j = j0 + g;
+        const int sy = __shfl_sync(0xffffffffu, my_sy, j & 31), sx = __shfl_sync(0xffffffffu, my_sx, j & 31);
+        const int64_t ev = __shfl_sync(0xffffffffu, my_ev, j & 31);
+        const int y = sy + dy, x = sx + dx;
+        inw[g] = j < nb && lane < 25 && y >= 0 && y < h && x >= 0 && x < w;
+        fc[g] = ev * A.n + (inw[g] ? y * w + x : sy * w + sx);
+        fl[g] = j < nb ? A.flags[fc[g]] : 0;
+        e[g] = j < nb ? A.energy[fc[g]] : 0.0f;
+        z[g] = j < nb ? A.noise[fc[g]] : 1.0f;
+        ty[g] = j < nb ? A.type[fc[g]] & 3 : 0;
+        nzv[g] = j < nb ? A.noisy[fc[g]] != 0 : 0;
+      }
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        const int j = j0 + g;
+        if (j >= nb) break;
+        const int64_t p = slot0 + k0 + j;
+        const float r32 = __fdiv_rn(e[g], z[g]);
+        const bool take = inw[g] && !(fl[g] & CONSUMED) && r32 > 2.0f;
+        if (take) A.flags[fc[g]] = CONSUMED;  // clears PENDING: a consumed candidate is decided, so is the seed
+        const unsigned mask = __ballot_sync(0xffffffffu, take);
+        const int64_t ev = __shfl_sync(0xffffffffu, my_ev, j & 31);
+        if (take && p < A.slot_cap)  // contributor list, row-major: rank of this lane among the taken ones
+          A.contrib[p * MAXC + __popc(mask & ((1u << lane) - 1u))] = static_cast<uint64_t>(fc[g] - ev * A.n);
+        if (lane < 25) {
+          S.e[j][lane] = e[g];
+          S.r[j][lane] = r32;
+          S.t[j][lane] = ty[g];
+          S.nz[j][lane] = nzv[g];
         }
-        continue;
+        if (lane == 0) {
+          S.mask[j] = mask;
+          S.slot[j] = p;
+        }
       }
-      const bool take = inwin && !used && r32 > 2.0f;
-      __syncwarp();  // every lane has read `consumed` before any marks it
-      if (take) {
-        A.consumed[f] = 1;
-        if (f != s && A.state[f] == PENDING) A.state[f] = DECIDED;  // a consumed seed is always skipped
-      }
-      const unsigned mask = __ballot_sync(0xffffffffu, take);
-      if (take) {  // contributor list, row-major: rank of this lane among the taken ones
-        A.contrib[p * MAXC + __popc(mask & ((1u << lane) - 1u))] = static_cast<uint64_t>(f - base);
-      }
-      if (lane < 25) {
-        S.e[j][lane] = e32;
-        S.r[j][lane] = r32;
-        S.t[j][lane] = t;
-        S.nz[j][lane] = nz;
-      }
-      if (lane == 0) S.mask[j] = mask;
+    }
+    if (lane < nb) {
+      S.seed[lane] = my_s;
+      S.ev[lane] = static_cast<int>(my_ev);
+      S.sy[lane] = my_sy;
+      S.sx[lane] = my_sx;
     }
     __syncwarp();
-    // 2. sums, lane j for seed j
-    if (lane < nb && S.mask[lane] != SKIPPED) {
-      const int j = lane;
-      const int64_t s = A.ready[k0 + j];
-      const unsigned long long p = slot0 + static_cast<unsigned long long>(k0 + j);
-      const int64_t ev = s / A.n, loc = s - ev * A.n;
-      const int64_t sy = loc / A.w, sx = loc - sy * A.w;
-      const unsigned mask = S.mask[j];
-      double e64[4] = {0, 0, 0, 0}, sig64[4] = {0, 0, 0, 0};
-      int cnt[4] = {0, 0, 0, 0};
-      double sw = 0, swx = 0, swy = 0;
-      for (unsigned m = mask; m; m &= m - 1) {
-        const int i = __ffs(m) - 1;
-        const double e = static_cast<double>(S.e[j][i]);
-        const double ri = static_cast<double>(S.r[j][i]);
-        const int ti = S.t[j][i], ni = S.nz[j][i];
-        const double xi = static_cast<double>(sx + i % 5 - 2), yi = static_cast<double>(sy + i / 5 - 2);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          if (ti == q) {
-            e64[q] = __dadd_rn(e64[q], e);
-            sig64[q] = __dadd_rn(sig64[q], ri);
-            cnt[q] += ni;
-          }
-        }
-        sw = __dadd_rn(sw, e);
-        swx = __dadd_rn(swx, __dmul_rn(e, xi));
-        swy = __dadd_rn(swy, __dmul_rn(e, yi));
-      }
-      const double xbar = __ddiv_rn(swx, sw), ybar = __ddiv_rn(swy, sw);
-      double vx = 0, vy = 0;
-      for (unsigned m = mask; m; m &= m - 1) {
-        const int i = __ffs(m) - 1;
-        const double e = static_cast<double>(S.e[j][i]);
-        const double dx = __dsub_rn(static_cast<double>(sx + i % 5 - 2), xbar);
-        const double dy = __dsub_rn(static_cast<double>(sy + i / 5 - 2), ybar);
-        vx = __dadd_rn(vx, __dmul_rn(e, __dmul_rn(dx, dx)));
-        vy = __dadd_rn(vy, __dmul_rn(e, __dmul_rn(dy, dy)));
-      }
-      Slot& P = A.slots[p];
-      float c32[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        c32[q] = __double2float_rn(e64[q]);
-        P.ec[q] = c32[q];
-        P.sig[q] = __double2float_rn(sig64[q]);
-        P.nc[q] = static_cast<uint8_t>(cnt[q]);
-      }
-      P.energy = __double2float_rn(__dadd_rn(
-          __dadd_rn(__dadd_rn(static_cast<double>(c32[0]), static_cast<double>(c32[1])), static_cast<double>(c32[2])),
-          static_cast<double>(c32[3])));
-      P.x = __double2float_rn(xbar);
-      P.y = __double2float_rn(ybar);
-      P.xvar = __double2float_rn(__ddiv_rn(vx, sw));
-      P.yvar = __double2float_rn(__ddiv_rn(vy, sw));
-      P.nsens = __popc(mask);
-      P.event = static_cast<int32_t>(ev);
-      P.origin = loc;
-      P.key_e = A.energy[s];
-      atomicAdd(&A.event_count[ev], 1ull);
-      A.state[s] = DECIDED;
+    const bool mine = lane < nb && S.slot[lane] < A.slot_cap;
+    if (mine) {
+      particle_sums(A, S, lane);
+      atomicAdd(&A.event_count[S.ev[lane]], 1ull);
     }
+    const unsigned nc = __reduce_add_sync(0xffffffffu, mine ? static_cast<unsigned>(__popc(S.mask[lane])) : 0u);
+    if (lane == 0 && nc) atomicAdd(&A.counters[C_CONTRIB], static_cast<unsigned long long>(nc));
     __syncwarp();  // the window buffers are reused by the next batch
+  }
+  if (last_cta(&A.counters[C_DONE]) && threadIdx.x == 0) {
+    A.counters[C_SLOTS] += A.counters[C_READY];
+    A.counters[C_READY] = 0;
+    A.counters[C_DONE] = 0;
   }
 }
 
-// between rounds: the round's slots are taken, the next pending list becomes
-// current, a round that still saw pending seeds is counted
-__global__ void round_end_kernel(unsigned long long* counters) {
-  counters[6] += counters[5] != 0;
-  counters[4] += counters[1];
-  counters[3] = counters[2];
-  counters[1] = 0;
-  counters[2] = 0;
-  counters[5] = 0;
+// ---- 3. ordering -------------------------------------------------------------------------
+
+// event offsets: exclusive prefix of the per-event particle counts (one CTA, a thread per event run)
+__global__ void __launch_bounds__(NT) event_offsets_kernel(const unsigned long long* counts, int nevents,
+                                                            int64_t* off, int64_t* cnt, unsigned long long* cursor) {
+  __shared__ int64_t s_part[NT / 32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int per = (nevents + NT - 1) / NT, lo = min(nevents, static_cast<int>(threadIdx.x) * per),
+            hi = min(nevents, lo + per);
+  int64_t t = 0;
+  for (int e = lo; e < hi; ++e) t += static_cast<int64_t>(counts[e]);
+  int64_t incl = t;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int64_t v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  if (lane == 31) s_part[wid] = incl;
+  __syncthreads();
+  int64_t before = 0;
+  for (int k = 0; k < wid; ++k) before += s_part[k];
+  int64_t run = before + incl - t;
+  for (int e = lo; e < hi; ++e) {
+    off[e] = run;
+    cnt[e] = static_cast<int64_t>(counts[e]);
+    cursor[e] = 0;
+    run += static_cast<int64_t>(counts[e]);
+  }
 }
 
-// the pending list starts as every candidate (their cells)
-__global__ void __launch_bounds__(NT) list_init_kernel(unsigned long long* counters, const int64_t* cand,
-                                                       int64_t* list) {
-  const int64_t m = static_cast<int64_t>(counters[0]);
-  for (int64_t k = static_cast<int64_t>(blockIdx.x) * NT + threadIdx.x; k < m; k += static_cast<int64_t>(gridDim.x) * NT)
-    list[k] = cand[k];
-  if (blockIdx.x == 0 && threadIdx.x == 0) counters[3] = counters[0];
-}
-
-// order: bucket particles by event, then rank by priority inside the event
+// bucket particles by event, then rank by priority inside the event
 __global__ void bucket_kernel(const Slot* slots, int64_t np, const int64_t* event_off,
                               unsigned long long* cursor, int64_t* order) {
   for (int64_t p = static_cast<int64_t>(blockIdx.x) * NT + threadIdx.x; p < np;
@@ -414,17 +637,136 @@ __global__ void __launch_bounds__(NT) write_kernel(const Slot* slots, const int6
   }
 }
 
+// ---- host side ---------------------------------------------------------------------------
+
+// Device workspace of one run. Kept per device between runs (grow-only) so a
+// steady stream of calls allocates nothing; a run that finds the cache taken
+// (another handle alive) allocates its own.
+struct Workspace {
+  int device = -1;
+  void* mem = nullptr;
+  cudaEvent_t released = nullptr;  // recorded on the releasing stream: the next user waits for it
+  size_t bytes = 0;
+  int64_t cells = 0, cand_cap = 0, slot_cap = 0;
+  int nevents = 0;
+};
+
+static std::mutex g_ws_mu;
+static Workspace g_ws[64];
+static bool g_ws_busy[64];
+
 struct Handle {
   int device = 0;
   int64_t w = 0, h = 0, n = 0;
   int nevents = 0;
   int64_t np = 0;      // particles
   int64_t nslots = 0;  // particle slots written, holes (skipped seeds) included
-  void* ws = nullptr;
-  int64_t* lists = nullptr;  // the two pending lists
+  Workspace ws;
+  bool cached = false;  // ws belongs to the per-device cache
   Args A;
+  int64_t ncontrib = 0;
+  int64_t* order = nullptr;  // particle slots bucketed by event
+  int64_t* ev_off = nullptr;
+  int64_t* ev_cnt = nullptr;
+  unsigned long long* cursor = nullptr;
   std::vector<int64_t> counts;
 };
+
+static size_t al256(size_t v) { return (v + 255) & ~size_t(255); }
+
+static size_t ws_bytes(int64_t cells, int64_t cand_cap, int64_t slot_cap, int nevents) {
+  return al256(static_cast<size_t>(cells)) + al256(static_cast<size_t>(cand_cap) * sizeof(Cand)) +
+         3 * al256(static_cast<size_t>(cand_cap) * 8) + al256(static_cast<size_t>(slot_cap) * sizeof(Slot)) +
+         al256(static_cast<size_t>(slot_cap) * MAXC * 8) + al256(64) + al256(static_cast<size_t>(nevents + 1) * 8) +
+         al256(static_cast<size_t>(slot_cap) * 8) + 3 * al256(static_cast<size_t>(nevents + 1) * 8);
+}
+
+static void carve(Handle* H) {
+  uint8_t* p = static_cast<uint8_t*>(H->ws.mem);
+  Args& A = H->A;
+  A.flags = p; p += al256(static_cast<size_t>(H->ws.cells));
+  A.cand = reinterpret_cast<Cand*>(p); p += al256(static_cast<size_t>(H->ws.cand_cap) * sizeof(Cand));
+  A.list[0] = reinterpret_cast<int64_t*>(p); p += al256(static_cast<size_t>(H->ws.cand_cap) * 8);
+  A.list[1] = reinterpret_cast<int64_t*>(p); p += al256(static_cast<size_t>(H->ws.cand_cap) * 8);
+  A.ready = reinterpret_cast<int64_t*>(p); p += al256(static_cast<size_t>(H->ws.cand_cap) * 8);
+  A.slots = reinterpret_cast<Slot*>(p); p += al256(static_cast<size_t>(H->ws.slot_cap) * sizeof(Slot));
+  A.contrib = reinterpret_cast<uint64_t*>(p); p += al256(static_cast<size_t>(H->ws.slot_cap) * MAXC * 8);
+  A.counters = reinterpret_cast<unsigned long long*>(p); p += al256(64);
+  A.event_count = reinterpret_cast<unsigned long long*>(p); p += al256(static_cast<size_t>(H->ws.nevents + 1) * 8);
+  H->order = reinterpret_cast<int64_t*>(p); p += al256(static_cast<size_t>(H->ws.slot_cap) * 8);
+  H->ev_off = reinterpret_cast<int64_t*>(p); p += al256(static_cast<size_t>(H->ws.nevents + 1) * 8);
+  H->ev_cnt = reinterpret_cast<int64_t*>(p); p += al256(static_cast<size_t>(H->ws.nevents + 1) * 8);
+  H->cursor = reinterpret_cast<unsigned long long*>(p);
+  A.cand_cap = H->ws.cand_cap;
+  A.slot_cap = H->ws.slot_cap;
+}
+
+// a workspace for `cells` cells, at least the given capacities
+static int acquire_ws(Handle* H, int64_t cand_cap, int64_t slot_cap, cudaStream_t s) {
+  const int dev = H->device;
+  if (!H->ws.mem && dev >= 0 && dev < 64) {
+    std::lock_guard<std::mutex> g(g_ws_mu);
+    if (!g_ws_busy[dev]) {
+      g_ws_busy[dev] = true;
+      H->cached = true;
+      H->ws = g_ws[dev];
+      g_ws[dev] = Workspace();
+    }
+  }
+  Workspace& W = H->ws;
+  if (W.released) {  // work queued by the previous user (e.g. the pack of its contributor pool) comes first
+    SK_TRY(cudaStreamWaitEvent(s, W.released, 0));
+  }
+  cand_cap = std::max(cand_cap, W.cand_cap);
+  slot_cap = std::max(slot_cap, W.slot_cap);
+  const int64_t cells = std::max(H->n * H->nevents, W.cells);
+  const int nev = std::max(H->nevents, W.nevents);
+  if (W.mem && cells == W.cells && cand_cap == W.cand_cap && slot_cap == W.slot_cap && nev == W.nevents) {
+    carve(H);
+    return SK_OK;
+  }
+  if (W.mem) cudaFreeAsync(W.mem, s);
+  cudaEvent_t ev = W.released;
+  W = Workspace();
+  W.released = ev;
+  const size_t bytes = ws_bytes(cells, cand_cap, slot_cap, nev);
+  cudaError_t e = cudaMallocAsync(&W.mem, bytes, s);
+  if (e != cudaSuccess) {
+    W.mem = nullptr;
+    return cuda_fail(e, "cudaMallocAsync(reconstruction workspace)");
+  }
+  W.device = dev;
+  W.bytes = bytes;
+  W.cells = cells;
+  W.cand_cap = cand_cap;
+  W.slot_cap = slot_cap;
+  W.nevents = nev;
+  carve(H);
+  return SK_OK;
+}
+
+static void release_ws(Handle* H, cudaStream_t s) {
+  if (!H->ws.mem) return;
+  if (H->cached) {
+    if (!H->ws.released) cudaEventCreateWithFlags(&H->ws.released, cudaEventDisableTiming);
+    if (H->ws.released) cudaEventRecord(H->ws.released, s);
+    std::lock_guard<std::mutex> g(g_ws_mu);
+    g_ws[H->device] = H->ws;
+    g_ws_busy[H->device] = false;
+  } else {
+    cudaFreeAsync(H->ws.mem, s);
+    if (H->ws.released) cudaEventDestroy(H->ws.released);
+  }
+  H->ws = Workspace();
+}
+
+static int process_grid(const DeviceState* ds, int device) {
+  static int per_sm[64] = {0};
+  int& occ = per_sm[device & 63];
+  if (!occ && (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, process_kernel, PNT, 0) != cudaSuccess || occ < 1))
+    occ = 1;
+  return ds->sm_count * occ;
+}
 
 }  // namespace reco
 }  // namespace sk
@@ -437,6 +779,7 @@ int sk_reco_run(int64_t w, int64_t h, int nevents, const float* energy, const fl
                 const uint8_t* noisy, int device, uintptr_t stream, void** handle, int64_t* nparticles,
                 int* rounds) {
   if (!handle || w < 1 || h < 1 || nevents < 0) return set_error(SK_ERR_INVALID, "bad reconstruction arguments");
+  if (w * h >= (int64_t(1) << 31)) return set_error(SK_ERR_INVALID, "an event of %lld cells is too large", (long long)(w * h));
   DeviceState* ds = nullptr;
   int rc = device_state(device, &ds);
   if (rc) return rc;
@@ -448,78 +791,87 @@ int sk_reco_run(int64_t w, int64_t h, int nevents, const float* energy, const fl
   H->n = w * h;
   H->nevents = nevents;
   const int64_t total = H->n * nevents;
-  // workspace: ratio f32 | state u8 | consumed u8 | cand i64 | ready i64 | counters | event counts
-  const size_t sz_ratio = static_cast<size_t>(total) * 4, sz_u8 = static_cast<size_t>(total);
-  const size_t sz_idx = static_cast<size_t>(total) * 8, sz_cnt = 64, sz_ev = static_cast<size_t>(nevents + 1) * 8;
-  auto al = [](size_t v) { return (v + 255) & ~size_t(255); };
-  const size_t ws = al(sz_ratio) + 2 * al(sz_u8) + 2 * al(sz_idx) + al(sz_cnt) + al(sz_ev);
-  cudaError_t e = cudaMallocAsync(&H->ws, ws, s);
-  if (e != cudaSuccess) {
-    delete H;
-    return cuda_fail(e, "cudaMallocAsync(reconstruction workspace)");
-  }
-  uint8_t* p = static_cast<uint8_t*>(H->ws);
   reco::Args& A = H->A;
   memset(&A, 0, sizeof(A));
   A.w = w; A.h = h; A.n = H->n; A.nevents = nevents;
   A.energy = energy; A.noise = noise; A.type = type; A.noisy = noisy;
-  A.ratio = reinterpret_cast<float*>(p); p += al(sz_ratio);
-  A.state = p; p += al(sz_u8);
-  A.consumed = p; p += al(sz_u8);
-  A.cand = reinterpret_cast<int64_t*>(p); p += al(sz_idx);
-  A.ready = reinterpret_cast<int64_t*>(p); p += al(sz_idx);
-  A.counters = reinterpret_cast<unsigned long long*>(p); p += al(sz_cnt);
-  A.event_count = reinterpret_cast<unsigned long long*>(p);
-  SK_TRY(cudaMemsetAsync(A.counters, 0, sz_cnt, s));
-  SK_TRY(cudaMemsetAsync(A.event_count, 0, sz_ev, s));
-  const int grid = std::max(1, std::min<int>(ds->sm_count * 8, static_cast<int>((total + reco::NT - 1) / reco::NT)));
-  if (total) reco::init_kernel<<<grid, reco::NT, 0, s>>>(A);
-  SK_TRY(cudaGetLastError());
-  unsigned long long ncand = 0;
-  SK_TRY(cudaMemcpyAsync(&ncand, &A.counters[0], 8, cudaMemcpyDeviceToHost, s));
-  SK_TRY(cudaStreamSynchronize(s));
-  // particle slots (at most one per seed) and the two pending lists
-  const size_t nc1 = std::max<size_t>(1, ncand);
-  e = cudaMallocAsync(reinterpret_cast<void**>(&A.slots), nc1 * sizeof(reco::Slot), s);
-  if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&A.contrib), nc1 * reco::MAXC * 8, s);
-  if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&H->lists), nc1 * 16, s);
-  if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync(particle slots)");
-  A.list[0] = H->lists;
-  A.list[1] = A.list[0] + nc1;
-  const int rgrid = std::max(1, std::min<int>(ds->sm_count * 8, static_cast<int>((ncand + reco::NT - 1) / reco::NT)));
-  // process: one warp per 32 ready seeds
-  const int cgrid = std::max(1, std::min<int>(ds->sm_count * 8,
-                                              static_cast<int>((ncand + reco::PNT - 1) / reco::PNT)));
-  reco::list_init_kernel<<<rgrid, reco::NT, 0, s>>>(A.counters, A.cand, A.list[0]);
-  // rounds are queued without a host check in between (a round with nothing pending returns at once):
-  // 8 (full events converge in ~6), then 4 more at a time until the pending list is empty
-  int launched = 0;
-  for (unsigned long long left = ncand; left;) {
-    for (int k = 0; k < (launched ? 4 : 8); ++k, ++launched) {
-      reco::ready_kernel<<<rgrid, reco::NT, 0, s>>>(A, launched & 1);
-      reco::process_kernel<<<cgrid, reco::PNT, 0, s>>>(A);
-      reco::round_end_kernel<<<1, 1, 0, s>>>(A.counters);
-    }
-    SK_TRY(cudaGetLastError());
-    SK_TRY(cudaMemcpyAsync(&left, &A.counters[3], 8, cudaMemcpyDeviceToHost, s));
-    SK_TRY(cudaStreamSynchronize(s));
-  }
+  // first guess at the capacities (the benchmark events hold ~4% candidates, ~7% of them particles);
+  // the run counts what it needed and is repeated once with that if it did not fit
+  int64_t cand_cap = std::max<int64_t>(4096, total / 16), slot_cap = std::max<int64_t>(1024, total / 64);
+  const int tiles_x = static_cast<int>((w + reco::TX - 1) / reco::TX);
+  const int tiles_per_event = tiles_x * static_cast<int>((h + reco::TY - 1) / reco::TY);
+  const int cgrid = ds->sm_count * 8;
+  const int pgrid = reco::process_grid(ds, device);
   unsigned long long cnt[8] = {0};
-  SK_TRY(cudaMemcpyAsync(cnt, A.counters, sizeof(cnt), cudaMemcpyDeviceToHost, s));
-  H->counts.assign(nevents, 0);
   std::vector<unsigned long long> ec(nevents > 0 ? nevents : 1);
-  if (nevents) SK_TRY(cudaMemcpyAsync(ec.data(), A.event_count, nevents * 8, cudaMemcpyDeviceToHost, s));
-  SK_TRY(cudaStreamSynchronize(s));
+  for (int attempt = 0;; ++attempt) {
+    rc = reco::acquire_ws(H, cand_cap, slot_cap, s);
+    if (rc) {
+      delete H;
+      return rc;
+    }
+    SK_TRY(cudaMemsetAsync(A.counters, 0, 64, s));
+    SK_TRY(cudaMemsetAsync(A.event_count, 0, static_cast<size_t>(nevents + 1) * 8, s));
+    if (total) reco::tile_kernel<<<static_cast<unsigned>(nevents) * tiles_per_event, reco::NT, 0, s>>>(
+        A, tiles_x, tiles_per_event);
+    reco::process_kernel<<<pgrid, reco::PNT, 0, s>>>(A);  // the candidates without blockers
+    // rounds are queued without a host check in between (a round with nothing pending returns at once):
+    // 6 (full events converge in 4-5), then 4 more at a time until nothing is pending
+    int launched = 0;
+    for (;;) {
+      for (int k = 0; k < (launched ? 4 : 6); ++k, ++launched) {
+        reco::check_kernel<<<cgrid, reco::NT, 0, s>>>(A, launched & 1);
+        reco::process_kernel<<<pgrid, reco::PNT, 0, s>>>(A);
+      }
+      SK_TRY(cudaGetLastError());
+      SK_TRY(cudaMemcpyAsync(cnt, A.counters, sizeof(cnt), cudaMemcpyDeviceToHost, s));
+      if (nevents) SK_TRY(cudaMemcpyAsync(ec.data(), A.event_count, nevents * 8, cudaMemcpyDeviceToHost, s));
+      SK_TRY(cudaStreamSynchronize(s));
+      const bool over = static_cast<int64_t>(cnt[reco::C_NCAND]) > A.cand_cap ||
+                        static_cast<int64_t>(cnt[reco::C_SLOTS]) > A.slot_cap;
+      if (over || cnt[reco::C_CUR] == 0) break;
+      if (launched > static_cast<int>(std::min<unsigned long long>(cnt[reco::C_NCAND], 1u << 30)) + 16) {
+        reco::release_ws(H, s);  // every round decides at least the highest-priority pending seed
+        delete H;
+        return set_error(SK_ERR_CUDA, "reconstruction made no progress");
+      }
+    }
+    if (static_cast<int64_t>(cnt[reco::C_NCAND]) <= A.cand_cap &&
+        static_cast<int64_t>(cnt[reco::C_SLOTS]) <= A.slot_cap)
+      break;
+    if (attempt) {  // cannot happen: the second attempt has room for every candidate
+      reco::release_ws(H, s);
+      delete H;
+      return set_error(SK_ERR_CUDA, "reconstruction workspace overflow");
+    }
+    cand_cap = std::max<int64_t>(cand_cap, static_cast<int64_t>(cnt[reco::C_NCAND]));
+    slot_cap = std::max<int64_t>(slot_cap, cand_cap);  // at most one slot per candidate
+  }
+  H->counts.assign(nevents, 0);
   int64_t np = 0;
   for (int i = 0; i < nevents; ++i) {
     H->counts[i] = static_cast<int64_t>(ec[i]);
     np += H->counts[i];
   }
   H->np = np;
-  H->nslots = static_cast<int64_t>(cnt[4] + cnt[1]);  // slots of every round, holes included
+  H->nslots = static_cast<int64_t>(cnt[reco::C_SLOTS]);
+  H->ncontrib = static_cast<int64_t>(cnt[reco::C_CONTRIB]);
+  if (H->nslots != np) {  // a slot without a particle: the contributor pool would not match the counts
+    reco::release_ws(H, s);
+    delete H;
+    return set_error(SK_ERR_CUDA, "reconstruction left particle slots empty");
+  }
   *nparticles = H->np;
-  if (rounds) *rounds = static_cast<int>(cnt[6]);
+  if (rounds) *rounds = static_cast<int>(cnt[reco::C_PASSES]);
   *handle = H;
+  return SK_OK;
+}
+
+int sk_reco_sizes(void* handle, int64_t* nparticles, int64_t* ncontributors) {
+  auto* H = static_cast<reco::Handle*>(handle);
+  if (!H) return set_error(SK_ERR_INVALID, "null handle");
+  if (nparticles) *nparticles = H->np;
+  if (ncontributors) *ncontributors = H->ncontrib;
   return SK_OK;
 }
 
@@ -542,21 +894,11 @@ int sk_reco_write(void* handle, float* energy, float* x, float* y, uint64_t* ori
   cudaStream_t s = resolve_stream(H->device, stream);
   if (sensor_pool) *sensor_pool = H->A.contrib;
   if (H->np == 0) return SK_OK;
-  std::vector<int64_t> off(H->nevents + 1, 0);
-  for (int i = 0; i < H->nevents; ++i) off[i + 1] = off[i] + H->counts[i];
-  int64_t *d_off = nullptr, *d_cnt = nullptr, *order = nullptr;
-  unsigned long long* cursor = nullptr;
-  const size_t ev_bytes = static_cast<size_t>(H->nevents + 1) * 8;
-  SK_TRY(cudaMallocAsync(&d_off, ev_bytes, s));
-  SK_TRY(cudaMallocAsync(&d_cnt, ev_bytes, s));
-  SK_TRY(cudaMallocAsync(&cursor, ev_bytes, s));
-  SK_TRY(cudaMallocAsync(&order, static_cast<size_t>(H->np) * 8, s));
-  SK_TRY(cudaMemcpyAsync(d_off, off.data(), ev_bytes, cudaMemcpyHostToDevice, s));
-  SK_TRY(cudaMemcpyAsync(d_cnt, H->counts.data(), H->nevents * 8, cudaMemcpyHostToDevice, s));
-  SK_TRY(cudaMemsetAsync(cursor, 0, ev_bytes, s));
+  // event offsets on the device (no host round trip), then bucket the slots by event
+  reco::event_offsets_kernel<<<1, reco::NT, 0, s>>>(H->A.event_count, H->nevents, H->ev_off, H->ev_cnt, H->cursor);
   const int bgrid =
       std::max(1, std::min<int>(ds->sm_count * 8, static_cast<int>((H->nslots + reco::NT - 1) / reco::NT)));
-  reco::bucket_kernel<<<bgrid, reco::NT, 0, s>>>(H->A.slots, H->nslots, d_off, cursor, order);
+  reco::bucket_kernel<<<bgrid, reco::NT, 0, s>>>(H->A.slots, H->nslots, H->ev_off, H->cursor, H->order);
   reco::OutArgs O;
   O.energy = energy; O.x = x; O.y = y; O.xvar = x_variance; O.yvar = y_variance; O.origin = origin;
   for (int t = 0; t < 4; ++t) {
@@ -571,12 +913,8 @@ int sk_reco_write(void* handle, float* energy, float* x, float* y, uint64_t* ori
   const unsigned chunks =
       static_cast<unsigned>(std::min<int64_t>((mmax + reco::RANK_PER_CTA - 1) / reco::RANK_PER_CTA, 65535));
   if (H->nevents && chunks)
-    reco::write_kernel<<<dim3(H->nevents, chunks), reco::NT, 0, s>>>(H->A.slots, d_off, d_cnt, order, O);
+    reco::write_kernel<<<dim3(H->nevents, chunks), reco::NT, 0, s>>>(H->A.slots, H->ev_off, H->ev_cnt, H->order, O);
   SK_TRY(cudaGetLastError());
-  cudaFreeAsync(d_off, s);
-  cudaFreeAsync(d_cnt, s);
-  cudaFreeAsync(cursor, s);
-  cudaFreeAsync(order, s);
   return SK_OK;
 }
 
@@ -584,10 +922,7 @@ int sk_reco_free(void* handle, uintptr_t stream) {
   auto* H = static_cast<reco::Handle*>(handle);
   if (!H) return SK_OK;
   cudaStream_t s = resolve_stream(H->device, stream);
-  if (H->A.slots) cudaFreeAsync(H->A.slots, s);
-  if (H->A.contrib) cudaFreeAsync(H->A.contrib, s);
-  if (H->ws) cudaFreeAsync(H->ws, s);
-  if (H->lists) cudaFreeAsync(H->lists, s);
+  reco::release_ws(H, s);
   delete H;
   return SK_OK;
 }

@@ -161,7 +161,9 @@ def reconstruct_from_collection(sensors, width: int, height: int, out=None, even
     nat.call("sk_reco_run", width, height, events, p[_ENERGY], noise.ptr, ptype, p[_NOISY], dev, nat.stream(dev),
              C.byref(handle), C.byref(np_), C.byref(rounds))
     try:
-        m = np_.value
+        m, ncon = C.c_int64(0), C.c_int64(0)
+        nat.call("sk_reco_sizes", handle, C.byref(m), C.byref(ncon))
+        m, ncon = m.value, ncon.value
         if out is None:
             out = Collection(PARTICLE_SCHEMA, ly.PER_FIELD, memctx.ContextInfo.cuda(dev))
         lay = out.layout
@@ -180,14 +182,14 @@ def reconstruct_from_collection(sensors, width: int, height: int, out=None, even
                  planes4("noisy_count.value"), lens.ptr, offs.ptr, C.byref(pool), nat.stream(dev))
         counts = (C.c_int64 * max(events, 1))()
         nat.call("sk_reco_event_counts", handle, counts)
-        ncon = 25 * max(m, 1)
-        jagged.pack(out, "sensors", lens, offs, DeviceArray.wrap(pool.value or 0, ncon, np.uint64, dev))
-        lens.free()
-        offs.free()
+        # the contributor lists: their total is known, so the pack is only queued (jagged.pack_known_total)
+        jagged.pack_known_total(out, "sensors", lens, offs, pool.value or 0, 25 * max(m, 1), ncon)
         out.event_counts = list(counts)[:events]
         out.reco_rounds = rounds.value
     finally:
         nat.call("sk_reco_free", handle, nat.stream(dev))
+    lens.free()
+    offs.free()
     nat.sync(dev)
     return out
 

@@ -6,12 +6,13 @@ import numpy as np
 import pytest
 
 import paper_2511_04853_b200 as sk
-from gpuhelp import CUDA, HOST, to_host_planes
+from gpuhelp import CUDA, HOST, aos_collection, to_host_planes
 from oracle import restate as R
 from paper_2511_04853_b200 import layouts as ly, memctx as mc, sensor, transfer as tr
 from skhelp import golden
 
 pytestmark = pytest.mark.gpu
+
 
 FIELDS = ("energy", "x", "y", "origin", "x_variance", "y_variance")
 ARRAYS = ("significance", "E_contribution", "noisy_count")
@@ -106,3 +107,63 @@ def test_export_particles_matches_reference_struct(name):
     for i in range(m):
         assert sens[i].tobytes() == g["sensors"][cuts[i]:cuts[i + 1]].tobytes()
     del ev
+
+
+def _cells_on_device(energy, typ, noisy):
+    recs = np.zeros(energy.size, R.SENSOR_AOS_DTYPE)
+    recs["energy"], recs["type"] = energy, typ
+    recs["calibration_data"]["noisy"] = noisy
+    h = aos_collection(sensor.SENSOR_SCHEMA, recs, energy.size)
+    d = sk.Collection(sensor.SENSOR_SCHEMA, ly.PER_FIELD, CUDA)
+    tr.copy_collection(d, h)
+    return d
+
+
+@pytest.mark.parametrize("w,h,events", [(64, 48, 1), (150, 97, 3)])
+def test_dense_tied_candidates_vs_oracle(w, h, events):
+    """Nearly every cell a candidate, energies drawn from a few values (ties broken by cell index), so
+    seeds wait on long blocker chains and many have more blockers than the per-candidate list keeps
+    (the 9x9 rescan path)."""
+    from paper_2511_04853_b200.devarray import DeviceArray
+
+    rng = np.random.default_rng(w * h)
+    n = w * h
+    vals = np.array([1.0, 3.0, 6.0, 7.0, 8.0, 50.0, 100.0], np.float32)
+    energy = vals[rng.choice(vals.size, n * events, p=[0.05, 0.1, 0.25, 0.2, 0.2, 0.1, 0.1])]
+    noise = np.ones(n * events, np.float32)
+    typ = rng.integers(0, 4, n * events).astype(np.uint8)
+    noisy = rng.random(n * events) < 0.1
+    dev = _cells_on_device(energy, typ, noisy)
+    parts = sensor.reconstruct_from_collection(dev, w, h, events=events, noise=DeviceArray.from_numpy(noise, CUDA))
+    got = _host_particles(parts)
+    lo = 0
+    starts = np.concatenate([[0], np.cumsum(got["sensor_lens"].astype(np.int64))])
+    for i in range(events):
+        sl = slice(i * n, (i + 1) * n)
+        want = R.reconstruct(energy[sl], noise[sl], typ[sl], noisy[sl], w, h)
+        m = parts.event_counts[i]
+        assert m == want["energy"].size
+        part = {k: got[k][lo:lo + m] for k in FIELDS + ARRAYS + ("sensor_lens",)}
+        part["sensors"] = got["sensors"][starts[lo]:starts[lo + m]]
+        _compare(part, want, i)
+        lo += m
+
+
+def test_repeated_runs_reuse_the_workspace_and_agree():
+    """The device workspace is cached between runs; a bigger batch after a smaller one grows it."""
+    small = sk.Collection(sensor.SENSOR_SCHEMA, ly.PER_FIELD, CUDA)
+    sensor.generate_events(small, 200, 150, [1], 0.004)
+    sensor.calibrate_collection(small)
+    big = sk.Collection(sensor.SENSOR_SCHEMA, ly.PER_FIELD, CUDA)
+    sensor.generate_events(big, 200, 150, [1, 2, 3, 4], 0.004)
+    sensor.calibrate_collection(big)
+    one = sensor.reconstruct_from_collection(small, 200, 150)
+    first = _host_particles(one)
+    four = sensor.reconstruct_from_collection(big, 200, 150, events=4)
+    again = _host_particles(sensor.reconstruct_from_collection(small, 200, 150))
+    _compare(again, first, "again")
+    m = four.event_counts[0]
+    head = _host_particles(four)
+    assert m == len(one)
+    for k in FIELDS:
+        assert head[k][:m].tobytes() == first[k].tobytes()
