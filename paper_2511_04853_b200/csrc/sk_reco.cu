@@ -49,17 +49,6 @@ constexpr int MAXC = 25;  // contributors per particle (5x5 window)
 constexpr uint8_t PENDING = 1;   // a candidate not decided yet
 constexpr uint8_t CONSUMED = 2;  // taken by a particle (a consumed candidate is decided)
 
-constexpr int KB = 48;                 // blocker offsets kept per candidate
-constexpr uint32_t OVERFLOW = ~0u;     // more blockers than KB: the pass scans the 9x9 neighbourhood instead
-
-struct Cand {          // 64 B
-  int64_t cell;        // cell index (event-major)
-  uint32_t n;          // blockers, or OVERFLOW
-  uint32_t cur;        // blockers [0, cur) are known to be decided
-  uint8_t off[KB];     // (dy + 4) * 9 + (dx + 4), row-major
-};
-static_assert(sizeof(Cand) == 64, "Cand is one 64-byte record");
-
 struct Slot {  // one reconstructed particle, before ordering
   float energy, x, y, xvar, yvar;
   float sig[4], ec[4];
@@ -83,9 +72,8 @@ struct Args {
   const uint8_t* type;
   const uint8_t* noisy;
   uint8_t* flags;
-  Cand* cand;
-  int64_t cand_cap;
-  int64_t* list[2];  // candidates (indices into cand) still pending
+  int64_t cand_cap;  // capacity of the lists
+  int64_t* list[2];  // candidates (cells) still pending
   int64_t* ready;    // this round's ready seeds (cells)
   Slot* slots;
   uint64_t* contrib;  // MAXC per slot
@@ -96,16 +84,17 @@ struct Args {
 
 // ---- 1. tiles: flags, candidates and their blockers ------------------------------------
 
-constexpr int TX = 56, TY = 32, HALO = 4, HX = TX + 2 * HALO, HY = TY + 2 * HALO;  // HX = 64: two lane chunks
+constexpr int TX = 56, TY = 40, HALO = 4, HX = TX + 2 * HALO, HY = TY + 2 * HALO;  // a halo tile of 64 x 48
 
 // One CTA per tile. Each candidate's 81-cell neighbourhood is scanned by one
 // warp (lane l looks at cells l, l + 32, l + 64 of the 9x9 square, row-major),
 // the blockers collected with three ballots. Candidates without blockers are
 // ready for the first round, the others start the first pending list. Index
 // math inside an event is 32-bit (events hold fewer than 2^31 cells).
+template <bool VEC>
 __global__ void __launch_bounds__(NT, 4) tile_kernel(Args A, int tiles_x, int tiles_per_event) {
-  __shared__ float se[HY * HX];
-  __shared__ uint8_t sc[HY * HX];
+  __shared__ __align__(16) float se[HY * HX];
+  __shared__ __align__(16) uint8_t sc[HY * HX];
   __shared__ uint16_t cl[TX * TY];   // the tile's candidates (halo index)
   __shared__ uint16_t cls[TX * TY];  // their list (bit 15) and position in it
   __shared__ int s_cnt[NT / 32];
@@ -120,45 +109,78 @@ __global__ void __launch_bounds__(NT, 4) tile_kernel(Args A, int tiles_x, int ti
   const float* NZ = A.noise + base;
   uint8_t* F = A.flags + base;
   if (threadIdx.x < 2) s_nl[threadIdx.x] = 0;
-  // a warp loads whole halo rows (HX = 2 x 32 lanes), all of its rows in flight at once
-  constexpr int RPW = HY / (NT / 32);  // rows per warp
-  static_assert(HY % (NT / 32) == 0 && HX == 64, "tile shape");
-  const int lane0 = threadIdx.x & 31, wid0 = threadIdx.x >> 5;
-  float e[RPW][2], nz[RPW][2];
+  if constexpr (VEC) {
+    // w % 4 == 0 and 16-byte aligned planes: a thread loads 4 cells at once (a group of 4 is wholly
+    // inside or outside the grid, wholly interior or halo), all of its rows in flight together
+    constexpr int G4 = HX / 4, RG = NT / G4, RPT = HY / RG;
+    static_assert(NT % G4 == 0 && HY % RG == 0, "tile shape");
+    const int c4 = threadIdx.x % G4, rg = threadIdx.x / G4;
+    const int hx = c4 * 4, x = tx0 - HALO + hx;
+    const bool xin = x >= 0 && x < w, xint = hx >= HALO && hx < HALO + TX;
+    float4 e[RPT], z[RPT];
 #pragma unroll
-  for (int r = 0; r < RPW; ++r) {
-    const int y = ty0 - HALO + wid0 + r * (NT / 32);
-#pragma unroll
-    for (int ch = 0; ch < 2; ++ch) {
-      const int x = tx0 - HALO + ch * 32 + lane0;
-      const bool in = y >= 0 && y < h && x >= 0 && x < w;
-      e[r][ch] = in ? E[y * w + x] : 0.0f;
-      nz[r][ch] = in ? NZ[y * w + x] : 1.0f;
+    for (int r = 0; r < RPT; ++r) {
+      const int y = ty0 - HALO + rg + r * RG;
+      const bool in = xin && y >= 0 && y < h;
+      e[r] = in ? *reinterpret_cast<const float4*>(E + static_cast<int64_t>(y) * w + x) : make_float4(0, 0, 0, 0);
+      z[r] = in ? *reinterpret_cast<const float4*>(NZ + static_cast<int64_t>(y) * w + x) : make_float4(1, 1, 1, 1);
     }
-  }
 #pragma unroll
-  for (int r = 0; r < RPW; ++r) {
-    const int hy = wid0 + r * (NT / 32), y = ty0 - HALO + hy;
+    for (int r = 0; r < RPT; ++r) {
+      const int hy = rg + r * RG, y = ty0 - HALO + hy;
+      const bool in = xin && y >= 0 && y < h;
+      // numpy f32 division (IEEE); NaN is no candidate
+      const uint32_t cand = in ? (static_cast<uint32_t>(__fdiv_rn(e[r].x, z[r].x) > 5.0f) |
+                                  static_cast<uint32_t>(__fdiv_rn(e[r].y, z[r].y) > 5.0f) << 8 |
+                                  static_cast<uint32_t>(__fdiv_rn(e[r].z, z[r].z) > 5.0f) << 16 |
+                                  static_cast<uint32_t>(__fdiv_rn(e[r].w, z[r].w) > 5.0f) << 24)
+                               : 0u;
+      if (in && xint && hy >= HALO && hy < HALO + TY)  // PENDING == 1: the candidate bytes are the flags
+        *reinterpret_cast<uint32_t*>(F + static_cast<int64_t>(y) * w + x) = cand;
+      *reinterpret_cast<float4*>(&se[hy * HX + hx]) = e[r];
+      *reinterpret_cast<uint32_t*>(&sc[hy * HX + hx]) = cand;
+    }
+  } else {
+    // a warp loads whole halo rows (HX = 2 x 32 lanes), all of its rows in flight at once
+    constexpr int RPW = HY / (NT / 32);  // rows per warp
+    static_assert(HY % (NT / 32) == 0 && HX == 64, "tile shape");
+    const int lane0 = threadIdx.x & 31, wid0 = threadIdx.x >> 5;
+    float e[RPW][2], nz[RPW][2];
 #pragma unroll
-    for (int ch = 0; ch < 2; ++ch) {
-      const int hx = ch * 32 + lane0, x = tx0 - HALO + hx;
-      const bool in = y >= 0 && y < h && x >= 0 && x < w;
-      const bool cand = in && __fdiv_rn(e[r][ch], nz[r][ch]) > 5.0f;  // numpy f32 division; NaN: no candidate
-      if (in && hy >= HALO && hy < HALO + TY && hx >= HALO && hx < HALO + TX)
-        F[y * w + x] = cand ? PENDING : 0;  // read by the rounds (later launches)
-      se[hy * HX + hx] = e[r][ch];
-      sc[hy * HX + hx] = cand;
+    for (int r = 0; r < RPW; ++r) {
+      const int y = ty0 - HALO + wid0 + r * (NT / 32);
+#pragma unroll
+      for (int ch = 0; ch < 2; ++ch) {
+        const int x = tx0 - HALO + ch * 32 + lane0;
+        const bool in = y >= 0 && y < h && x >= 0 && x < w;
+        e[r][ch] = in ? E[static_cast<int64_t>(y) * w + x] : 0.0f;
+        nz[r][ch] = in ? NZ[static_cast<int64_t>(y) * w + x] : 1.0f;
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < RPW; ++r) {
+      const int hy = wid0 + r * (NT / 32), y = ty0 - HALO + hy;
+#pragma unroll
+      for (int ch = 0; ch < 2; ++ch) {
+        const int hx = ch * 32 + lane0, x = tx0 - HALO + hx;
+        const bool in = y >= 0 && y < h && x >= 0 && x < w;
+        const bool cand = in && __fdiv_rn(e[r][ch], nz[r][ch]) > 5.0f;  // numpy f32 division; NaN: no candidate
+        if (in && hy >= HALO && hy < HALO + TY && hx >= HALO && hx < HALO + TX)
+          F[static_cast<int64_t>(y) * w + x] = cand ? PENDING : 0;  // read by the rounds (later launches)
+        se[hy * HX + hx] = e[r][ch];
+        sc[hy * HX + hx] = cand;
+      }
     }
   }
   __syncthreads();
   // compact the tile's candidates (row-major order) into cl
-  constexpr int PER = TX * TY / NT;
+  constexpr int PER = (TX * TY + NT - 1) / NT;  // a contiguous run of interior cells per thread
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   int mine = 0;
 #pragma unroll
   for (int k = 0; k < PER; ++k) {
     const int j = threadIdx.x * PER + k, iy = j / TX, ix = j - iy * TX;
-    mine += sc[(iy + HALO) * HX + ix + HALO];
+    if (j < TX * TY) mine += sc[(iy + HALO) * HX + ix + HALO];
   }
   int incl = mine;
 #pragma unroll
@@ -187,49 +209,35 @@ __global__ void __launch_bounds__(NT, 4) tile_kernel(Args A, int tiles_x, int ti
     for (int k = 0; k < PER; ++k) {
       const int j = threadIdx.x * PER + k, iy = j / TX, ix = j - iy * TX;
       const int hc = (iy + HALO) * HX + ix + HALO;
-      if (sc[hc]) cl[pos++] = static_cast<uint16_t>(hc);
+      if (j < TX * TY && sc[hc]) cl[pos++] = static_cast<uint16_t>(hc);
     }
   }
   __syncthreads();
-  // this lane's three cells of the 9x9 square: offset in the halo tile (0 for lanes past the square or
-  // at its centre, which then never count), and whether it precedes the centre in cell order
-  int d[3];
-  bool valid[3], before[3];
-#pragma unroll
-  for (int r = 0; r < 3; ++r) {
-    const int j = lane + 32 * r;
-    valid[r] = j < 81 && j != 40;
-    before[r] = j < 40;  // a smaller cell index in the same event
-    d[r] = valid[r] ? (j / 9 - 4) * HX + (j % 9 - 4) : 0;
-  }
-  const unsigned lt = (1u << lane) - 1u;
+  // one thread per candidate: is it the top priority among the candidates of its 9x9 neighbourhood? The
+  // neighbourhood is walked ring by ring from the centre, every offset a constant, and the walk stops at
+  // the first candidate of higher priority (usually an adjacent one)
   const int64_t cap = A.cand_cap;
-  for (int q = wid; q < total; q += NT / 32) {
+  for (int q = threadIdx.x; q < total; q += NT) {
     const int hc = cl[q];
     const float ec = se[hc];
-    unsigned m[3];
+    bool top = true;
 #pragma unroll
-    for (int r = 0; r < 3; ++r) {
-      const float eq = se[hc + d[r]];
-      m[r] = __ballot_sync(0xffffffffu, valid[r] & (sc[hc + d[r]] != 0) & ((eq > ec) | ((eq == ec) & before[r])));
-    }
-    const int c0 = __popc(m[0]), c1 = __popc(m[1]);
-    const int n = c0 + c1 + __popc(m[2]);
-    const int64_t kk = static_cast<int64_t>(s_base) + q;
-    if (kk < cap) {
-      Cand& R = A.cand[kk];
-      const int p0 = __popc(m[0] & lt), p1 = c0 + __popc(m[1] & lt), p2 = c0 + c1 + __popc(m[2] & lt);
-      if (((m[0] >> lane) & 1u) && p0 < KB) R.off[p0] = static_cast<uint8_t>(lane);
-      if (((m[1] >> lane) & 1u) && p1 < KB) R.off[p1] = static_cast<uint8_t>(lane + 32);
-      if (((m[2] >> lane) & 1u) && p2 < KB) R.off[p2] = static_cast<uint8_t>(lane + 64);
-      if (lane == 0) {
-        const int iy = hc / HX - HALO, ix = hc % HX - HALO;
-        const longlong2 head = make_longlong2(base + (ty0 + iy) * w + tx0 + ix,
-                                              static_cast<long long>(n <= KB ? static_cast<uint32_t>(n) : OVERFLOW));
-        *reinterpret_cast<longlong2*>(&R) = head;  // cell, n, cur = 0
-        const int which = n ? 1 : 0;  // 0: no blockers, ready for the first round
-        cls[q] = static_cast<uint16_t>(atomicAdd(&s_nl[which], 1) | (which << 15));
-      }
+    for (int r = 1; r <= HALO && top; ++r)
+#pragma unroll
+      for (int dy = -r; dy <= r; ++dy)
+#pragma unroll
+        for (int dx = -r; dx <= r; ++dx) {
+          if (dy != -r && dy != r && dx != -r && dx != r) continue;  // ring r only
+          const int d = dy * HX + dx;
+          const bool before = dy < 0 || (dy == 0 && dx < 0);  // a smaller cell index in the same event
+          if (top && sc[hc + d]) {
+            const float eq = se[hc + d];
+            if (eq > ec || (before && eq == ec)) top = false;
+          }
+        }
+    if (static_cast<int64_t>(s_base) + q < cap) {
+      const int which = top ? 0 : 1;  // 0: no blockers, ready for the first round
+      cls[q] = static_cast<uint16_t>(atomicAdd(&s_nl[which], 1) | (which << 15));
     }
   }
   __syncthreads();
@@ -243,12 +251,12 @@ __global__ void __launch_bounds__(NT, 4) tile_kernel(Args A, int tiles_x, int ti
     const int64_t kk = static_cast<int64_t>(s_base) + q;  // the others: the first pending list (records)
     if (kk >= cap) continue;
     const int which = cls[q] >> 15, li = cls[q] & 0x7fff;
-    if (which) {
-      A.list[0][s_lb[1] + li] = kk;
-    } else {
-      const int hc = cl[q], iy = hc / HX - HALO, ix = hc % HX - HALO;
-      A.ready[s_lb[0] + li] = base + (ty0 + iy) * w + tx0 + ix;
-    }
+    const int hc = cl[q], iy = hc / HX - HALO, ix = hc % HX - HALO;
+    const int64_t cell = base + (ty0 + iy) * w + tx0 + ix;
+    if (which)
+      A.list[0][s_lb[1] + li] = cell;
+    else
+      A.ready[s_lb[0] + li] = cell;
   }
 }
 
@@ -339,15 +347,76 @@ __device__ __forceinline__ bool higher(const Args& A, int64_t q, int64_t c) {
   return eq > ec || (eq == ec && q < c);
 }
 
-// a candidate with more than KB blockers: any pending candidate of higher priority in its 9x9 neighbourhood?
-__device__ bool scan_blocked(const Args& A, int64_t c) {
-  const int64_t base = (c / A.n) * A.n, loc = c - base;
-  const int64_t cy = loc / A.w, cx = loc - cy * A.w;
-  for (int64_t y = max(static_cast<int64_t>(0), cy - 4); y <= min(A.h - 1, cy + 4); ++y)
-    for (int64_t x = max(static_cast<int64_t>(0), cx - 4); x <= min(A.w - 1, cx + 4); ++x) {
-      const int64_t q = base + y * A.w + x;
-      if (q != c && (A.flags[q] & PENDING) && higher(A, q, c)) return true;
+// bit 0 of each byte of v, in byte order
+__device__ __forceinline__ uint32_t low_bits8(uint64_t v) {
+  return static_cast<uint32_t>(((v & 0x0101010101010101ull) * 0x0102040810204080ull) >> 56);
+}
+
+// Is pending candidate c blocked, i.e. is a pending candidate of higher priority within distance 4?
+// The 81 flags come in with two aligned 8-byte loads per row (all in flight together) and are reduced to
+// an 81-bit mask of pending neighbours (bit = row * 9 + column of the 9x9 square); their energies are
+// then fetched 8 at a time, stopping at the first one of higher priority.
+__device__ bool blocked(const Args& A, int64_t c) {
+  const int w = static_cast<int>(A.w), h = static_cast<int>(A.h);
+  const int64_t ev = c / A.n, base = ev * A.n;
+  const int loc = static_cast<int>(c - base), cy = loc / w, cx = loc - cy * w;
+  const int x0 = max(0, cx - 4), len = min(w - 1, cx + 4) - x0 + 1, shift = x0 - (cx - 4);
+  uint64_t lo[9], hi[9];
+  int off[9];
+#pragma unroll
+  for (int r = 0; r < 9; ++r) {
+    const int y = cy - 4 + r;
+    lo[r] = hi[r] = 0;
+    off[r] = 0;
+    if (y >= 0 && y < h) {
+      const uintptr_t start = reinterpret_cast<uintptr_t>(A.flags + base + static_cast<int64_t>(y) * w + x0);
+      const uint64_t* al = reinterpret_cast<const uint64_t*>(start & ~uintptr_t(7));
+      off[r] = static_cast<int>(start & 7);
+      lo[r] = al[0];
+      hi[r] = al[1];  // the flags allocation is padded: this may read up to 15 bytes past the last cell
     }
+  }
+  uint32_t m[3] = {0, 0, 0};
+#pragma unroll
+  for (int r = 0; r < 9; ++r) {
+    uint32_t row = ((low_bits8(lo[r]) | (low_bits8(hi[r]) << 8)) >> off[r]) & ((1u << len) - 1u);
+    row <<= shift;  // into the 9-wide frame
+    if (r == 4) row &= ~(1u << 4);  // the candidate itself
+    const int b = r * 9;  // bits b .. b + 8 of the 81-bit mask
+    if (b < 32) {
+      m[0] |= row << b;
+      if (b + 9 > 32) m[1] |= row >> (32 - b);
+    } else if (b < 64) {
+      m[1] |= row << (b - 32);
+      if (b + 9 > 64) m[2] |= row >> (64 - b);
+    } else {
+      m[2] |= row << (b - 64);
+    }
+  }
+  const float ec = A.energy[c];
+  while (m[0] | m[1] | m[2]) {
+    int js[8];
+    float eq[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      int j = -1;
+      if (m[0]) {
+        j = __ffs(m[0]) - 1;
+        m[0] &= m[0] - 1;
+      } else if (m[1]) {
+        j = 31 + __ffs(m[1]);
+        m[1] &= m[1] - 1;
+      } else if (m[2]) {
+        j = 63 + __ffs(m[2]);
+        m[2] &= m[2] - 1;
+      }
+      js[u] = j;
+      eq[u] = j >= 0 ? A.energy[base + static_cast<int64_t>(cy - 4 + j / 9) * w + (cx - 4 + j % 9)] : 0.0f;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (js[u] >= 0 && (eq[u] > ec || (js[u] < 40 && eq[u] == ec))) return true;  // j < 40: smaller cell index
+  }
   return false;
 }
 
@@ -372,44 +441,9 @@ __global__ void __launch_bounds__(NT) check_kernel(Args A, int parity) {
   for (int64_t i0 = static_cast<int64_t>(blockIdx.x) * NT + (threadIdx.x & ~31); i0 < m; i0 += stride) {
     const int64_t i = i0 + lane;
     const bool have = i < m;
-    const int64_t k = have ? cur[i] : 0;
-    Cand& R = A.cand[k];
-    const longlong2 head = have ? *reinterpret_cast<const longlong2*>(&R) : make_longlong2(0, 0);
-    const int64_t c = head.x;
-    const bool pend = have && (A.flags[c] & PENDING);
-    bool ok = pend;
-    if (pend) {
-      const uint32_t n = static_cast<uint32_t>(static_cast<uint64_t>(head.y) & 0xffffffffu);
-      if (n == OVERFLOW) {
-        ok = !scan_blocked(A, c);
-      } else {
-        uint32_t j = static_cast<uint32_t>(static_cast<uint64_t>(head.y) >> 32);
-        const uint32_t j0 = j;
-        while (j < n) {  // 8 blocker flags in flight at a time, stop at the first pending one
-          const uint32_t j8 = j & ~7u;
-          const uint64_t ow = *reinterpret_cast<const uint64_t*>(&R.off[j8]);
-          uint8_t st[8];
-#pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            const uint32_t idx = j8 + u;
-            const int o = static_cast<int>((ow >> (8 * u)) & 0xff);
-            const int64_t q = c + static_cast<int64_t>(o / 9 - 4) * A.w + (o % 9 - 4);
-            st[u] = (idx >= j && idx < n) ? A.flags[q] : 0;
-          }
-          uint32_t hit = n;
-#pragma unroll
-          for (int u = 7; u >= 0; --u)
-            if (st[u] & PENDING) hit = j8 + u;
-          if (hit < n) {
-            ok = false;
-            j = hit;
-            break;
-          }
-          j = j8 + 8;
-        }
-        if (!ok && j != j0) R.cur = j;
-      }
-    }
+    const int64_t c = have ? cur[i] : 0;
+    const bool pend = have && (A.flags[c] & PENDING);  // most were consumed by the previous round
+    const bool ok = pend && !blocked(A, c);
     const bool wait = pend && !ok;
     const unsigned wm = __ballot_sync(0xffffffffu, wait), rm = __ballot_sync(0xffffffffu, ok);
     const unsigned below = (1u << lane) - 1u;
@@ -420,7 +454,7 @@ __global__ void __launch_bounds__(NT) check_kernel(Args A, int parity) {
     }
     wb = __shfl_sync(0xffffffffu, wb, 0);
     rb = __shfl_sync(0xffffffffu, rb, 0);
-    if (wait) nxt[wb + __popc(wm & below)] = k;
+    if (wait) nxt[wb + __popc(wm & below)] = c;
     if (ok) A.ready[rb + __popc(rm & below)] = c;
   }
   if (last_cta(&A.counters[C_DONE]) && threadIdx.x == 0) {
@@ -675,7 +709,7 @@ struct Handle {
 static size_t al256(size_t v) { return (v + 255) & ~size_t(255); }
 
 static size_t ws_bytes(int64_t cells, int64_t cand_cap, int64_t slot_cap, int nevents) {
-  return al256(static_cast<size_t>(cells)) + al256(static_cast<size_t>(cand_cap) * sizeof(Cand)) +
+  return al256(static_cast<size_t>(cells) + 16) +
          3 * al256(static_cast<size_t>(cand_cap) * 8) + al256(static_cast<size_t>(slot_cap) * sizeof(Slot)) +
          al256(static_cast<size_t>(slot_cap) * MAXC * 8) + al256(64) + al256(static_cast<size_t>(nevents + 1) * 8) +
          al256(static_cast<size_t>(slot_cap) * 8) + 3 * al256(static_cast<size_t>(nevents + 1) * 8);
@@ -684,8 +718,7 @@ static size_t ws_bytes(int64_t cells, int64_t cand_cap, int64_t slot_cap, int ne
 static void carve(Handle* H) {
   uint8_t* p = static_cast<uint8_t*>(H->ws.mem);
   Args& A = H->A;
-  A.flags = p; p += al256(static_cast<size_t>(H->ws.cells));
-  A.cand = reinterpret_cast<Cand*>(p); p += al256(static_cast<size_t>(H->ws.cand_cap) * sizeof(Cand));
+  A.flags = p; p += al256(static_cast<size_t>(H->ws.cells) + 16);  // + 16: blocked() reads whole words
   A.list[0] = reinterpret_cast<int64_t*>(p); p += al256(static_cast<size_t>(H->ws.cand_cap) * 8);
   A.list[1] = reinterpret_cast<int64_t*>(p); p += al256(static_cast<size_t>(H->ws.cand_cap) * 8);
   A.ready = reinterpret_cast<int64_t*>(p); p += al256(static_cast<size_t>(H->ws.cand_cap) * 8);
@@ -801,6 +834,7 @@ int sk_reco_run(int64_t w, int64_t h, int nevents, const float* energy, const fl
   const int tiles_x = static_cast<int>((w + reco::TX - 1) / reco::TX);
   const int tiles_per_event = tiles_x * static_cast<int>((h + reco::TY - 1) / reco::TY);
   const int cgrid = ds->sm_count * 8;
+  const bool vec = w % 4 == 0 && ((reinterpret_cast<uintptr_t>(energy) | reinterpret_cast<uintptr_t>(noise)) & 15) == 0;
   const int pgrid = reco::process_grid(ds, device);
   unsigned long long cnt[8] = {0};
   std::vector<unsigned long long> ec(nevents > 0 ? nevents : 1);
@@ -812,8 +846,12 @@ int sk_reco_run(int64_t w, int64_t h, int nevents, const float* energy, const fl
     }
     SK_TRY(cudaMemsetAsync(A.counters, 0, 64, s));
     SK_TRY(cudaMemsetAsync(A.event_count, 0, static_cast<size_t>(nevents + 1) * 8, s));
-    if (total) reco::tile_kernel<<<static_cast<unsigned>(nevents) * tiles_per_event, reco::NT, 0, s>>>(
-        A, tiles_x, tiles_per_event);
+    if (total && vec)
+      reco::tile_kernel<true><<<static_cast<unsigned>(nevents) * tiles_per_event, reco::NT, 0, s>>>(
+          A, tiles_x, tiles_per_event);
+    else if (total)
+      reco::tile_kernel<false><<<static_cast<unsigned>(nevents) * tiles_per_event, reco::NT, 0, s>>>(
+          A, tiles_x, tiles_per_event);
     reco::process_kernel<<<pgrid, reco::PNT, 0, s>>>(A);  // the candidates without blockers
     // rounds are queued without a host check in between (a round with nothing pending returns at once):
     // 6 (full events converge in 4-5), then 4 more at a time until nothing is pending
