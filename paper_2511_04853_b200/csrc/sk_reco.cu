@@ -59,10 +59,11 @@ struct Slot {  // one reconstructed particle, before ordering
   float key_e;     // priority: energy desc, then origin asc
 };
 
-// [0] candidates [1] ready seeds of this round [2] next round's list size [3] this round's list size
+// [1] ready seeds of this round [2] next round's list size [3] this round's list size
 // [4] slots taken [5] CTAs finished in the current kernel [6] rounds that saw work [7] contributors
-constexpr int C_NCAND = 0, C_READY = 1, C_NEXT = 2, C_CUR = 3, C_SLOTS = 4, C_DONE = 5, C_PASSES = 6,
-              C_CONTRIB = 7;
+// [8] the tile pass's list sizes: candidates without blockers (low 32 bits), the others (high 32 bits)
+constexpr int C_READY = 1, C_NEXT = 2, C_CUR = 3, C_SLOTS = 4, C_DONE = 5, C_PASSES = 6, C_CONTRIB = 7,
+              C_TILE = 8, NCOUNTERS = 16;
 
 struct Args {
   int64_t w, h, n;  // n = cells per event
@@ -91,15 +92,26 @@ constexpr int TX = 56, TY = 40, HALO = 4, HX = TX + 2 * HALO, HY = TY + 2 * HALO
 // the blockers collected with three ballots. Candidates without blockers are
 // ready for the first round, the others start the first pending list. Index
 // math inside an event is 32-bit (events hold fewer than 2^31 cells).
+// the 80 cells of a 9x9 square around its centre, nearest ring first, as offsets in the HX = 64 wide halo
+// tile (dy * 64 + dx; negative = a smaller cell index in the same event)
+__constant__ int16_t kRing[80] = {
+    -65, -64, -63, -1, 1, 63, 64, 65,
+    -130, -129, -128, -127, -126, -66, -62, -2, 2, 62, 66, 126, 127, 128, 129, 130,
+    -195, -194, -193, -192, -191, -190, -189, -131, -125, -67, -61, -3, 3, 61, 67, 125, 131, 189, 190, 191, 192,
+    193, 194, 195,
+    -260, -259, -258, -257, -256, -255, -254, -253, -252, -196, -188, -132, -124, -68, -60, -4, 4, 60, 68, 124,
+    132, 188, 196, 252, 253, 254, 255, 256, 257, 258, 259, 260};
+
 template <bool VEC>
-__global__ void __launch_bounds__(NT, 4) tile_kernel(Args A, int tiles_x, int tiles_per_event) {
+__global__ void __launch_bounds__(NT, 5) tile_kernel(Args A, int tiles_x, int tiles_per_event) {
   __shared__ __align__(16) float se[HY * HX];
   __shared__ __align__(16) uint8_t sc[HY * HX];
   __shared__ uint16_t cl[TX * TY];   // the tile's candidates (halo index)
   __shared__ uint16_t cls[TX * TY];  // their list (bit 15) and position in it
   __shared__ int s_cnt[NT / 32];
   __shared__ int s_nl[2];
-  __shared__ unsigned long long s_base, s_lb[2];
+  __shared__ int s_total;
+  __shared__ unsigned long long s_lb;
   const int ev = blockIdx.x / tiles_per_event;
   const int tile = blockIdx.x - ev * tiles_per_event;
   const int ty0 = (tile / tiles_x) * TY, tx0 = (tile % tiles_x) * TX;
@@ -197,11 +209,10 @@ __global__ void __launch_bounds__(NT, 4) tile_kernel(Args A, int tiles_x, int ti
       s_cnt[k] = t;
       t += v;
     }
-    s_base = t ? atomicAdd(&A.counters[C_NCAND], static_cast<unsigned long long>(t)) : 0ull;
-    s_lb[0] = static_cast<unsigned long long>(t);
+    s_total = t;
   }
   __syncthreads();
-  const int total = static_cast<int>(s_lb[0]);
+  const int total = s_total;
   if (!total) return;
   {
     int pos = s_cnt[wid] + incl - mine;
@@ -213,50 +224,46 @@ __global__ void __launch_bounds__(NT, 4) tile_kernel(Args A, int tiles_x, int ti
     }
   }
   __syncthreads();
-  // one thread per candidate: is it the top priority among the candidates of its 9x9 neighbourhood? The
-  // neighbourhood is walked ring by ring from the centre, every offset a constant, and the walk stops at
-  // the first candidate of higher priority (usually an adjacent one)
-  const int64_t cap = A.cand_cap;
-  for (int q = threadIdx.x; q < total; q += NT) {
-    const int hc = cl[q];
+  // is each candidate the top priority among the candidates of its 9x9 neighbourhood? Eight lanes per
+  // candidate walk the neighbourhood nearest ring first, 8 cells a step, and stop at the first candidate of
+  // higher priority (usually in the first ring): four candidates per warp, every warp busy
+  static_assert(HX == 64, "kRing assumes a 64-wide halo tile");
+  const int sub = lane & 7, grp = lane >> 3;
+  int ring[10];
+#pragma unroll
+  for (int it = 0; it < 10; ++it) ring[it] = kRing[it * 8 + sub];
+  for (int q0 = wid * 4; q0 < total; q0 += NT / 8) {
+    const int q = q0 + grp;
+    const bool have = q < total;
+    const int hc = have ? cl[q] : HALO * HX + HALO;
     const float ec = se[hc];
-    bool top = true;
+    bool top = have;
 #pragma unroll
-    for (int r = 1; r <= HALO && top; ++r)
-#pragma unroll
-      for (int dy = -r; dy <= r; ++dy)
-#pragma unroll
-        for (int dx = -r; dx <= r; ++dx) {
-          if (dy != -r && dy != r && dx != -r && dx != r) continue;  // ring r only
-          const int d = dy * HX + dx;
-          const bool before = dy < 0 || (dy == 0 && dx < 0);  // a smaller cell index in the same event
-          if (top && sc[hc + d]) {
-            const float eq = se[hc + d];
-            if (eq > ec || (before && eq == ec)) top = false;
-          }
-        }
-    if (static_cast<int64_t>(s_base) + q < cap) {
+    for (int it = 0; it < 10; ++it) {
+      const int d = ring[it];
+      const float eq = se[hc + d];
+      const bool blk = top && sc[hc + d] && (eq > ec || (d < 0 && eq == ec));
+      const unsigned b = __ballot_sync(0xffffffffu, blk);
+      if ((b >> (grp * 8)) & 0xffu) top = false;
+      if (!__any_sync(0xffffffffu, top)) break;
+    }
+    if (have && sub == 0) {
       const int which = top ? 0 : 1;  // 0: no blockers, ready for the first round
       cls[q] = static_cast<uint16_t>(atomicAdd(&s_nl[which], 1) | (which << 15));
     }
   }
   __syncthreads();
-  if (threadIdx.x < 2) {
-    const int c = s_nl[threadIdx.x];
-    s_lb[threadIdx.x] = c ? atomicAdd(&A.counters[threadIdx.x ? C_CUR : C_READY], static_cast<unsigned long long>(c))
-                          : 0ull;
-  }
+  if (threadIdx.x == 0)  // both lists' places with one atomic
+    s_lb = atomicAdd(&A.counters[C_TILE],
+                     static_cast<unsigned long long>(s_nl[1]) << 32 | static_cast<unsigned long long>(s_nl[0]));
   __syncthreads();
-  for (int q = threadIdx.x; q < total; q += NT) {  // no blockers: ready for the first round (cells);
-    const int64_t kk = static_cast<int64_t>(s_base) + q;  // the others: the first pending list (records)
-    if (kk >= cap) continue;
-    const int which = cls[q] >> 15, li = cls[q] & 0x7fff;
+  const int64_t cap = A.cand_cap;
+  for (int q = threadIdx.x; q < total; q += NT) {  // no blockers: ready for the first round; the others: the
+    const int which = cls[q] >> 15, li = cls[q] & 0x7fff;  // first pending list (cells, both)
+    const int64_t at = static_cast<int64_t>(which ? s_lb >> 32 : s_lb & 0xffffffffull) + li;
+    if (at >= cap) continue;  // over capacity: counted, the host grows the lists and runs again
     const int hc = cl[q], iy = hc / HX - HALO, ix = hc % HX - HALO;
-    const int64_t cell = base + (ty0 + iy) * w + tx0 + ix;
-    if (which)
-      A.list[0][s_lb[1] + li] = cell;
-    else
-      A.ready[s_lb[0] + li] = cell;
+    (which ? A.list[0] : A.ready)[at] = base + (ty0 + iy) * w + tx0 + ix;
   }
 }
 
@@ -469,11 +476,13 @@ __global__ void __launch_bounds__(NT) check_kernel(Args A, int parity) {
 // examines window cell (l / 5 - 2, l % 5 - 2) -- every load in one round trip,
 // the taken cells marked consumed, the contributor list written, the values
 // kept in shared memory -- then lane j adds up seed j's contributors.
-__global__ void __launch_bounds__(PNT) process_kernel(Args A) {
+__global__ void __launch_bounds__(PNT) process_kernel(Args A, int first) {
   __shared__ WinSmem W[PW];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   WinSmem& S = W[wid];
-  const int64_t nready = static_cast<int64_t>(A.counters[C_READY]);
+  // the first round's ready seeds come from the tile pass
+  const int64_t nready = first ? min(static_cast<int64_t>(A.counters[C_TILE] & 0xffffffffull), A.cand_cap)
+                               : static_cast<int64_t>(A.counters[C_READY]);
   const int64_t slot0 = static_cast<int64_t>(A.counters[C_SLOTS]);
   const int w = static_cast<int>(A.w), h = static_cast<int>(A.h);
   // seeds per warp batch: spread over every warp of the grid (the window step is serial per warp)
@@ -550,8 +559,9 @@ __global__ void __launch_bounds__(PNT) process_kernel(Args A) {
     __syncwarp();  // the window buffers are reused by the next batch
   }
   if (last_cta(&A.counters[C_DONE]) && threadIdx.x == 0) {
-    A.counters[C_SLOTS] += A.counters[C_READY];
+    A.counters[C_SLOTS] += nready;
     A.counters[C_READY] = 0;
+    if (first) A.counters[C_CUR] = min(static_cast<int64_t>(A.counters[C_TILE] >> 32), A.cand_cap);
     A.counters[C_DONE] = 0;
   }
 }
@@ -711,7 +721,7 @@ static size_t al256(size_t v) { return (v + 255) & ~size_t(255); }
 static size_t ws_bytes(int64_t cells, int64_t cand_cap, int64_t slot_cap, int nevents) {
   return al256(static_cast<size_t>(cells) + 16) +
          3 * al256(static_cast<size_t>(cand_cap) * 8) + al256(static_cast<size_t>(slot_cap) * sizeof(Slot)) +
-         al256(static_cast<size_t>(slot_cap) * MAXC * 8) + al256(64) + al256(static_cast<size_t>(nevents + 1) * 8) +
+         al256(static_cast<size_t>(slot_cap) * MAXC * 8) + al256(NCOUNTERS * 8) + al256(static_cast<size_t>(nevents + 1) * 8) +
          al256(static_cast<size_t>(slot_cap) * 8) + 3 * al256(static_cast<size_t>(nevents + 1) * 8);
 }
 
@@ -724,7 +734,7 @@ static void carve(Handle* H) {
   A.ready = reinterpret_cast<int64_t*>(p); p += al256(static_cast<size_t>(H->ws.cand_cap) * 8);
   A.slots = reinterpret_cast<Slot*>(p); p += al256(static_cast<size_t>(H->ws.slot_cap) * sizeof(Slot));
   A.contrib = reinterpret_cast<uint64_t*>(p); p += al256(static_cast<size_t>(H->ws.slot_cap) * MAXC * 8);
-  A.counters = reinterpret_cast<unsigned long long*>(p); p += al256(64);
+  A.counters = reinterpret_cast<unsigned long long*>(p); p += al256(NCOUNTERS * 8);
   A.event_count = reinterpret_cast<unsigned long long*>(p); p += al256(static_cast<size_t>(H->ws.nevents + 1) * 8);
   H->order = reinterpret_cast<int64_t*>(p); p += al256(static_cast<size_t>(H->ws.slot_cap) * 8);
   H->ev_off = reinterpret_cast<int64_t*>(p); p += al256(static_cast<size_t>(H->ws.nevents + 1) * 8);
@@ -812,7 +822,9 @@ int sk_reco_run(int64_t w, int64_t h, int nevents, const float* energy, const fl
                 const uint8_t* noisy, int device, uintptr_t stream, void** handle, int64_t* nparticles,
                 int* rounds) {
   if (!handle || w < 1 || h < 1 || nevents < 0) return set_error(SK_ERR_INVALID, "bad reconstruction arguments");
-  if (w * h >= (int64_t(1) << 31)) return set_error(SK_ERR_INVALID, "an event of %lld cells is too large", (long long)(w * h));
+  if (w * h >= (int64_t(1) << 31) || w * h * nevents >= (int64_t(1) << 32))
+    return set_error(SK_ERR_INVALID, "%d events of %lld cells: too many cells for one run", nevents,
+                     static_cast<long long>(w * h));
   DeviceState* ds = nullptr;
   int rc = device_state(device, &ds);
   if (rc) return rc;
@@ -836,7 +848,7 @@ int sk_reco_run(int64_t w, int64_t h, int nevents, const float* energy, const fl
   const int cgrid = ds->sm_count * 8;
   const bool vec = w % 4 == 0 && ((reinterpret_cast<uintptr_t>(energy) | reinterpret_cast<uintptr_t>(noise)) & 15) == 0;
   const int pgrid = reco::process_grid(ds, device);
-  unsigned long long cnt[8] = {0};
+  unsigned long long cnt[reco::NCOUNTERS] = {0};
   std::vector<unsigned long long> ec(nevents > 0 ? nevents : 1);
   for (int attempt = 0;; ++attempt) {
     rc = reco::acquire_ws(H, cand_cap, slot_cap, s);
@@ -844,7 +856,7 @@ int sk_reco_run(int64_t w, int64_t h, int nevents, const float* energy, const fl
       delete H;
       return rc;
     }
-    SK_TRY(cudaMemsetAsync(A.counters, 0, 64, s));
+    SK_TRY(cudaMemsetAsync(A.counters, 0, reco::NCOUNTERS * 8, s));
     SK_TRY(cudaMemsetAsync(A.event_count, 0, static_cast<size_t>(nevents + 1) * 8, s));
     if (total && vec)
       reco::tile_kernel<true><<<static_cast<unsigned>(nevents) * tiles_per_event, reco::NT, 0, s>>>(
@@ -852,38 +864,39 @@ int sk_reco_run(int64_t w, int64_t h, int nevents, const float* energy, const fl
     else if (total)
       reco::tile_kernel<false><<<static_cast<unsigned>(nevents) * tiles_per_event, reco::NT, 0, s>>>(
           A, tiles_x, tiles_per_event);
-    reco::process_kernel<<<pgrid, reco::PNT, 0, s>>>(A);  // the candidates without blockers
+    reco::process_kernel<<<pgrid, reco::PNT, 0, s>>>(A, 1);  // the candidates without blockers
     // rounds are queued without a host check in between (a round with nothing pending returns at once):
     // 6 (full events converge in 4-5), then 4 more at a time until nothing is pending
     int launched = 0;
     for (;;) {
       for (int k = 0; k < (launched ? 4 : 6); ++k, ++launched) {
         reco::check_kernel<<<cgrid, reco::NT, 0, s>>>(A, launched & 1);
-        reco::process_kernel<<<pgrid, reco::PNT, 0, s>>>(A);
+        reco::process_kernel<<<pgrid, reco::PNT, 0, s>>>(A, 0);
       }
       SK_TRY(cudaGetLastError());
       SK_TRY(cudaMemcpyAsync(cnt, A.counters, sizeof(cnt), cudaMemcpyDeviceToHost, s));
       if (nevents) SK_TRY(cudaMemcpyAsync(ec.data(), A.event_count, nevents * 8, cudaMemcpyDeviceToHost, s));
       SK_TRY(cudaStreamSynchronize(s));
-      const bool over = static_cast<int64_t>(cnt[reco::C_NCAND]) > A.cand_cap ||
-                        static_cast<int64_t>(cnt[reco::C_SLOTS]) > A.slot_cap;
+      const int64_t n_top = static_cast<int64_t>(cnt[reco::C_TILE] & 0xffffffffull);
+      const int64_t n_rest = static_cast<int64_t>(cnt[reco::C_TILE] >> 32);
+      const bool over = n_top > A.cand_cap || n_rest > A.cand_cap || static_cast<int64_t>(cnt[reco::C_SLOTS]) > A.slot_cap;
       if (over || cnt[reco::C_CUR] == 0) break;
-      if (launched > static_cast<int>(std::min<unsigned long long>(cnt[reco::C_NCAND], 1u << 30)) + 16) {
+      if (launched > static_cast<int>(std::min<int64_t>(n_top + n_rest, 1 << 30)) + 16) {
         reco::release_ws(H, s);  // every round decides at least the highest-priority pending seed
         delete H;
         return set_error(SK_ERR_CUDA, "reconstruction made no progress");
       }
     }
-    if (static_cast<int64_t>(cnt[reco::C_NCAND]) <= A.cand_cap &&
-        static_cast<int64_t>(cnt[reco::C_SLOTS]) <= A.slot_cap)
-      break;
+    const int64_t n_top = static_cast<int64_t>(cnt[reco::C_TILE] & 0xffffffffull);
+    const int64_t n_rest = static_cast<int64_t>(cnt[reco::C_TILE] >> 32);
+    if (n_top <= A.cand_cap && n_rest <= A.cand_cap && static_cast<int64_t>(cnt[reco::C_SLOTS]) <= A.slot_cap) break;
     if (attempt) {  // cannot happen: the second attempt has room for every candidate
       reco::release_ws(H, s);
       delete H;
       return set_error(SK_ERR_CUDA, "reconstruction workspace overflow");
     }
-    cand_cap = std::max<int64_t>(cand_cap, static_cast<int64_t>(cnt[reco::C_NCAND]));
-    slot_cap = std::max<int64_t>(slot_cap, cand_cap);  // at most one slot per candidate
+    cand_cap = std::max({cand_cap, n_top, n_rest});
+    slot_cap = std::max<int64_t>(slot_cap, n_top + n_rest);  // at most one slot per candidate
   }
   H->counts.assign(nevents, 0);
   int64_t np = 0;
