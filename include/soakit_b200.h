@@ -267,25 +267,40 @@ int sk_sensor_generate(int64_t w, int64_t h, const uint64_t* seeds, int nevents,
 /* Particle reconstruction (reconstruct_arrays, detector/reconstruct.py:53-136)
    over nevents calibrated events of w x h cells (energy/noise/type/noisy
    planes, event-major). Round-synchronous parallel greedy over the seeds'
-   blocker lists: same particles in the same order as the reference's
-   sequential seed walk. Returns an opaque
-   handle with the particles and per-event counts; sk_reco_write then writes
-   them in reference order into per-field planes (slot planes of the 4-wide
-   arrays as separate pointers), the per-particle contributor counts and
-   offsets into a contributor pool owned by the handle (*sensor_pool, u64
-   cell indices) for the jagged packer; sk_reco_free releases everything. */
+   blockers: same particles in the same order as the reference's sequential
+   seed walk. The output is per_field planes of a Particle collection
+   (reconstruct.py:172-194): the attribute planes (the 4-wide arrays as 4 slot
+   planes each), the sensor lists' prefix plane (particle_capacity + 1 entries
+   of sensor_prefix_type) and pool (u64 cell indices inside the event). */
+typedef struct sk_reco_out {
+  float* energy;
+  float* x;
+  float* y;
+  uint64_t* origin;
+  float* x_variance;
+  float* y_variance;
+  float* significance[4];
+  float* e_contribution[4];
+  uint8_t* noisy_count[4];
+  void* sensor_prefix;
+  int sensor_prefix_type;
+  uint64_t* sensor_pool;
+  int64_t particle_capacity; /* rows of each particle plane */
+  int64_t pool_capacity;     /* cells of sensor_pool */
+} sk_reco_out;
+/* Runs the reconstruction; with `out`, the write into it is queued behind the
+   rounds, and one host synchronisation covers both. *written = 1 when the
+   particles and their sensor lists fit out's capacities; otherwise grow the
+   output to *nparticles / *ncontributors and call sk_reco_write. The handle
+   keeps the particles and per-event counts until sk_reco_free. */
 int sk_reco_run(int64_t w, int64_t h, int nevents, const float* energy,
                 const float* noise, const uint8_t* type, const uint8_t* noisy,
-                int device, uintptr_t stream, void** handle, int64_t* nparticles,
-                int* rounds);
-/* Particles and contributor cells (the total of the per-particle sensor lists) of a run. */
-int sk_reco_sizes(void* handle, int64_t* nparticles, int64_t* ncontributors);
+                const sk_reco_out* out, int device, uintptr_t stream, void** handle,
+                int64_t* nparticles, int64_t* ncontributors, int* rounds,
+                int* written);
 int sk_reco_event_counts(void* handle, int64_t* counts);
-int sk_reco_write(void* handle, float* energy, float* x, float* y, uint64_t* origin,
-                  float* x_variance, float* y_variance, float* const* significance,
-                  float* const* e_contribution, uint8_t* const* noisy_count,
-                  int32_t* sensor_lens, int64_t* sensor_offsets,
-                  const uint64_t** sensor_pool, uintptr_t stream);
+/* Queue the write into an output large enough for the run (SK_ERR_RANGE otherwise). */
+int sk_reco_write(void* handle, const sk_reco_out* out, uintptr_t stream);
 int sk_reco_free(void* handle, uintptr_t stream);
 
 /* ---- synthetic inputs ------------------------------------------------------- */

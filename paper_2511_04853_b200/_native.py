@@ -62,6 +62,26 @@ class ConvDesc(C.Structure):
     ]
 
 
+class RecoOut(C.Structure):
+    """sk_reco_out: the per_field planes a reconstruction writes into."""
+    _fields_ = [
+        ("energy", C.c_void_p),
+        ("x", C.c_void_p),
+        ("y", C.c_void_p),
+        ("origin", C.c_void_p),
+        ("x_variance", C.c_void_p),
+        ("y_variance", C.c_void_p),
+        ("significance", C.c_void_p * 4),
+        ("e_contribution", C.c_void_p * 4),
+        ("noisy_count", C.c_void_p * 4),
+        ("sensor_prefix", C.c_void_p),
+        ("sensor_prefix_type", C.c_int),
+        ("sensor_pool", C.c_void_p),
+        ("particle_capacity", C.c_int64),
+        ("pool_capacity", C.c_int64),
+    ]
+
+
 _P = C.c_void_p
 _U = C.c_size_t
 _I = C.c_int
@@ -112,11 +132,10 @@ _SIGNATURES = {
     "sk_sensor_convert_calibrate": [C.POINTER(ConvDesc), _I, _I, _I, _I, _I, _I, _I, _P, _I, _U],
     "sk_sensor_generate": [_I64, _I64, C.POINTER(C.c_uint64), _I, _I64, C.POINTER(C.c_double), _P, _P, _P, _P, _P,
                            _P, _P, _P, _U],
-    "sk_reco_run": [_I64, _I64, _I, _P, _P, _P, _P, _I, _U, C.POINTER(_P), C.POINTER(_I64), C.POINTER(_I)],
-    "sk_reco_sizes": [_P, C.POINTER(_I64), C.POINTER(_I64)],
+    "sk_reco_run": [_I64, _I64, _I, _P, _P, _P, _P, C.POINTER(RecoOut), _I, _U, C.POINTER(_P), C.POINTER(_I64),
+                    C.POINTER(_I64), C.POINTER(_I), C.POINTER(_I)],
     "sk_reco_event_counts": [_P, C.POINTER(_I64)],
-    "sk_reco_write": [_P, _P, _P, _P, _P, _P, _P, C.POINTER(_P), C.POINTER(_P), C.POINTER(_P), _P, _P,
-                      C.POINTER(_P), _U],
+    "sk_reco_write": [_P, C.POINTER(RecoOut), _U],
     "sk_reco_free": [_P, _U],
     "sk_fill_random": [_P, _SZ, C.c_uint64, C.c_uint64, _U],
     "sk_compare_bytes": [_P, _P, _SZ, _P, _U],

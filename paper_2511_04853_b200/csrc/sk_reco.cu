@@ -45,6 +45,30 @@ namespace reco {
 constexpr int NT = 256;
 constexpr int MAXC = 25;  // contributors per particle (5x5 window)
 
+// Programmatic dependent launch: every kernel of a run is launched with programmatic stream
+// serialisation, waits for its predecessor's results (griddepcontrol.wait) before it reads anything and
+// lets its successor be scheduled right away, so the launch gap between the many short kernels of a
+// reconstruction overlaps the previous kernel's tail.
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+template <class... KArgs, class... Args>
+static cudaError_t launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 // per-cell flags
 constexpr uint8_t PENDING = 1;   // a candidate not decided yet
 constexpr uint8_t CONSUMED = 2;  // taken by a particle (a consumed candidate is decided)
@@ -104,6 +128,7 @@ __constant__ int16_t kRing[80] = {
 
 template <bool VEC>
 __global__ void __launch_bounds__(NT, 5) tile_kernel(Args A, int tiles_x, int tiles_per_event) {
+  pdl_enter();
   __shared__ __align__(16) float se[HY * HX];
   __shared__ __align__(16) uint8_t sc[HY * HX];
   __shared__ uint16_t cl[TX * TY];   // the tile's candidates (halo index)
@@ -440,8 +465,10 @@ __device__ __forceinline__ bool last_cta(unsigned long long* done) {
 }
 
 __global__ void __launch_bounds__(NT) check_kernel(Args A, int parity) {
+  pdl_enter();
   const int lane = threadIdx.x & 31;
   const int64_t m = static_cast<int64_t>(A.counters[C_CUR]);
+  if (m == 0) return;  // converged: nothing to check, nothing to book
   const int64_t* cur = A.list[parity];
   int64_t* nxt = A.list[parity ^ 1];
   const int64_t stride = static_cast<int64_t>(gridDim.x) * NT;
@@ -477,12 +504,14 @@ __global__ void __launch_bounds__(NT) check_kernel(Args A, int parity) {
 // the taken cells marked consumed, the contributor list written, the values
 // kept in shared memory -- then lane j adds up seed j's contributors.
 __global__ void __launch_bounds__(PNT) process_kernel(Args A, int first) {
+  pdl_enter();
   __shared__ WinSmem W[PW];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   WinSmem& S = W[wid];
   // the first round's ready seeds come from the tile pass
   const int64_t nready = first ? min(static_cast<int64_t>(A.counters[C_TILE] & 0xffffffffull), A.cand_cap)
                                : static_cast<int64_t>(A.counters[C_READY]);
+  if (nready == 0 && !first) return;  // an empty round
   const int64_t slot0 = static_cast<int64_t>(A.counters[C_SLOTS]);
   const int w = static_cast<int>(A.w), h = static_cast<int>(A.h);
   // seeds per warp batch: spread over every warp of the grid (the window step is serial per warp)
@@ -571,6 +600,7 @@ __global__ void __launch_bounds__(PNT) process_kernel(Args A, int first) {
 // event offsets: exclusive prefix of the per-event particle counts (one CTA, a thread per event run)
 __global__ void __launch_bounds__(NT) event_offsets_kernel(const unsigned long long* counts, int nevents,
                                                             int64_t* off, int64_t* cnt, unsigned long long* cursor) {
+  pdl_enter();
   __shared__ int64_t s_part[NT / 32];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int per = (nevents + NT - 1) / NT, lo = min(nevents, static_cast<int>(threadIdx.x) * per),
@@ -597,8 +627,14 @@ __global__ void __launch_bounds__(NT) event_offsets_kernel(const unsigned long l
 }
 
 // bucket particles by event, then rank by priority inside the event
-__global__ void bucket_kernel(const Slot* slots, int64_t np, const int64_t* event_off,
-                              unsigned long long* cursor, int64_t* order) {
+__global__ void bucket_kernel(const Slot* slots, const unsigned long long* nslots, int64_t cap,
+                              const int64_t* event_off, unsigned long long* cursor, int64_t* order, int32_t* lens,
+                              int64_t nlens) {
+  pdl_enter();
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * NT + threadIdx.x; i < nlens;
+       i += static_cast<int64_t>(gridDim.x) * NT)
+    lens[i] = 0;  // the write sets the particles' contributor counts; the rest of the capacity packs nothing
+  const int64_t np = min(static_cast<int64_t>(*nslots), cap);
   for (int64_t p = static_cast<int64_t>(blockIdx.x) * NT + threadIdx.x; p < np;
        p += static_cast<int64_t>(gridDim.x) * NT) {
     const int e = slots[p].event;
@@ -626,7 +662,9 @@ constexpr int RANK_SPLIT = 4;                 // threads per particle in the ran
 constexpr int RANK_PER_CTA = NT / RANK_SPLIT;  // particles ranked per CTA
 
 __global__ void __launch_bounds__(NT) write_kernel(const Slot* slots, const int64_t* event_off,
-                                                   const int64_t* event_cnt, const int64_t* order, OutArgs O) {
+                                                   const int64_t* event_cnt, const int64_t* order, OutArgs O,
+                                                   int64_t cap) {
+  pdl_enter();
   __shared__ float ke[RANK_SMEM];
   __shared__ int64_t ko[RANK_SMEM];
   const int64_t ev = blockIdx.x;
@@ -663,8 +701,8 @@ __global__ void __launch_bounds__(NT) write_kernel(const Slot* slots, const int6
     }
 #pragma unroll
     for (int o = 1; o < RANK_SPLIT; o <<= 1) rank += __shfl_xor_sync(0xffffffffu, rank, o);
-    if (!have || q) continue;
     const int64_t o = b + rank;
+    if (!have || q || o >= cap) continue;  // (past the output's capacity: the caller grows it, writes again)
     O.energy[o] = S.energy;
     O.x[o] = S.x;
     O.y[o] = S.y;
@@ -693,6 +731,8 @@ struct Workspace {
   size_t bytes = 0;
   int64_t cells = 0, cand_cap = 0, slot_cap = 0;
   int nevents = 0;
+  void* aux = nullptr;  // the write's temporaries: contributor counts / offsets, the packer's scratch
+  size_t aux_bytes = 0;
 };
 
 static std::mutex g_ws_mu;
@@ -770,8 +810,12 @@ static int acquire_ws(Handle* H, int64_t cand_cap, int64_t slot_cap, cudaStream_
   }
   if (W.mem) cudaFreeAsync(W.mem, s);
   cudaEvent_t ev = W.released;
+  void* aux = W.aux;
+  const size_t aux_bytes = W.aux_bytes;
   W = Workspace();
   W.released = ev;
+  W.aux = aux;
+  W.aux_bytes = aux_bytes;
   const size_t bytes = ws_bytes(cells, cand_cap, slot_cap, nev);
   cudaError_t e = cudaMallocAsync(&W.mem, bytes, s);
   if (e != cudaSuccess) {
@@ -798,6 +842,7 @@ static void release_ws(Handle* H, cudaStream_t s) {
     g_ws_busy[H->device] = false;
   } else {
     cudaFreeAsync(H->ws.mem, s);
+    if (H->ws.aux) cudaFreeAsync(H->ws.aux, s);
     if (H->ws.released) cudaEventDestroy(H->ws.released);
   }
   H->ws = Workspace();
@@ -811,6 +856,55 @@ static int process_grid(const DeviceState* ds, int device) {
   return ds->sm_count * occ;
 }
 
+// Queue the write of the particles (reference order) and of their contributor lists into `out`: event
+// offsets, bucketing and ranking on the device, then the jagged packer over `out`'s whole particle capacity
+// (contributor counts past the particles are zero). Sizes are read on the device, so this can be queued
+// before the host knows them; whatever does not fit the capacities is dropped and reported by the caller.
+static int queue_write(Handle* H, const sk_reco_out* out, cudaStream_t s, const DeviceState* ds, unsigned chunks) {
+  const int64_t pcap = std::max<int64_t>(out->particle_capacity, 0);
+  size_t scan = 0;
+  sk_jagged_scratch_bytes(pcap, &scan);
+  const size_t scratch = al256(scan) + static_cast<size_t>((std::max<int64_t>(out->pool_capacity, 0) + 255) / 256 + 1) * 8;
+  const size_t need = al256(static_cast<size_t>(pcap) * 4) + al256(static_cast<size_t>(pcap) * 8) + al256(16) + scratch;
+  Workspace& W = H->ws;
+  if (W.aux_bytes < need) {
+    if (W.aux) cudaFreeAsync(W.aux, s);
+    W.aux = nullptr;
+    W.aux_bytes = 0;
+    cudaError_t e = cudaMallocAsync(&W.aux, need, s);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync(reconstruction write scratch)");
+    W.aux_bytes = need;
+  }
+  uint8_t* p = static_cast<uint8_t*>(W.aux);
+  int32_t* lens = reinterpret_cast<int32_t*>(p); p += al256(static_cast<size_t>(pcap) * 4);
+  int64_t* offs = reinterpret_cast<int64_t*>(p); p += al256(static_cast<size_t>(pcap) * 8);
+  int64_t* total = reinterpret_cast<int64_t*>(p); p += al256(16);
+  void* pack_scratch = p;
+  SK_TRY(launch(event_offsets_kernel, dim3(1), dim3(NT), s, H->A.event_count, H->nevents, H->ev_off, H->ev_cnt,
+                H->cursor));
+  SK_TRY(launch(bucket_kernel, dim3(ds->sm_count * 4), dim3(NT), s, H->A.slots, &H->A.counters[C_SLOTS],
+                H->A.slot_cap, H->ev_off, H->cursor, H->order, lens, pcap));
+  OutArgs O;
+  O.energy = out->energy; O.x = out->x; O.y = out->y; O.xvar = out->x_variance; O.yvar = out->y_variance;
+  O.origin = out->origin;
+  for (int t = 0; t < 4; ++t) {
+    O.sig[t] = out->significance[t];
+    O.ec[t] = out->e_contribution[t];
+    O.nc[t] = out->noisy_count[t];
+  }
+  O.lens = lens;
+  O.offsets = offs;
+  if (H->nevents && chunks)
+    SK_TRY(launch(write_kernel, dim3(H->nevents, chunks), dim3(NT), s, H->A.slots, H->ev_off, H->ev_cnt, H->order, O,
+                  pcap));
+  const int64_t field_off = 0;
+  const int32_t field_size = 8;
+  void* dst = out->sensor_pool;
+  return sk_jagged_pack(pcap, lens, SK_I32, out->sensor_prefix, out->sensor_prefix_type, offs, H->A.contrib,
+                        H->A.slot_cap * MAXC, 8, 1, &field_off, &field_size, &dst, out->pool_capacity, pack_scratch,
+                        scratch, total, reinterpret_cast<uintptr_t>(s));
+}
+
 }  // namespace reco
 }  // namespace sk
 
@@ -819,12 +913,13 @@ using namespace sk;
 extern "C" {
 
 int sk_reco_run(int64_t w, int64_t h, int nevents, const float* energy, const float* noise, const uint8_t* type,
-                const uint8_t* noisy, int device, uintptr_t stream, void** handle, int64_t* nparticles,
-                int* rounds) {
+                const uint8_t* noisy, const sk_reco_out* out, int device, uintptr_t stream, void** handle,
+                int64_t* nparticles, int64_t* ncontributors, int* rounds, int* written) {
   if (!handle || w < 1 || h < 1 || nevents < 0) return set_error(SK_ERR_INVALID, "bad reconstruction arguments");
   if (w * h >= (int64_t(1) << 31) || w * h * nevents >= (int64_t(1) << 32))
     return set_error(SK_ERR_INVALID, "%d events of %lld cells: too many cells for one run", nevents,
                      static_cast<long long>(w * h));
+  if (written) *written = 0;
   DeviceState* ds = nullptr;
   int rc = device_state(device, &ds);
   if (rc) return rc;
@@ -850,6 +945,11 @@ int sk_reco_run(int64_t w, int64_t h, int nevents, const float* energy, const fl
   const int pgrid = reco::process_grid(ds, device);
   unsigned long long cnt[reco::NCOUNTERS] = {0};
   std::vector<unsigned long long> ec(nevents > 0 ? nevents : 1);
+  auto fail = [&](int code) {
+    reco::release_ws(H, s);
+    delete H;
+    return code;
+  };
   for (int attempt = 0;; ++attempt) {
     rc = reco::acquire_ws(H, cand_cap, slot_cap, s);
     if (rc) {
@@ -858,22 +958,22 @@ int sk_reco_run(int64_t w, int64_t h, int nevents, const float* energy, const fl
     }
     SK_TRY(cudaMemsetAsync(A.counters, 0, reco::NCOUNTERS * 8, s));
     SK_TRY(cudaMemsetAsync(A.event_count, 0, static_cast<size_t>(nevents + 1) * 8, s));
-    if (total && vec)
-      reco::tile_kernel<true><<<static_cast<unsigned>(nevents) * tiles_per_event, reco::NT, 0, s>>>(
-          A, tiles_x, tiles_per_event);
-    else if (total)
-      reco::tile_kernel<false><<<static_cast<unsigned>(nevents) * tiles_per_event, reco::NT, 0, s>>>(
-          A, tiles_x, tiles_per_event);
-    reco::process_kernel<<<pgrid, reco::PNT, 0, s>>>(A, 1);  // the candidates without blockers
+    const dim3 tgrid(static_cast<unsigned>(nevents) * tiles_per_event);
+    if (total) SK_TRY(reco::launch(vec ? reco::tile_kernel<true> : reco::tile_kernel<false>, tgrid, dim3(reco::NT), s, A,
+                                   tiles_x, tiles_per_event));
+    SK_TRY(reco::launch(reco::process_kernel, dim3(pgrid), dim3(reco::PNT), s, A, 1));  // candidates without blockers
     // rounds are queued without a host check in between (a round with nothing pending returns at once):
-    // 6 (full events converge in 4-5), then 4 more at a time until nothing is pending
+    // 6 (full events converge in 4-5), then 4 more at a time until nothing is pending. The write into `out`
+    // is queued behind them, so one host synchronisation covers the whole reconstruction.
     int launched = 0;
     for (;;) {
-      for (int k = 0; k < (launched ? 4 : 6); ++k, ++launched) {
-        reco::check_kernel<<<cgrid, reco::NT, 0, s>>>(A, launched & 1);
-        reco::process_kernel<<<pgrid, reco::PNT, 0, s>>>(A, 0);
+      const int batch = launched ? 4 : 6;
+      for (int k = 0; k < batch; ++k, ++launched) {
+        SK_TRY(reco::launch(reco::check_kernel, dim3(cgrid), dim3(reco::NT), s, A, launched & 1));
+        SK_TRY(reco::launch(reco::process_kernel, dim3(pgrid), dim3(reco::PNT), s, A, 0));
       }
       SK_TRY(cudaGetLastError());
+      if (out && (rc = reco::queue_write(H, out, s, ds, 8))) return fail(rc);
       SK_TRY(cudaMemcpyAsync(cnt, A.counters, sizeof(cnt), cudaMemcpyDeviceToHost, s));
       if (nevents) SK_TRY(cudaMemcpyAsync(ec.data(), A.event_count, nevents * 8, cudaMemcpyDeviceToHost, s));
       SK_TRY(cudaStreamSynchronize(s));
@@ -881,20 +981,13 @@ int sk_reco_run(int64_t w, int64_t h, int nevents, const float* energy, const fl
       const int64_t n_rest = static_cast<int64_t>(cnt[reco::C_TILE] >> 32);
       const bool over = n_top > A.cand_cap || n_rest > A.cand_cap || static_cast<int64_t>(cnt[reco::C_SLOTS]) > A.slot_cap;
       if (over || cnt[reco::C_CUR] == 0) break;
-      if (launched > static_cast<int>(std::min<int64_t>(n_top + n_rest, 1 << 30)) + 16) {
-        reco::release_ws(H, s);  // every round decides at least the highest-priority pending seed
-        delete H;
-        return set_error(SK_ERR_CUDA, "reconstruction made no progress");
-      }
+      if (launched > static_cast<int>(std::min<int64_t>(n_top + n_rest, 1 << 30)) + 16)
+        return fail(set_error(SK_ERR_CUDA, "reconstruction made no progress"));  // a round decides >= 1 seed
     }
     const int64_t n_top = static_cast<int64_t>(cnt[reco::C_TILE] & 0xffffffffull);
     const int64_t n_rest = static_cast<int64_t>(cnt[reco::C_TILE] >> 32);
     if (n_top <= A.cand_cap && n_rest <= A.cand_cap && static_cast<int64_t>(cnt[reco::C_SLOTS]) <= A.slot_cap) break;
-    if (attempt) {  // cannot happen: the second attempt has room for every candidate
-      reco::release_ws(H, s);
-      delete H;
-      return set_error(SK_ERR_CUDA, "reconstruction workspace overflow");
-    }
+    if (attempt) return fail(set_error(SK_ERR_CUDA, "reconstruction workspace overflow"));  // cannot happen
     cand_cap = std::max({cand_cap, n_top, n_rest});
     slot_cap = std::max<int64_t>(slot_cap, n_top + n_rest);  // at most one slot per candidate
   }
@@ -907,22 +1000,13 @@ int sk_reco_run(int64_t w, int64_t h, int nevents, const float* energy, const fl
   H->np = np;
   H->nslots = static_cast<int64_t>(cnt[reco::C_SLOTS]);
   H->ncontrib = static_cast<int64_t>(cnt[reco::C_CONTRIB]);
-  if (H->nslots != np) {  // a slot without a particle: the contributor pool would not match the counts
-    reco::release_ws(H, s);
-    delete H;
-    return set_error(SK_ERR_CUDA, "reconstruction left particle slots empty");
-  }
-  *nparticles = H->np;
-  if (rounds) *rounds = static_cast<int>(cnt[reco::C_PASSES]);
-  *handle = H;
-  return SK_OK;
-}
-
-int sk_reco_sizes(void* handle, int64_t* nparticles, int64_t* ncontributors) {
-  auto* H = static_cast<reco::Handle*>(handle);
-  if (!H) return set_error(SK_ERR_INVALID, "null handle");
+  if (H->nslots != np)  // a slot without a particle: the contributor pool would not match the counts
+    return fail(set_error(SK_ERR_CUDA, "reconstruction left particle slots empty"));
   if (nparticles) *nparticles = H->np;
   if (ncontributors) *ncontributors = H->ncontrib;
+  if (rounds) *rounds = static_cast<int>(cnt[reco::C_PASSES]);
+  if (written) *written = out && H->np <= out->particle_capacity && H->ncontrib <= out->pool_capacity;
+  *handle = H;
   return SK_OK;
 }
 
@@ -933,40 +1017,22 @@ int sk_reco_event_counts(void* handle, int64_t* counts) {
   return SK_OK;
 }
 
-int sk_reco_write(void* handle, float* energy, float* x, float* y, uint64_t* origin, float* x_variance,
-                  float* y_variance, float* const* significance, float* const* e_contribution,
-                  uint8_t* const* noisy_count, int32_t* sensor_lens, int64_t* sensor_offsets,
-                  const uint64_t** sensor_pool, uintptr_t stream) {
+int sk_reco_write(void* handle, const sk_reco_out* out, uintptr_t stream) {
   auto* H = static_cast<reco::Handle*>(handle);
-  if (!H) return set_error(SK_ERR_INVALID, "null handle");
+  if (!H || !out) return set_error(SK_ERR_INVALID, "null handle or output");
+  if (out->particle_capacity < H->np || out->pool_capacity < H->ncontrib)
+    return set_error(SK_ERR_RANGE, "output holds %lld particles / %lld contributors, the run has %lld / %lld",
+                     static_cast<long long>(out->particle_capacity), static_cast<long long>(out->pool_capacity),
+                     static_cast<long long>(H->np), static_cast<long long>(H->ncontrib));
   DeviceState* ds = nullptr;
   int rc = device_state(H->device, &ds);
   if (rc) return rc;
   cudaStream_t s = resolve_stream(H->device, stream);
-  if (sensor_pool) *sensor_pool = H->A.contrib;
-  if (H->np == 0) return SK_OK;
-  // event offsets on the device (no host round trip), then bucket the slots by event
-  reco::event_offsets_kernel<<<1, reco::NT, 0, s>>>(H->A.event_count, H->nevents, H->ev_off, H->ev_cnt, H->cursor);
-  const int bgrid =
-      std::max(1, std::min<int>(ds->sm_count * 8, static_cast<int>((H->nslots + reco::NT - 1) / reco::NT)));
-  reco::bucket_kernel<<<bgrid, reco::NT, 0, s>>>(H->A.slots, H->nslots, H->ev_off, H->cursor, H->order);
-  reco::OutArgs O;
-  O.energy = energy; O.x = x; O.y = y; O.xvar = x_variance; O.yvar = y_variance; O.origin = origin;
-  for (int t = 0; t < 4; ++t) {
-    O.sig[t] = significance[t];
-    O.ec[t] = e_contribution[t];
-    O.nc[t] = noisy_count[t];
-  }
-  O.lens = sensor_lens;
-  O.offsets = sensor_offsets;
   int64_t mmax = 0;
   for (int i = 0; i < H->nevents; ++i) mmax = std::max(mmax, H->counts[i]);
   const unsigned chunks =
       static_cast<unsigned>(std::min<int64_t>((mmax + reco::RANK_PER_CTA - 1) / reco::RANK_PER_CTA, 65535));
-  if (H->nevents && chunks)
-    reco::write_kernel<<<dim3(H->nevents, chunks), reco::NT, 0, s>>>(H->A.slots, H->ev_off, H->ev_cnt, H->order, O);
-  SK_TRY(cudaGetLastError());
-  return SK_OK;
+  return reco::queue_write(H, out, s, ds, std::max(chunks, 1u));
 }
 
 int sk_reco_free(void* handle, uintptr_t stream) {

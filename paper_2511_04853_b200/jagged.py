@@ -160,40 +160,6 @@ def _invalid_segments(bad: int) -> BoundsError:
     return BoundsError(f"{bad} segment(s) have a negative length or lie outside the source pool")
 
 
-def pack_known_total(coll, path: str, lens: DeviceArray, src_offsets: DeviceArray, src_pool_ptr: int,
-                     src_members: int, total: int) -> None:
-    """Fill single-leaf jagged vector `path` of a device-resident collection
-    from device inputs the library produced itself, whose member total is
-    known in advance (the particle reconstruction's contributor lists): the
-    pool is sized first and the fused scan + gather is only queued -- no
-    validation pass and no read back of the total, so nothing waits on the
-    device. Stream-ordered like the launches before it."""
-    lay = coll.layout
-    leaves = [lf for lf in coll.plan.leaves if lf.size_tag == path and lf.role == ROLE_ELEMENT]
-    if lay.host_visible or len(leaves) != 1 or leaves[0].extent_multiplier != 1:
-        raise KindError("pack_known_total packs one device-resident single-leaf vector")
-    n = coll.size()
-    dev = lay.device
-    with lay.engine_ops():
-        lay.reserve(path, total)
-        lay._set_sizes_for_engine({path: total})
-    coll._bump()
-    pleaf = coll.plan.leaf(path + ".prefix_sum")
-    if n == 0:
-        nat.call("sk_memset_async", lay.plane_address(pleaf, 0), 0, pleaf.value_type.size_bytes, nat.stream(dev))
-        return
-    cap = max(lay.capacity(path), 1)
-    ws = _workspace(dev)
-    need = C.c_size_t(0)
-    nat.call("sk_jagged_scratch_bytes", n, C.byref(need))
-    scratch = ws.scratch_for(-(-need.value // 256) * 256 + ((cap + 255) // 256 + 1) * 8)
-    lf = leaves[0]
-    nat.call("sk_jagged_pack", n, lens.ptr, nat.TYPE_CODES[_NP_CODE[lens.dtype]], lay.plane_address(pleaf, 0),
-             nat.TYPE_CODES[pleaf.value_type.storage_code], src_offsets.ptr, src_pool_ptr, src_members,
-             lf.value_type.size_bytes, 1, (C.c_int64 * 1)(0), (C.c_int32 * 1)(lf.value_type.size_bytes),
-             (C.c_void_p * 1)(lay.plane_address(lf, 0)), cap, scratch.ptr, scratch.n, ws.total.ptr, nat.stream(dev))
-
-
 def pack(coll, path: str, lens, src_offsets, src_pool, member_stride: int | None = None,
          member_offsets: Mapping[str, int] | None = None) -> int:
     """Fill jagged vector `path` of `coll` from a member pool; returns the total.

@@ -145,7 +145,6 @@ def reconstruct_from_collection(sensors, width: int, height: int, out=None, even
     collection (or fills `out`) with the reference's particles in the
     reference's order, events concatenated; out.event_counts holds the
     per-event particle counts."""
-    from . import jagged
     from .collection import Collection
 
     dev, p = _device_planes(sensors)
@@ -155,43 +154,59 @@ def reconstruct_from_collection(sensors, width: int, height: int, out=None, even
     if noise is None:
         noise = noise_for_collection(sensors, sync=False)
     ptype = sensors.layout.plane_address(sensors.plan.leaf("type"), 0)
+    if out is None:
+        out = Collection(PARTICLE_SCHEMA, ly.PER_FIELD, memctx.ContextInfo.cuda(dev))
+    lay = out.layout
+    # the output is written before the host learns the particle count: give it room for a typical run
+    # (benchmark events: ~0.27% of the cells become particles, ~20 sensors each), or what it already has
+    with lay.engine_ops():
+        out.clear()
+        lay.reserve(sc.MAIN_TAG, max(1024, n * events // 200))
+        lay.reserve("sensors", 24 * lay.capacity(sc.MAIN_TAG))
     handle = C.c_void_p(0)
-    np_ = C.c_int64(0)
-    rounds = C.c_int(0)
-    nat.call("sk_reco_run", width, height, events, p[_ENERGY], noise.ptr, ptype, p[_NOISY], dev, nat.stream(dev),
-             C.byref(handle), C.byref(np_), C.byref(rounds))
+    m, ncon, rounds, written = C.c_int64(0), C.c_int64(0), C.c_int(0), C.c_int(0)
+    nat.call("sk_reco_run", width, height, events, p[_ENERGY], noise.ptr, ptype, p[_NOISY],
+             C.byref(_reco_out(out)), dev, nat.stream(dev), C.byref(handle), C.byref(m), C.byref(ncon),
+             C.byref(rounds), C.byref(written))
     try:
-        m, ncon = C.c_int64(0), C.c_int64(0)
-        nat.call("sk_reco_sizes", handle, C.byref(m), C.byref(ncon))
         m, ncon = m.value, ncon.value
-        if out is None:
-            out = Collection(PARTICLE_SCHEMA, ly.PER_FIELD, memctx.ContextInfo.cuda(dev))
-        lay = out.layout
+        if not written.value:  # more particles than room: grow the output, write again
+            with lay.engine_ops():
+                lay.reserve(sc.MAIN_TAG, m)
+                lay.reserve("sensors", ncon)
+            nat.call("sk_reco_write", handle, C.byref(_reco_out(out)), nat.stream(dev))
         with lay.engine_ops():
-            out.clear()
-            lay.reserve(sc.MAIN_TAG, m)
-            lay._set_sizes_for_engine({sc.MAIN_TAG: m})
+            lay._set_sizes_for_engine({sc.MAIN_TAG: m, "sensors": ncon})
         out._bump()
-        addr = lambda leaf, k=0: lay.plane_address(PARTICLE_PLAN.leaf(leaf), k)  # noqa: E731
-        lens = DeviceArray(m, np.int32, memctx.ContextInfo.cuda(dev))
-        offs = DeviceArray(m, np.int64, memctx.ContextInfo.cuda(dev))
-        pool = C.c_void_p(0)
-        planes4 = lambda leaf: (C.c_void_p * 4)(*[addr(leaf, k) for k in range(4)])  # noqa: E731
-        nat.call("sk_reco_write", handle, addr("energy"), addr("x"), addr("y"), addr("origin"), addr("x_variance"),
-                 addr("y_variance"), planes4("significance.value"), planes4("E_contribution.value"),
-                 planes4("noisy_count.value"), lens.ptr, offs.ptr, C.byref(pool), nat.stream(dev))
         counts = (C.c_int64 * max(events, 1))()
         nat.call("sk_reco_event_counts", handle, counts)
-        # the contributor lists: their total is known, so the pack is only queued (jagged.pack_known_total)
-        jagged.pack_known_total(out, "sensors", lens, offs, pool.value or 0, 25 * max(m, 1), ncon)
         out.event_counts = list(counts)[:events]
         out.reco_rounds = rounds.value
     finally:
         nat.call("sk_reco_free", handle, nat.stream(dev))
-    lens.free()
-    offs.free()
-    nat.sync(dev)
+    if not written.value:
+        nat.sync(dev)
     return out
+
+
+def _reco_out(coll) -> "nat.RecoOut":
+    """The sk_reco_out view of a device per_field Particle collection, at its current capacities."""
+    lay = coll.layout
+    addr = lambda leaf, k=0: lay.plane_address(PARTICLE_PLAN.leaf(leaf), k)  # noqa: E731
+    o = nat.RecoOut()
+    o.energy, o.x, o.y, o.origin = addr("energy"), addr("x"), addr("y"), addr("origin")
+    o.x_variance, o.y_variance = addr("x_variance"), addr("y_variance")
+    for k in range(4):
+        o.significance[k] = addr("significance.value", k)
+        o.e_contribution[k] = addr("E_contribution.value", k)
+        o.noisy_count[k] = addr("noisy_count.value", k)
+    pleaf = PARTICLE_PLAN.leaf("sensors.prefix_sum")
+    o.sensor_prefix = lay.plane_address(pleaf, 0)
+    o.sensor_prefix_type = nat.TYPE_CODES[pleaf.value_type.storage_code]
+    o.sensor_pool = addr("sensors.value")
+    o.particle_capacity = lay.capacity(sc.MAIN_TAG)
+    o.pool_capacity = lay.capacity("sensors")
+    return o
 
 
 def fused_transfer(dst, src, opts=None) -> None:
