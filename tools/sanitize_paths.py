@@ -58,6 +58,20 @@ noise = DeviceArray(len(a), np.float32, CUDA)
 sensor.transfer_calibrate(p, a, noise)
 parts = sk.Collection(sensor.PARTICLE_SCHEMA, ly.PER_FIELD, CUDA)
 sensor.reconstruct_from_collection(p, 40, 30, out=parts, events=2, noise=noise)
+# the scalar tile pass (w % 4 != 0) on dense, tied events: long blocker chains, several rounds, and more
+# particles than the output's first guess (the grow-and-write-again path)
+rng = np.random.default_rng(5)
+dw, dh, dev_n = 37, 23, 3
+recs = np.zeros(dw * dh * dev_n, sensor.SENSOR_AOS_DTYPE)
+recs["energy"] = np.array([1.0, 3.0, 6.0, 7.0, 8.0, 50.0], np.float32)[rng.integers(0, 6, recs.size)]
+recs["type"] = rng.integers(0, 4, recs.size)
+dense_h = sk.Collection(sensor.SENSOR_SCHEMA, ly.AOS, mc.ContextInfo.pinned())
+dense_h.resize(recs.size)
+dense_h.layout._struct_buf._data[: recs.nbytes] = recs.view(np.uint8)
+dense = sk.Collection(sensor.SENSOR_SCHEMA, ly.PER_FIELD, CUDA)
+tr.copy_collection(dense, dense_h)
+ones = DeviceArray.from_numpy(np.ones(recs.size, np.float32), CUDA)
+sensor.reconstruct_from_collection(dense, dw, dh, events=dev_n, noise=ones)
 # AoSoA: AoS -> AoSoA (record groups), per_field -> AoSoA and AoSoA -> per_field (block transform),
 # AoSoA -> AoS (record groups reading AoSoA blocks)
 for m in (3, 1001):
