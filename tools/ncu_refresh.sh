@@ -6,8 +6,8 @@ tag=${1:-head}; shift
 jobs=${@:-obj8_a2p sensor_fused sensor_calnoise track_aosoa jagged}
 mkdir -p gpurun_out
 for j in $jobs; do
-  if [ "$j" = reco ]; then  # the reconstruction round kernels of 64 events (first round's pair)
-    timeout 600 ncu --set full --clock-control none --import-source on -k 'regex:ready_kernel|process_kernel' -s 24 -c 2 \
+  if [ "$j" = reco ]; then  # the reconstruction of 64 events: tile pass, first process, first check (call 4)
+    timeout 600 ncu --set full --clock-control none --import-source on -k 'regex:tile_kernel|check_kernel|process_kernel' -s 42 -c 3 \
         -o gpurun_out/ncu_${tag}_reco -f python tools/time_reco.py > gpurun_out/ncu_${tag}_reco.log 2>&1
     echo "reco rc=$?"; continue
   fi
