@@ -160,12 +160,61 @@ PyObject* pack_segments(PyObject*, PyObject* args) {
   return out;
 }
 
+// split_views(pool, bounds) -> [pool[bounds[i]:bounds[i+1]] for i in range(len(bounds) - 1)]
+//   The inverse direction (Particle export, baselines.py:104-120): one view of a 1-D C-contiguous pool per
+//   segment, made in C instead of one Python slice at a time. bounds: int64 array of n + 1 offsets.
+PyObject* split_views(PyObject*, PyObject* args) {
+  PyArrayObject* pool = nullptr;
+  PyArrayObject* bounds = nullptr;
+  if (!PyArg_ParseTuple(args, "O!O!", &PyArray_Type, &pool, &PyArray_Type, &bounds)) return nullptr;
+  if (PyArray_NDIM(pool) != 1 || !PyArray_IS_C_CONTIGUOUS(pool) || PyArray_NDIM(bounds) != 1 ||
+      PyArray_TYPE(bounds) != NPY_INT64 || !PyArray_IS_C_CONTIGUOUS(bounds)) {
+    PyErr_SetString(PyExc_ValueError, "split_views needs a 1-D contiguous pool and int64 bounds");
+    return nullptr;
+  }
+  const npy_intp nb = PyArray_DIM(bounds, 0);
+  const npy_intp n = nb > 0 ? nb - 1 : 0;
+  const int64_t* b = static_cast<const int64_t*>(PyArray_DATA(bounds));
+  const npy_intp len = PyArray_DIM(pool, 0);
+  for (npy_intp i = 0; i < n; ++i)
+    if (b[i] < 0 || b[i] > b[i + 1] || b[i + 1] > len) {
+      PyErr_SetString(PyExc_ValueError, "bounds out of order or past the pool");
+      return nullptr;
+    }
+  PyObject* out = PyList_New(n);
+  if (!out) return nullptr;
+  PyArray_Descr* descr = PyArray_DESCR(pool);
+  const npy_intp item = PyArray_ITEMSIZE(pool);
+  char* data = static_cast<char*>(PyArray_DATA(pool));
+  const int flags = PyArray_FLAGS(pool) & (NPY_ARRAY_WRITEABLE | NPY_ARRAY_ALIGNED);
+  for (npy_intp i = 0; i < n; ++i) {
+    npy_intp dim = static_cast<npy_intp>(b[i + 1] - b[i]);
+    Py_INCREF(descr);  // stolen by NewFromDescr
+    PyObject* v = PyArray_NewFromDescr(&PyArray_Type, descr, 1, &dim, nullptr, data + b[i] * item,
+                                       flags | NPY_ARRAY_C_CONTIGUOUS, nullptr);
+    if (!v) {
+      Py_DECREF(out);
+      return nullptr;
+    }
+    Py_INCREF(pool);
+    if (PyArray_SetBaseObject(reinterpret_cast<PyArrayObject*>(v), reinterpret_cast<PyObject*>(pool)) < 0) {
+      Py_DECREF(v);
+      Py_DECREF(out);
+      return nullptr;
+    }
+    PyList_SET_ITEM(out, i, v);
+  }
+  return out;
+}
+
 PyMethodDef kMethods[] = {
     {"pack_segments", pack_segments, METH_VARARGS,
      "pack_segments(segments, dtype, alloc=None) -> buffer [lengths i64 | starts i64 | pool], or None"},
+    {"split_views", split_views, METH_VARARGS, "split_views(pool, bounds) -> list of views pool[b[i]:b[i+1]]"},
     {nullptr, nullptr, 0, nullptr}};
 
-PyModuleDef kModule = {PyModuleDef_HEAD_INIT, "_segpack", "jagged_fill host packing", -1, kMethods};
+PyModuleDef kModule = {PyModuleDef_HEAD_INIT, "_segpack", "host packing and splitting of jagged segments", -1,
+                       kMethods};
 
 }  // namespace
 

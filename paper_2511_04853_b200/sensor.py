@@ -314,8 +314,13 @@ def export_particles_from_collection(coll, stage=None) -> tuple[np.ndarray, list
     lay = stage.layout
     recs = np.array(lay._struct_buf._data[: n * PARTICLE_AOS_DTYPE.itemsize].view(PARTICLE_AOS_DTYPE))
     pool = np.array(lay._plane_view(stage.plan.leaf("sensors.value"), 0))
-    b = np.array(lay._plane_view(stage.plan.leaf("sensors.prefix_sum"), 0)).astype(np.int64).tolist()
-    return recs, [pool[b[i]:b[i + 1]] for i in range(n)]  # views of one pool (np.split is slower)
+    b = np.array(lay._plane_view(stage.plan.leaf("sensors.prefix_sum"), 0)).astype(np.int64)
+    try:  # one view of the pool per particle, made in C (csrc/segpack.cpp)
+        from . import _segpack
+        return recs, _segpack.split_views(pool, b[: n + 1])
+    except ImportError:  # pragma: no cover - not built
+        bl = b.tolist()
+        return recs, [pool[bl[i]:bl[i + 1]] for i in range(n)]
 
 
 _EVENT_COLUMNS = ("type", "counts", "noisy", "parameter_A", "parameter_B", "noise_A", "noise_B")

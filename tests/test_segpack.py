@@ -64,3 +64,16 @@ def test_errors():
         _segpack.pack_segments([np.arange(4, dtype=np.uint64)], np.uint64, lambda nb: bytearray(nb - 1))
     with pytest.raises(BufferError):
         _segpack.pack_segments([np.arange(4, dtype=np.uint64)], np.uint64, lambda nb: b"x" * nb)  # read-only
+
+
+def test_split_views_match_slices():
+    pool = np.arange(1000, dtype=np.uint64)
+    b = np.array([0, 3, 3, 10, 999, 1000], np.int64)
+    v = _segpack.split_views(pool, b)
+    assert [x.tolist() for x in v] == [pool[b[i]:b[i + 1]].tolist() for i in range(5)]
+    assert all(x.base is not None for x in v) and v[2].size == 0
+    assert _segpack.split_views(pool, np.zeros(1, np.int64)) == []
+    with pytest.raises(ValueError):
+        _segpack.split_views(pool, np.array([0, 5, 3], np.int64))  # out of order
+    with pytest.raises(ValueError):
+        _segpack.split_views(pool, np.array([0, 1001], np.int64))  # past the pool
