@@ -31,6 +31,7 @@
 #include <atomic>
 #include <cstdio>
 #include <cstdlib>
+#include <type_traits>
 #include <utility>
 
 #include "sk_internal.cuh"
@@ -1189,6 +1190,381 @@ __global__ void __launch_bounds__(F_NT, 3) pack_fused_kernel(const __grid_consta
   stamp(3);
 }
 
+
+// ---- fused pack, register gather (one naturally aligned 4/8-byte member field) ----
+//
+// The default single-pass pack. Tiles of RG_TR = 2048 records are handed out by
+// ticket (a CTA holding tile t only ever waits on tiles < t, whose holders are
+// running: no co-residency assumption). Per tile:
+//   1. every warp loads the lengths and source offsets of its 8 groups of 32
+//      records (coalesced, all 16 loads in flight), scans each group with
+//      shuffles, and leaves the group-local exclusive prefix and
+//      D = src_off - prefix in shared memory; the CTA publishes the tile total;
+//   2. a warp gathers its groups: lane i of round q takes group member
+//      m = 32 q + i, finds its record by a 5-step shuffle search over the
+//      group's prefixes and loads src[D + m] into a register -- up to RG_K
+//      rounds (384 members) are in flight per warp before the first store;
+//   3. the first store waits for the tile's exclusive prefix E, which warp 0
+//      finds by decoupled look-back (32 predecessors per round, stopping at
+//      the nearest inclusive prefix) while its own first loads are in flight;
+//   4. prefix elements P[r] = E + local prefix are stored, truncated to the
+//      index dtype; the tile holding the last record writes P[n] and the total.
+// A group of more than RG_BIG members (skewed lengths) is not gathered by its
+// warp: it is queued, and every warp that finishes its tile takes 1536-member
+// chunks of the queued groups it sees (an entry queued later is drained by its
+// owner's CTA, which looks at the queue after all its warps have queued).
+// Measured against the cp.async window design below (pack_fused_kernel, kept
+// for multi-field member records): 43 vs 50 us on config 3 -- the member
+// loads need registers, not shared-memory staging (tools/jag_micro.cu,
+// profiles/r02_jagged_redesign.md).
+
+constexpr int RG_NW = 8;
+constexpr int RG_GPW = 8;                      // groups of 32 records per warp and tile
+constexpr int RG_TR = RG_NW * RG_GPW * 32;     // records per tile
+constexpr int RG_K = 12;                       // 32-member rounds in flight per warp
+constexpr int64_t RG_BIG = 32 * RG_K * 8;      // group members above which the group is queued
+constexpr int64_t RG_CHUNK = 32 * RG_K * 4;    // members per queued-group work item
+constexpr int64_t RG_QMAX = 65536;             // queue entries (a full queue: the owner warp gathers itself)
+
+struct RegHdr {
+  unsigned int nq;  // queued groups (zeroed by tile 0 before it publishes)
+  unsigned int pad[15];
+};
+
+// per-tile look-back word: {value, gen << 2 | 1 (value = the tile's total) or | 2 (its inclusive prefix)},
+// written and read as ONE 128-bit access (PTX .b128, single-copy atomic). Nothing in the scratch needs
+// zeroing between launches: a word counts only when it carries this launch's generation.
+struct __align__(16) RegStatus {
+  unsigned long long v;
+  unsigned long long tag;
+};
+
+__device__ __forceinline__ void st_status(RegStatus* p, int64_t v, unsigned long long tag) {
+  asm volatile("{ .reg .b128 t; mov.b128 t, {%1, %2}; st.release.gpu.global.b128 [%0], t; }" ::"l"(p),
+               "l"(static_cast<unsigned long long>(v)), "l"(tag)
+               : "memory");
+}
+
+__device__ __forceinline__ void ld_status(const RegStatus* p, int64_t& v, unsigned long long& tag) {
+  unsigned long long a, b;
+  asm volatile("{ .reg .b128 t; ld.relaxed.gpu.global.b128 t, [%2]; mov.b128 {%0, %1}, t; }"
+               : "=l"(a), "=l"(b)
+               : "l"(p)
+               : "memory");
+  v = static_cast<int64_t>(a);
+  tag = b;
+}
+
+struct RegEntry {
+  int64_t rec0;              // first record of the group
+  int64_t out0;              // output member index of its first member
+  int64_t T;                 // its members
+  unsigned long long next;   // next chunk to hand out
+  unsigned long long ready;  // = the launch's generation (release) once the fields above are written
+  int cnt;                   // records in the group
+  int pad0;
+  int64_t pad[2];
+};
+
+struct RegArgs {
+  int64_t n;
+  const void* lens;
+  int lens_type;
+  void* prefix;
+  int prefix_type;
+  int64_t* total;
+  int64_t* bad;         // += records whose segment lies outside the source pool (their tile is not gathered)
+  const int64_t* src_off;
+  const uint8_t* src;   // pool + field offset
+  int64_t member_stride;
+  uint8_t* dst;         // MS-aligned
+  int64_t capacity;
+  int64_t src_members;
+  RegHdr* hdr;
+  RegStatus* status;    // per tile
+  RegEntry* q;
+  int64_t qmax;
+  unsigned long long gen;
+};
+
+template <int MS, bool PACKED>
+__device__ __forceinline__ typename MemberWord<MS>::T rg_load(const RegArgs& F, int64_t j) {
+  if constexpr (PACKED) return reinterpret_cast<const typename MemberWord<MS>::T*>(F.src)[j];
+  return *reinterpret_cast<const typename MemberWord<MS>::T*>(F.src + j * F.member_stride);
+}
+
+template <int MS>
+__device__ __forceinline__ void rg_store(const RegArgs& F, int64_t j, typename MemberWord<MS>::T v) {
+  __stcs(reinterpret_cast<typename MemberWord<MS>::T*>(F.dst) + j, v);
+}
+
+// tile 0 has zeroed the queue and invalid-record counters of this launch
+__device__ __forceinline__ void rg_wait_tile0(const RegArgs& F, unsigned long long gen2) {
+  while ((ld_acquire(&F.status[0].tag) & ~3ull) != gen2) __nanosleep(32);
+}
+
+// a queued group's members [m_begin, m_end): its records' prefixes are rebuilt
+// from the lengths (64-bit search: such a group may exceed 2^31 members)
+template <int MS, bool PACKED>
+__device__ __forceinline__ void rg_gather_big(const RegArgs& F, const RegEntry& ent, int64_t m_begin, int64_t m_end) {
+  using V = typename MemberWord<MS>::T;
+  const int lane = threadIdx.x & 31;
+  const int64_t r = ent.rec0 + lane;
+  const int64_t len = lane < ent.cnt ? load_int(F.lens, F.lens_type, r) : 0;
+  const int64_t off = lane < ent.cnt ? F.src_off[r] : 0;
+  int64_t x = len;
+#pragma unroll
+  for (int s = 1; s < 32; s <<= 1) {
+    const int64_t y = __shfl_up_sync(0xffffffffu, x, s);
+    if (lane >= s) x += y;
+  }
+  const int64_t ex = x - len, d = off - ex;
+  for (int64_t m0 = m_begin; m0 < m_end; m0 += 32 * RG_K) {
+    V v[RG_K];
+#pragma unroll
+    for (int q = 0; q < RG_K; ++q) {
+      const int64_t m = m0 + q * 32 + lane;
+      if (m0 + q * 32 < m_end) {
+        int lo = 0;
+#pragma unroll
+        for (int s = 16; s >= 1; s >>= 1) {
+          const int64_t e = __shfl_sync(0xffffffffu, ex, lo + s);
+          if (e <= m) lo += s;
+        }
+        const int64_t dd = __shfl_sync(0xffffffffu, d, lo);
+        if (m < m_end) v[q] = rg_load<MS, PACKED>(F, dd + m);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < RG_K; ++q) {
+      const int64_t m = m0 + q * 32 + lane;
+      if (m < m_end) rg_store<MS>(F, ent.out0 + m, v[q]);
+    }
+  }
+}
+
+// WIDE: 64-bit or u32 lengths (held as int64 while the loads fly); otherwise int32
+template <int MS, bool WIDE, bool PACKED>
+__global__ void __launch_bounds__(RG_NW * 32, 4) pack_reg_kernel(const __grid_constant__ RegArgs F) {
+  using LT = typename std::conditional<WIDE, int64_t, int32_t>::type;
+  using V = typename MemberWord<MS>::T;
+  __shared__ int64_t sD[RG_TR];
+  __shared__ int64_t sEx[RG_TR];  // group-local exclusive prefix
+  __shared__ int64_t sGb[RG_NW * RG_GPW];
+  __shared__ int64_t sWt[RG_NW];
+  __shared__ int sBad[RG_NW];
+  __shared__ int64_t sE;
+  __shared__ unsigned int sNq;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // tiles in block order: a tile waits only on lower-indexed blocks, which in-order dispatch has started
+  // (the look-back assumption of CUB's single-pass scan)
+  const int64_t t = blockIdx.x, rw = t * RG_TR + warp * (RG_GPW * 32);
+  const unsigned long long gen2 = F.gen << 2;
+  // the previous kernel in the stream has completed (lengths final, scratch no longer in use)
+  pdl_wait_prior();
+  if (t == 0 && tid == 0) {
+    F.hdr->nq = 0;
+    *F.bad = 0;
+    __threadfence();
+  }
+  // 1. lengths and offsets of this warp's groups, group scans
+  LT len[RG_GPW];
+  int64_t off[RG_GPW];
+#pragma unroll
+  for (int k = 0; k < RG_GPW; ++k) {
+    const int64_t r = rw + k * 32 + lane;
+    len[k] = r < F.n ? static_cast<LT>(load_int(F.lens, F.lens_type, r)) : 0;
+    off[k] = r < F.n ? F.src_off[r] : 0;
+  }
+  int64_t wsum = 0;
+  unsigned nbad = 0;
+#pragma unroll
+  for (int k = 0; k < RG_GPW; ++k) {
+    // empty segments are valid whatever their offset (an empty list reads nothing)
+    nbad += len[k] < 0 || (len[k] > 0 && (off[k] < 0 || off[k] > F.src_members - len[k]));
+    int64_t x = len[k];
+#pragma unroll
+    for (int s = 1; s < 32; s <<= 1) {
+      const int64_t y = __shfl_up_sync(0xffffffffu, x, s);
+      if (lane >= s) x += y;
+    }
+    const int e = warp * (RG_GPW * 32) + k * 32 + lane;
+    sEx[e] = x - len[k];
+    sD[e] = off[k] - (x - len[k]);
+    if (lane == 0) sGb[warp * RG_GPW + k] = wsum;
+    wsum += __shfl_sync(0xffffffffu, x, 31);
+  }
+  const unsigned wbad = __reduce_add_sync(0xffffffffu, nbad);
+  if (lane == 0) {
+    sWt[warp] = wsum;
+    sBad[warp] = wbad != 0;
+  }
+  __syncthreads();
+  if (lane == 0 && wbad) {
+    if (t != 0) rg_wait_tile0(F, gen2);  // the counter is zeroed by tile 0 (in this CTA: before the barrier)
+    atomicAdd(reinterpret_cast<unsigned long long*>(F.bad), static_cast<unsigned long long>(wbad));
+  }
+  int64_t A = 0, Wo = 0;
+  bool bad = false;
+#pragma unroll
+  for (int w = 0; w < RG_NW; ++w) {
+    Wo += w < warp ? sWt[w] : 0;
+    A += sWt[w];
+    bad |= sBad[w] != 0;
+  }
+  if (tid == 0) {
+    st_status(&F.status[t], A, gen2 | (t == 0 ? 2 : 1));
+    __threadfence();  // push the total out now: every later tile looks back at it
+  }
+  // 3. the tile's exclusive prefix (warp 0 looks back; every warp calls this exactly once)
+  bool haveE = false;
+  int64_t E = 0;
+  auto get_E = [&]() {
+    if (warp == 0) {
+      int64_t acc = 0;
+      if (t > 0) {
+        int64_t idx = t - 1;
+        while (true) {
+          const int64_t j = idx - lane;
+          int64_t sv = 0;
+          unsigned long long f = gen2 | 2;
+          if (j >= 0) ld_status(&F.status[j], sv, f);
+          while (__any_sync(0xffffffffu, (f & ~3ull) != gen2)) {
+            if ((f & ~3ull) != gen2) ld_status(&F.status[j], sv, f);
+          }
+          const unsigned pm = __ballot_sync(0xffffffffu, (f & 3) == 2);
+          const int pl = pm ? __ffs(pm) - 1 : 32;
+          int64_t v = (lane <= pl && j >= 0) ? sv : 0;
+#pragma unroll
+          for (int q = 16; q; q >>= 1) v += __shfl_xor_sync(0xffffffffu, v, q);
+          acc += v;
+          if (pm) break;
+          idx -= 32;
+        }
+        if (lane == 0) st_status(&F.status[t], acc + A, gen2 | 2);
+      }
+      if (lane == 0) sE = acc;
+    }
+    asm volatile("bar.sync 1, %0;" ::"n"(RG_NW * 32) : "memory");
+    E = sE;
+    haveE = true;
+  };
+  // 2. the gather (not for a tile holding an invalid segment; no stores past the capacity); groups over
+  // RG_BIG members are set aside for the queue
+  unsigned big = 0;
+#pragma unroll 1
+  for (int k = 0; k < RG_GPW && !bad; ++k) {
+    const int g = warp * RG_GPW + k;
+    const int64_t g0 = sGb[g];
+    const int64_t T = (k + 1 < RG_GPW ? sGb[g + 1] : sWt[warp]) - g0;
+    if (T > RG_BIG) {
+      big |= 1u << k;
+      continue;
+    }
+    const int e = g * 32 + lane;
+    const int ex = static_cast<int>(sEx[e]);  // T <= RG_BIG
+    const int64_t d = sD[e];
+    const int Ti = static_cast<int>(T);
+#pragma unroll 1
+    for (int m0 = 0; m0 < Ti; m0 += 32 * RG_K) {
+      V v[RG_K];
+#pragma unroll
+      for (int q = 0; q < RG_K; ++q) {
+        const int m = m0 + q * 32 + lane;
+        if (m0 + q * 32 < Ti) {
+          int lo = 0;
+#pragma unroll
+          for (int s = 16; s >= 1; s >>= 1) {
+            const int ee = __shfl_sync(0xffffffffu, ex, lo + s);
+            if (ee <= m) lo += s;
+          }
+          const int64_t dd = __shfl_sync(0xffffffffu, d, lo);
+          if (m < Ti) v[q] = rg_load<MS, PACKED>(F, dd + m);
+        }
+      }
+      if (!haveE) get_E();
+      if (E + A > F.capacity) break;
+      V* ob = reinterpret_cast<V*>(F.dst) + (E + Wo + g0);
+#pragma unroll
+      for (int q = 0; q < RG_K; ++q) {
+        const int m = m0 + q * 32 + lane;
+        if (m < Ti) __stcs(ob + m, v[q]);
+      }
+    }
+  }
+  if (!haveE) get_E();
+  // the set-aside groups: queued for every warp to share (a full queue: gathered here)
+  if (E + A <= F.capacity) {
+#pragma unroll 1
+    for (; big; big &= big - 1) {
+      const int k = __ffs(big) - 1;
+      const int g = warp * RG_GPW + k;
+      const int64_t g0 = sGb[g];
+      RegEntry ent;
+      ent.rec0 = rw + k * 32;
+      ent.cnt = static_cast<int>(min(static_cast<int64_t>(32), F.n - ent.rec0));
+      ent.out0 = E + Wo + g0;
+      ent.T = (k + 1 < RG_GPW ? sGb[g + 1] : sWt[warp]) - g0;
+      unsigned slot = 0;
+      if (lane == 0) {
+        rg_wait_tile0(F, gen2);  // the queue counter is zeroed by tile 0
+        slot = atomicAdd(&F.hdr->nq, 1u);
+      }
+      slot = __shfl_sync(0xffffffffu, slot, 0);
+      if (slot < F.qmax) {
+        if (lane == 0) {
+          RegEntry& qe = F.q[slot];
+          qe.rec0 = ent.rec0;
+          qe.cnt = ent.cnt;
+          qe.out0 = ent.out0;
+          qe.T = ent.T;
+          qe.next = 0;
+          __threadfence();
+          st_release(&qe.ready, F.gen);
+        }
+      } else {
+        rg_gather_big<MS, PACKED>(F, ent, 0, ent.T);
+      }
+    }
+  }
+  // 4. prefix elements, truncated to the index dtype
+#pragma unroll
+  for (int k = 0; k < RG_GPW; ++k) {
+    const int64_t r = rw + k * 32 + lane;
+    const int e = warp * (RG_GPW * 32) + k * 32 + lane;
+    if (r < F.n) store_int(F.prefix, F.prefix_type, r, E + Wo + sGb[warp * RG_GPW + k] + sEx[e]);
+  }
+  if (tid == 0 && t * RG_TR + RG_TR >= F.n) {
+    store_int(F.prefix, F.prefix_type, F.n, E + A);
+    *F.total = E + A;
+  }
+  // queued groups: every entry queued so far (this CTA's included: the barrier orders its warps' queueing
+  // before the count is read). No warp waits for another to queue anything; an entry whose slot is taken
+  // but not yet written is being written by a running warp.
+  __syncthreads();
+  if (tid == 0) {
+    rg_wait_tile0(F, gen2);
+    sNq = min(static_cast<unsigned>(F.qmax), *reinterpret_cast<volatile unsigned int*>(&F.hdr->nq));
+  }
+  __syncthreads();
+  const unsigned nq = sNq;
+  for (unsigned dq = 0; dq < nq; ++dq) {
+    if (lane == 0)
+      while (ld_acquire(&F.q[dq].ready) != F.gen) __nanosleep(64);
+    __syncwarp();
+    const RegEntry ent = F.q[dq];
+    const int64_t nch = (ent.T + RG_CHUNK - 1) / RG_CHUNK;
+    while (true) {
+      unsigned long long c = 0;
+      if (lane == 0) c = atomicAdd(&F.q[dq].next, 1ull);
+      c = __shfl_sync(0xffffffffu, c, 0);
+      if (static_cast<int64_t>(c) >= nch) break;
+      const int64_t mb = static_cast<int64_t>(c) * RG_CHUNK;
+      rg_gather_big<MS, PACKED>(F, ent, mb, min(ent.T, mb + RG_CHUNK));
+    }
+  }
+}
+
 // zeroes the fused pack's scratch header + status words; lets the pack's CTAs
 // launch (and sum their lengths) meanwhile, but only once everything before it
 // in the stream has completed
@@ -1284,10 +1660,21 @@ static size_t fused_scratch_bytes(int64_t n) {
   return static_cast<size_t>(64 + ((t * 8 + 63) & ~int64_t(63)) + 2 * t * sizeof(jag::DeferEntry));
 }
 
+// register-gather pack scratch: header, one look-back status word per tile, the queue of skewed groups
+static int64_t reg_queue_entries(int64_t n) { return std::min<int64_t>(jag::RG_QMAX, (n + 31) / 32); }
+static size_t reg_status_bytes(int64_t n) {
+  const int64_t t = (n + jag::RG_TR - 1) / jag::RG_TR;
+  return static_cast<size_t>(t) * sizeof(jag::RegStatus);
+}
+static size_t reg_scratch_bytes(int64_t n) {
+  return 64 + reg_status_bytes(n) + static_cast<size_t>(reg_queue_entries(n)) * sizeof(jag::RegEntry);
+}
+
 int sk_jagged_scratch_bytes(int64_t n, size_t* nbytes) {
   if (!nbytes) return set_error(SK_ERR_INVALID, "null out");
   const int64_t tiles = n > 0 ? (n + jag::SCAN_TILE - 1) / jag::SCAN_TILE : 0;
-  *nbytes = std::max(static_cast<size_t>(16 + tiles * 8), n > 0 ? fused_scratch_bytes(n) : 0);
+  *nbytes = std::max({static_cast<size_t>(16 + tiles * 8), n > 0 ? fused_scratch_bytes(n) : size_t(0),
+                      n > 0 ? reg_scratch_bytes(n) : size_t(0)});
   return SK_OK;
 }
 
@@ -1443,6 +1830,30 @@ static int launch_fused_ms(jag::FusedArgs F, uint8_t* scratch, cudaStream_t s, i
   return SK_OK;
 }
 
+template <int MS>
+static int launch_reg_ms(jag::RegArgs R, uint8_t* scratch, cudaStream_t s) {
+  // no scratch zeroing: the kernel's flags carry the launch generation, tile 0 resets the counters
+  const int64_t ntiles = (R.n + jag::RG_TR - 1) / jag::RG_TR;
+  R.hdr = reinterpret_cast<jag::RegHdr*>(scratch);
+  R.status = reinterpret_cast<jag::RegStatus*>(scratch + 64);
+  R.q = reinterpret_cast<jag::RegEntry*>(scratch + 64 + reg_status_bytes(R.n));
+  R.qmax = reg_queue_entries(R.n);
+  const bool wide = dtype_size(R.lens_type) == 8 || R.lens_type == SK_U32, packed = R.member_stride == MS;
+  auto k = wide ? (packed ? jag::pack_reg_kernel<MS, true, true> : jag::pack_reg_kernel<MS, true, false>)
+                : (packed ? jag::pack_reg_kernel<MS, false, true> : jag::pack_reg_kernel<MS, false, false>);
+  SK_TRY(launch_pdl(k, dim3(static_cast<unsigned>(ntiles)), dim3(jag::RG_NW * 32), s, R));
+  return SK_OK;
+}
+
+static bool reg_pack_ok() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SK_JAGGED_REG");
+    v = e ? atoi(e) : 1;
+  }
+  return v != 0;
+}
+
 static bool fused_pack_ok() {
   static int v = -1;
   if (v < 0) {
@@ -1562,6 +1973,29 @@ int sk_jagged_pack(int64_t n, const void* lens, int lens_type, void* prefix, int
   for (int f = 0; f < nfields && split; ++f)
     split = A.aligned[f] && (A.field_size[f] == 4 || A.field_size[f] == 8) &&
             reinterpret_cast<uintptr_t>(A.dst[f]) % A.field_size[f] == 0;
+  // single field, MS-aligned destination: the register-gather pack
+  if (fused_pack_ok() && reg_pack_ok() && nfields == 1 && A.aligned[0] &&
+      (A.field_size[0] == 4 || A.field_size[0] == 8) &&
+      reinterpret_cast<uintptr_t>(A.dst[0]) % A.field_size[0] == 0 && reinterpret_cast<uintptr_t>(scratch) % 16 == 0) {
+    jag::RegArgs R{};
+    R.n = n;
+    R.lens = lens;
+    R.lens_type = lens_type;
+    R.prefix = prefix;
+    R.prefix_type = prefix_type;
+    R.total = total_dev;
+    R.bad = total_dev + 1;
+    R.src_off = src_off;
+    R.src = A.src_pool + A.field_off[0];
+    R.member_stride = member_stride;
+    R.dst = A.dst[0];
+    R.capacity = capacity;
+    R.src_members = src_members;
+    static std::atomic<unsigned long long> reg_generation{0};
+    R.gen = ++reg_generation;
+    uint8_t* sc = static_cast<uint8_t*>(scratch);
+    return A.field_size[0] == 8 ? launch_reg_ms<8>(R, sc, s) : launch_reg_ms<4>(R, sc, s);
+  }
   if (fused_pack_ok() && (single || split)) {
     DeviceState* ds = nullptr;
     if (int rc = device_state(dev, &ds)) return rc;
