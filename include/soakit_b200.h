@@ -202,11 +202,13 @@ int sk_jagged_validate(int64_t n, const void* lens, int lens_type, const int64_t
    reads both afterwards: invalid records -> nothing was gathered for their
    sub-tiles (the prefix is written regardless), raise; total > capacity ->
    grow the pools and gather again with sk_jagged_scatter. One naturally
-   aligned 4/8-byte member field (16-byte-aligned pool), or 2-4 such fields of
-   an 8/16-byte member record, runs as ONE kernel (prefixes and gather fused;
-   the scratch holds its per-block status words); the kernel needs no
-   co-residency of its CTAs beyond in-order dispatch (a CTA only waits on
-   lower-indexed blocks' published totals). Other member layouts run
+   aligned 4/8-byte member field (a 16-byte-aligned scratch) runs as ONE
+   launch: 2048-record tiles, register gather, 128-bit look-back words tagged
+   with the launch generation (nothing in the scratch is zeroed between
+   calls). 2-4 such fields of an 8/16-byte member record (16-byte-aligned
+   pool) run as one kernel behind a scratch-zeroing launch. Either kernel
+   needs no co-residency of its CTAs beyond in-order dispatch (a CTA only
+   waits on lower-indexed blocks' published totals). Other member layouts run
    validate, scan and gather back to
    back. Scratch: at least sk_jagged_scratch_bytes; with
    (ceil(capacity / 256) + 1) * 8 more bytes after it (256-aligned) the

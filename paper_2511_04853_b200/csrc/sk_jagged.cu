@@ -14,11 +14,12 @@
 // split: starts[w] = the record holding member w*W, and 1 + the last non-empty
 // record.
 //
-// sk_jagged_pack with one aligned 4/8-byte member field, or 2-4 such fields of
-// an 8/16-byte member record, runs both in ONE kernel (pack_fused_kernel,
-// below): per-CTA record blocks whose prefixes come from the predecessor
-// blocks' published totals, then per-sub-tile smem tables feeding the same
-// window gather. The two-kernel path (scan, then gather) serves
+// sk_jagged_pack with one aligned 4/8-byte member field runs both in ONE
+// kernel (pack_reg_kernel, below): 2048-record tiles with decoupled look-back
+// and a register gather. 2-4 such fields of an 8/16-byte member record run in
+// pack_fused_kernel: per-CTA record blocks whose prefixes come from the
+// predecessor blocks' published totals, then per-sub-tile smem tables feeding
+// the window gather. The two-kernel path (scan, then gather) serves
 // sk_jagged_scan / sk_jagged_scatter and the other member layouts.
 //
 // Gather: one warp per W = 256 consecutive output members, no block barriers.

@@ -169,7 +169,7 @@ __device__ __forceinline__ void st_rel(uint64_t* p, uint64_t v) {
 template <int NT> __device__ __forceinline__ void bar1() { asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory"); }
 
 // fused: ticketed tiles of 2048 records (8 warps x 8 groups x 32), decoupled look-back, register gather
-template <int K, int MINB, int SP, int GPW, int DBG = 0, int NW = 8, bool OWN = false>
+template <int K, int MINB, int SP, int GPW, int DBG = 0, int NW = 8, int OWN = 0>
 __global__ void __launch_bounds__(NW * 32, MINB) fused_k(int64_t n, const int* __restrict__ lens, const int64_t* __restrict__ off,
     const uint64_t* __restrict__ pool, uint64_t* __restrict__ out, int* __restrict__ P, unsigned* ticket,
     uint64_t* status, int64_t* total) {
@@ -180,7 +180,8 @@ __global__ void __launch_bounds__(NW * 32, MINB) fused_k(int64_t n, const int* _
   __shared__ int64_t swt[NW];
   __shared__ int64_t sE;
   __shared__ unsigned st;
-  __shared__ int64_t smap[OWN ? NW : 1][OWN ? K * 32 : 1];
+  __shared__ int64_t smap[OWN == 1 ? NW : 1][OWN == 1 ? K * 32 : 1];
+  __shared__ int64_t sdc[NW][32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) st = (DBG & 2) ? blockIdx.x : atomicAdd(ticket, 1u);
   __syncthreads();
@@ -217,13 +218,40 @@ __global__ void __launch_bounds__(NW * 32, MINB) fused_k(int64_t n, const int* _
     Wo += w < warp ? swt[w] : 0;
     A += swt[w];
   }
-  if (tid == 0) st_rel(&status[t], (t == 0 ? FLAG_P : FLAG_A) | (uint64_t(A) & VAL_MASK));
+  if (tid == 0) st_rel(&status[t], (t == 0 && !(DBG & 4) ? FLAG_P : FLAG_A) | (uint64_t(A) & VAL_MASK));
   bool haveE = false;
   int64_t E = 0;
   auto getE = [&]() {
     if (warp == 0) {
       int64_t acc = 0;
-      if (t > 0 && !(DBG & 1)) {
+      if (t > 0 && (DBG & 4)) {
+        // sum every predecessor's aggregate, 256 per round (no chain through inclusive prefixes)
+        for (int64_t e0 = 0; e0 < t; e0 += 256) {
+          uint64_t s[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const int64_t j = e0 + q * 32 + lane;
+            s[q] = j < t ? ld_poll(&status[j]) : FLAG_A;
+          }
+          bool miss = false;
+#pragma unroll
+          for (int q = 0; q < 8; ++q) miss |= (s[q] >> 62) == 0;
+          while (__any_sync(~0u, miss)) {
+            miss = false;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              if ((s[q] >> 62) == 0) s[q] = ld_poll(&status[e0 + q * 32 + lane]);
+              miss |= (s[q] >> 62) == 0;
+            }
+          }
+          int64_t v = 0;
+#pragma unroll
+          for (int q = 0; q < 8; ++q) if (e0 + q * 32 + lane < t) v += int64_t(s[q] & VAL_MASK);
+#pragma unroll
+          for (int q = 16; q; q >>= 1) v += __shfl_xor_sync(~0u, v, q);
+          acc += v;
+        }
+      } else if (t > 0 && !(DBG & 1)) {
         int64_t idx = t - 1;
         while (true) {
           const int64_t j = idx - lane;
@@ -257,10 +285,33 @@ __global__ void __launch_bounds__(NW * 32, MINB) fused_k(int64_t n, const int* _
     const int e = g * 32 + lane;
     const int ex = sex[e];
     const int64_t d = sd[e];
+    int cnt = 0;
 #pragma unroll 1
     for (int m0 = 0; m0 < T; m0 += 32 * K) {
       uint64_t v[K];
-      if constexpr (OWN) {
+      if constexpr (OWN == 2) {
+        // mask/rank search: record starts of each 32-member window by REDUX.OR, rank by popc,
+        // source base from the warp's compacted table of non-empty records
+        const int lenl = (lane < 31 ? sex[e + 1] : T) - ex;
+        const unsigned le = 0xffffffffu >> (31 - lane);
+        if (m0 == 0) {
+          const unsigned nz = __ballot_sync(~0u, lenl > 0);
+          if (lenl > 0) sdc[warp][__popc(nz & (le >> 1))] = d;
+          __syncwarp();
+          cnt = 0;
+        }
+#pragma unroll
+        for (int q = 0; q < K; ++q) {
+          const int base = m0 + q * 32;
+          if (base < T) {
+            const unsigned sb = (lenl > 0 && ex >= base && ex < base + 32) ? 1u << (ex - base) : 0u;
+            const unsigned mask = __reduce_or_sync(~0u, sb);
+            const int k2 = cnt + __popc(mask & le) - 1;
+            cnt += __popc(mask);
+            if (base + lane < T) v[q] = pool[sdc[warp][k2] + base + lane];
+          }
+        }
+      } else if constexpr (OWN == 1) {
         int64_t* map = smap[warp];
         __syncwarp();
         const int lenl = (lane < 31 ? sex[e + 1] : T) - ex;
@@ -424,6 +475,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) fused_cp(int64_t n, const int* 
     const int e = g * 32 + lane;
     const int ex = sex[e];
     const int64_t d = sd[e];
+    int cnt = 0;
 #pragma unroll 1
     for (int m0 = 0; m0 < T; m0 += 32 * K) {
       if (issued - drained == NS) {
@@ -835,7 +887,7 @@ int main(int argc, char** argv) {
   const int64_t maxtiles = (n + 31) / 32, SL = 64 + maxtiles * 8;
   CK(cudaMalloc(&dPo, (n + 1) * 4)); CK(cudaMalloc(&dtk, SL * 8 * 64)); CK(cudaMalloc(&dtot, 16));
   int launch_no = 0;
-#define F(K, MB, SP, GPW) FD(K, MB, SP, GPW, 0, 8, false)
+#define F(K, MB, SP, GPW) FD(K, MB, SP, GPW, 0, 8, 0)
 #define FD(K, MB, SP, GPW, DBG, NW, OWN)                                                                          \
   launch_no = 0; CK(cudaMemset(dtk, 0, SL * 8 * 64));                                                \
   run("fused K" #K " minb" #MB " sp" #SP " gpw" #GPW " nw" #NW " own" #OWN, [&] {                                          \
@@ -847,9 +899,9 @@ int main(int argc, char** argv) {
   }, true);
   run("gather K12 pol0 sp1 grid489", [&] { gather_k<12, 0, 1><<<489, 256>>>(n, dl, doff, dP, dpool, dout); }, true);
   F(12, 4, 1, 8)
-  FD(12, 8, 1, 8, 0, 4, true)
-  FD(12, 4, 1, 7, 0, 8, true)
-  FD(10, 4, 1, 8, 0, 8, true)
+  FD(12, 4, 1, 8, 4, 8, 0)
+  FD(12, 4, 1, 7, 4, 8, 0)
+  FD(12, 4, 1, 8, 4, 8, 2)
   run("gather_o K12", [&] { gather_o<12><<<nsm * 8, 256>>>(n, dl, doff, dP, dpool, dout); }, true);
   run("gather_o K16", [&] { gather_o<16><<<nsm * 8, 256>>>(n, dl, doff, dP, dpool, dout); }, true);
 
