@@ -12,7 +12,7 @@ for j in $jobs; do
     echo "reco rc=$?"; continue
   fi
   case $j in
-    jagged) k='regex:pack_fused' ;;
+    jagged) k='regex:pack_reg|pack_fused' ;;
     sensor_calnoise) k='regex:calibrate_kernel|noise_kernel' ;;
     *) k='regex:convert_kernel' ;;
   esac
