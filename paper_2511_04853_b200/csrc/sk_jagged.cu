@@ -30,6 +30,8 @@
 // window's members are.
 #include <algorithm>
 #include <atomic>
+#include <chrono>
+#include <random>
 #include <cstdio>
 #include <cstdlib>
 #include <type_traits>
@@ -1446,7 +1448,10 @@ __global__ void __launch_bounds__(RG_NW * 32, 4) pack_reg_kernel(const __grid_co
       }
       if (lane == 0) sE = acc;
     }
-    asm volatile("bar.sync 1, %0;" ::"n"(RG_NW * 32) : "memory");
+    // every warp arrives exactly once, from the gather loop or after it (two call sites): the non-aligned
+    // barrier, after the warp has reconverged
+    __syncwarp();
+    asm volatile("barrier.sync 1, %0;" ::"n"(RG_NW * 32) : "memory");
     E = sE;
     haveE = true;
   };
@@ -1846,6 +1851,20 @@ static int launch_reg_ms(jag::RegArgs R, uint8_t* scratch, cudaStream_t s) {
   return SK_OK;
 }
 
+// launch generations for the scratch words that are not zeroed between calls (queue entries, look-back
+// words). The scratch may hold words a previous process wrote with its own generations, so the sequence
+// starts at a random 61-bit point: a stale word matches a live generation with probability ~2^-61.
+static unsigned long long next_generation() {
+  static std::atomic<unsigned long long> g{[] {
+    std::random_device rd;
+    const unsigned long long r = (static_cast<unsigned long long>(rd()) << 32) ^ rd() ^
+                                 static_cast<unsigned long long>(
+                                     std::chrono::steady_clock::now().time_since_epoch().count());
+    return (r & ((1ull << 61) - 1)) | 1;
+  }()};
+  return (++g) & ((1ull << 62) - 1);  // gen << 2 must not lose bits that matter
+}
+
 static bool reg_pack_ok() {
   static int v = -1;
   if (v < 0) {
@@ -1992,8 +2011,7 @@ int sk_jagged_pack(int64_t n, const void* lens, int lens_type, void* prefix, int
     R.dst = A.dst[0];
     R.capacity = capacity;
     R.src_members = src_members;
-    static std::atomic<unsigned long long> reg_generation{0};
-    R.gen = ++reg_generation;
+    R.gen = next_generation();
     uint8_t* sc = static_cast<uint8_t*>(scratch);
     return A.field_size[0] == 8 ? launch_reg_ms<8>(R, sc, s) : launch_reg_ms<4>(R, sc, s);
   }
@@ -2027,8 +2045,7 @@ int sk_jagged_pack(int64_t n, const void* lens, int lens_type, void* prefix, int
     F.dbg = dbg;
     F.src_members = src_members;
     F.bad = total_dev + 1;
-    static std::atomic<unsigned long long> generation{0};
-    F.gen = ++generation;
+    F.gen = next_generation();
     uint8_t* sc = static_cast<uint8_t*>(scratch);
     if (split)
       return member_stride == 16 ? launch_fused_ms<16, true>(F, sc, s, dev, ds)

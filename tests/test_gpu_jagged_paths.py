@@ -423,3 +423,37 @@ def _expect_pool(lens, offs, pool):
     P = np.concatenate([[0], np.cumsum(lens.astype(np.int64))]).astype(np.int32)
     idx, _ = _gather_index(lens, offs)
     return P, pool[idx]
+
+
+def test_pack_on_reused_dirty_scratch():
+    """The single-field pack zeroes nothing in its scratch between calls (its look-back words and queue
+    entries carry a launch generation). One scratch buffer, filled with random bytes first, then reused
+    by packs of different sizes, including skewed lengths that take the queue path."""
+    rng = np.random.default_rng(31)
+    n_max = 1_000_000
+    need = C.c_size_t(0)
+    nat.call("sk_jagged_scratch_bytes", n_max, C.byref(need))
+    scratch = DeviceArray.from_numpy(rng.integers(0, 256, need.value, dtype=np.uint8), CUDA)
+    total = DeviceArray(2, np.int64, CUDA)
+    cases = [_inputs(n_max, 20, seed=1), _inputs(100_000, 20, seed=2), _skewed_inputs(200_000, seed=5),
+             _inputs(n_max, 20, seed=3), _inputs(7, 20, seed=4)]
+    try:
+        for lens, offs, plen in cases:
+            n, T = lens.size, int(lens.astype(np.int64).sum())
+            pool = rng.integers(0, 256, plen * 8, dtype=np.uint8)
+            d_lens, d_offs, d_pool = (DeviceArray.from_numpy(x, CUDA) for x in (lens, offs, pool))
+            prefix = DeviceArray(n + 1, np.int64, CUDA)
+            out = DeviceArray(max(T, 1) * 8, np.uint8, CUDA)
+            foff, fsz, dst = (C.c_int64 * 1)(0), (C.c_int32 * 1)(8), (C.c_void_p * 1)(out.ptr)
+            nat.call("sk_jagged_pack", n, d_lens.ptr, TC["i32"], prefix.ptr, TC["i64"], d_offs.ptr, d_pool.ptr,
+                     plen, 8, 1, foff, fsz, dst, T, scratch.ptr, scratch.n, total.ptr, nat.stream(0))
+            nat.sync(0)
+            pw, want, tw = _expect(lens, offs, pool, 8, [(0, 8)], "i64")
+            assert total.numpy().tolist() == [tw, 0]
+            assert prefix.numpy().tobytes() == pw.tobytes()
+            assert out.numpy()[:T * 8].tobytes() == want[0]
+            for a in (d_lens, d_offs, d_pool, prefix, out):
+                a.free()
+    finally:
+        scratch.free()
+        total.free()
