@@ -1288,6 +1288,7 @@ struct RegArgs {
   RegEntry* q;
   int64_t qmax;
   unsigned long long gen;
+  int gpw;              // groups of 32 records per warp and tile (1..RG_GPW)
 };
 
 template <int MS, bool PACKED>
@@ -1361,7 +1362,10 @@ __global__ void __launch_bounds__(RG_NW * 32, 4) pack_reg_kernel(const __grid_co
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   // tiles in block order: a tile waits only on lower-indexed blocks, which in-order dispatch has started
   // (the look-back assumption of CUB's single-pass scan)
-  const int64_t t = blockIdx.x, rw = t * RG_TR + warp * (RG_GPW * 32);
+  // F.gpw (<= RG_GPW) groups per warp and tile: fewer for small inputs, so the tiles cover the SMs;
+  // group slots past it are empty groups
+  const int64_t tile_recs = static_cast<int64_t>(RG_NW * 32) * F.gpw;
+  const int64_t t = blockIdx.x, rw = t * tile_recs + warp * (F.gpw * 32);
   const unsigned long long gen2 = F.gen << 2;
   // the previous kernel in the stream has completed (lengths final, scratch no longer in use)
   pdl_wait_prior();
@@ -1376,8 +1380,9 @@ __global__ void __launch_bounds__(RG_NW * 32, 4) pack_reg_kernel(const __grid_co
 #pragma unroll
   for (int k = 0; k < RG_GPW; ++k) {
     const int64_t r = rw + k * 32 + lane;
-    len[k] = r < F.n ? static_cast<LT>(load_int(F.lens, F.lens_type, r)) : 0;
-    off[k] = r < F.n ? F.src_off[r] : 0;
+    const bool in = k < F.gpw && r < F.n;
+    len[k] = in ? static_cast<LT>(load_int(F.lens, F.lens_type, r)) : 0;
+    off[k] = in ? F.src_off[r] : 0;
   }
   int64_t wsum = 0;
   unsigned nbad = 0;
@@ -1538,9 +1543,9 @@ __global__ void __launch_bounds__(RG_NW * 32, 4) pack_reg_kernel(const __grid_co
   for (int k = 0; k < RG_GPW; ++k) {
     const int64_t r = rw + k * 32 + lane;
     const int e = warp * (RG_GPW * 32) + k * 32 + lane;
-    if (r < F.n) store_int(F.prefix, F.prefix_type, r, E + Wo + sGb[warp * RG_GPW + k] + sEx[e]);
+    if (k < F.gpw && r < F.n) store_int(F.prefix, F.prefix_type, r, E + Wo + sGb[warp * RG_GPW + k] + sEx[e]);
   }
-  if (tid == 0 && t * RG_TR + RG_TR >= F.n) {
+  if (tid == 0 && (t + 1) * tile_recs >= F.n) {
     store_int(F.prefix, F.prefix_type, F.n, E + A);
     *F.total = E + A;
   }
@@ -1668,10 +1673,16 @@ static size_t fused_scratch_bytes(int64_t n) {
 
 // register-gather pack scratch: header, one look-back status word per tile, the queue of skewed groups
 static int64_t reg_queue_entries(int64_t n) { return std::min<int64_t>(jag::RG_QMAX, (n + 31) / 32); }
-static size_t reg_status_bytes(int64_t n) {
-  const int64_t t = (n + jag::RG_TR - 1) / jag::RG_TR;
-  return static_cast<size_t>(t) * sizeof(jag::RegStatus);
+// groups per warp: the full RG_GPW once the 8-warp tiles fill 4 CTAs per SM, fewer below that (small inputs
+// still spread over the SMs); tiles <= min(n / 256, n / 2048 + 4 * SMs + 1)
+static int reg_gpw(int64_t n, int sm_count) {
+  const int64_t groups = (n + 31) / 32, warps = static_cast<int64_t>(sm_count) * 4 * jag::RG_NW;
+  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(jag::RG_GPW, (groups + warps - 1) / warps)));
 }
+static int64_t reg_tiles_max(int64_t n) {  // any device (up to 1024 SMs)
+  return std::min<int64_t>((n + 255) / 256, (n + jag::RG_TR - 1) / jag::RG_TR + 4 * 1024 + 1);
+}
+static size_t reg_status_bytes(int64_t n) { return static_cast<size_t>(reg_tiles_max(n)) * sizeof(jag::RegStatus); }
 static size_t reg_scratch_bytes(int64_t n) {
   return 64 + reg_status_bytes(n) + static_cast<size_t>(reg_queue_entries(n)) * sizeof(jag::RegEntry);
 }
@@ -1837,9 +1848,12 @@ static int launch_fused_ms(jag::FusedArgs F, uint8_t* scratch, cudaStream_t s, i
 }
 
 template <int MS>
-static int launch_reg_ms(jag::RegArgs R, uint8_t* scratch, cudaStream_t s) {
+static int launch_reg_ms(jag::RegArgs R, uint8_t* scratch, cudaStream_t s, int sm_count) {
   // no scratch zeroing: the kernel's flags carry the launch generation, tile 0 resets the counters
-  const int64_t ntiles = (R.n + jag::RG_TR - 1) / jag::RG_TR;
+  R.gpw = reg_gpw(R.n, sm_count);
+  const int64_t tile_recs = static_cast<int64_t>(jag::RG_NW * 32) * R.gpw;
+  const int64_t ntiles = (R.n + tile_recs - 1) / tile_recs;
+  if (ntiles > reg_tiles_max(R.n)) return set_error(SK_ERR_INVALID, "jagged pack: %lld tiles exceed the scratch layout", (long long)ntiles);
   R.hdr = reinterpret_cast<jag::RegHdr*>(scratch);
   R.status = reinterpret_cast<jag::RegStatus*>(scratch + 64);
   R.q = reinterpret_cast<jag::RegEntry*>(scratch + 64 + reg_status_bytes(R.n));
@@ -2013,7 +2027,9 @@ int sk_jagged_pack(int64_t n, const void* lens, int lens_type, void* prefix, int
     R.src_members = src_members;
     R.gen = next_generation();
     uint8_t* sc = static_cast<uint8_t*>(scratch);
-    return A.field_size[0] == 8 ? launch_reg_ms<8>(R, sc, s) : launch_reg_ms<4>(R, sc, s);
+    DeviceState* ds = nullptr;
+    if (int rc = device_state(dev, &ds)) return rc;
+    return A.field_size[0] == 8 ? launch_reg_ms<8>(R, sc, s, ds->sm_count) : launch_reg_ms<4>(R, sc, s, ds->sm_count);
   }
   if (fused_pack_ok() && (single || split)) {
     DeviceState* ds = nullptr;
