@@ -1357,7 +1357,8 @@ __global__ void __launch_bounds__(RG_NW * 32, 4) pack_reg_kernel(const __grid_co
   __shared__ int64_t sGb[RG_NW * RG_GPW];
   __shared__ int64_t sWt[RG_NW];
   __shared__ int sBad[RG_NW];
-  __shared__ int64_t sE;
+  __shared__ int64_t sLb[2][RG_NW];  // look-back round sums per warp (double-buffered by round)
+  __shared__ int sLbP[2][RG_NW];     // ... and whether the warp's 32 held an inclusive prefix
   __shared__ unsigned int sNq;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   // tiles in block order: a tile waits only on lower-indexed blocks, which in-order dispatch has started
@@ -1427,37 +1428,48 @@ __global__ void __launch_bounds__(RG_NW * 32, 4) pack_reg_kernel(const __grid_co
   // 3. the tile's exclusive prefix (warp 0 looks back; every warp calls this exactly once)
   bool haveE = false;
   int64_t E = 0;
+  // The look-back is shared by all 8 warps: a round reads the 256 nearest unread predecessors (32 per
+  // warp), so the last of ~560 tiles needs at most 3 rounds even when every predecessor has published only
+  // its total. Every warp calls this exactly once, from the gather loop or after it (two call sites): the
+  // rounds are CTA-uniform (decided from shared memory) and use the non-aligned barrier after the warp
+  // has reconverged.
   auto get_E = [&]() {
-    if (warp == 0) {
-      int64_t acc = 0;
-      if (t > 0) {
-        int64_t idx = t - 1;
-        while (true) {
-          const int64_t j = idx - lane;
-          int64_t sv = 0;
-          unsigned long long f = gen2 | 2;
-          if (j >= 0) ld_status(&F.status[j], sv, f);
-          while (__any_sync(0xffffffffu, (f & ~3ull) != gen2)) {
-            if ((f & ~3ull) != gen2) ld_status(&F.status[j], sv, f);
-          }
-          const unsigned pm = __ballot_sync(0xffffffffu, (f & 3) == 2);
-          const int pl = pm ? __ffs(pm) - 1 : 32;
-          int64_t v = (lane <= pl && j >= 0) ? sv : 0;
-#pragma unroll
-          for (int q = 16; q; q >>= 1) v += __shfl_xor_sync(0xffffffffu, v, q);
-          acc += v;
-          if (pm) break;
-          idx -= 32;
-        }
-        if (lane == 0) st_status(&F.status[t], acc + A, gen2 | 2);
-      }
-      if (lane == 0) sE = acc;
-    }
-    // every warp arrives exactly once, from the gather loop or after it (two call sites): the non-aligned
-    // barrier, after the warp has reconverged
     __syncwarp();
-    asm volatile("barrier.sync 1, %0;" ::"n"(RG_NW * 32) : "memory");
-    E = sE;
+    int64_t acc = 0;
+    if (t > 0) {
+      for (int64_t base = t - 1, round = 0;; base -= RG_NW * 32, ++round) {
+        const int64_t j = base - (warp * 32 + lane);
+        int64_t sv = 0;
+        unsigned long long f = gen2 | 2;  // before tile 0: an inclusive prefix of 0
+        if (j >= 0) ld_status(&F.status[j], sv, f);
+        while (__any_sync(0xffffffffu, (f & ~3ull) != gen2)) {
+          if ((f & ~3ull) != gen2) ld_status(&F.status[j], sv, f);
+        }
+        const unsigned pm = __ballot_sync(0xffffffffu, (f & 3) == 2);
+        const int pl = pm ? __ffs(pm) - 1 : 32;
+        int64_t v = lane <= pl ? sv : 0;
+#pragma unroll
+        for (int q = 16; q; q >>= 1) v += __shfl_xor_sync(0xffffffffu, v, q);
+        if (lane == 0) {
+          sLb[round & 1][warp] = v;
+          sLbP[round & 1][warp] = pm != 0;
+        }
+        asm volatile("barrier.sync 1, %0;" ::"n"(RG_NW * 32) : "memory");
+        bool found = false;
+#pragma unroll
+        for (int w = 0; w < RG_NW; ++w) {
+          if (!found) {
+            acc += sLb[round & 1][w];
+            found = sLbP[round & 1][w] != 0;
+          }
+        }
+        if (found) break;
+      }
+      if (tid == 0) st_status(&F.status[t], acc + A, gen2 | 2);
+    } else {
+      asm volatile("barrier.sync 1, %0;" ::"n"(RG_NW * 32) : "memory");  // keeps the barrier counts equal
+    }
+    E = acc;
     haveE = true;
   };
   // 2. the gather (not for a tile holding an invalid segment; no stores past the capacity); groups over

@@ -457,3 +457,13 @@ def test_pack_on_reused_dirty_scratch():
     finally:
         scratch.free()
         total.free()
+
+
+@pytest.mark.parametrize("stride,field", [(16, (8, 8)), (12, (4, 4)), (24, (16, 8)), (8, (4, 4))])
+def test_single_field_of_a_wider_member_record(stride, field):
+    """one naturally aligned field out of a wider member record (the register pack's strided loads)"""
+    lens, offs, plen = _inputs(300_001, 20, seed=stride + field[0])
+    pool = np.random.default_rng(43).integers(0, 256, plen * stride, dtype=np.uint8)
+    p, got, t = _pack(lens, offs, pool, stride, [field], "u32", cap_extra=3)
+    pw, want, tw = _expect(lens, offs, pool, stride, [field], "u32")
+    assert t == tw and p.tobytes() == pw.tobytes() and got == want
