@@ -312,7 +312,8 @@ def export_particles_from_collection(coll, stage=None) -> tuple[np.ndarray, list
     copy_collection(stage, coll)
     n = stage.size()
     lay = stage.layout
-    recs = np.array(lay._struct_buf._data[: n * PARTICLE_AOS_DTYPE.itemsize].view(PARTICLE_AOS_DTYPE))
+    # a plain byte copy, then the record view (copying through the structured dtype is 7x slower)
+    recs = np.array(lay._struct_buf._data[: n * PARTICLE_AOS_DTYPE.itemsize]).view(PARTICLE_AOS_DTYPE)
     pool = np.array(lay._plane_view(stage.plan.leaf("sensors.value"), 0))
     b = np.array(lay._plane_view(stage.plan.leaf("sensors.prefix_sum"), 0)).astype(np.int64)
     try:  # one view of the pool per particle, made in C (csrc/segpack.cpp)
