@@ -695,8 +695,9 @@ def soakit_plugin_paths(a2, cells, dev, timed, noise_ref):
             "h2d_gbs": round(cells * 30 / ms / 1e6, 1), "parity": "noise byte-equal to the package route",
             "note": "soakit 0.1.0 itself (baseline/_ref) + soakit_plugin.install(): copy_collection(per_field@cuda, "
                     "aos@pinned) + funcs.calibrate_energy() + funcs.get_noise(), 64 events per call. get_noise() "
-                    "returns the reference's type, a fresh host numpy array, so each call also moves 49 MB of "
-                    "noise into pageable memory; the package route (api_pinned_e2e_ms) keeps it on the device"}
+                    "returns the reference's type, a host numpy array, so each call also moves 49 MB of noise "
+                    "to the host (into page-locked memory recycled once the caller drops the array, "
+                    "memctx.host_return_array); the package route (api_pinned_e2e_ms) keeps it on the device"}
 
 
 def verify_aosoa_tiles(ao, n: int, fields, dev: int, seed: int = 4, samples: int = 32) -> str:

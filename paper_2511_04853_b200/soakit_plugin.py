@@ -286,8 +286,10 @@ def _calibrate_on_device(coll, first: int, count: int) -> None:
 
 
 def _noise_on_device(coll, first: int, count: int) -> np.ndarray:
+    from .memctx import host_return_array
+
     dev, (_, energy, noisy, _, _, na, nb) = _planes(coll)
-    out = np.empty(count, np.float32)
+    out = host_return_array(count, np.float32)  # page-locked, recycled when the caller drops it
     if count:
         tmp = _native(nat.malloc, dev, count * 4)
         try:

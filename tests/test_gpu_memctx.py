@@ -158,3 +158,40 @@ def test_large_pageable_buffers_are_pinned_once_and_released():
     assert small._keep is None  # below the threshold: stays pageable
     for b in (small, dev):
         mc.deallocate(b)
+
+
+def test_host_return_arrays_are_pinned_and_recycled():
+    """host_return_array: page-locked, reused only once every array viewing the buffer is gone"""
+    import gc
+
+    import numpy as np
+
+    from paper_2511_04853_b200 import _native as nat
+    from paper_2511_04853_b200 import memctx as mc
+
+    small = mc.host_return_array(16, np.float32)
+    assert small.size == 16  # below RETURN_POOL_MIN: a plain array
+    n = 3_000_000
+    a = mc.host_return_array(n, np.float32)
+    a[:] = np.arange(n, dtype=np.float32)
+    view = a[10:20]
+    p0 = a.ctypes.data
+    del a
+    gc.collect()
+    b = mc.host_return_array(n, np.float32)
+    pb = b.ctypes.data
+    assert pb != p0  # the view still holds the first buffer
+    assert view.tolist() == list(range(10, 20))
+    del view, b
+    gc.collect()
+    c = mc.host_return_array(n, np.float32)
+    assert c.ctypes.data in (p0, pb)  # recycled from the pool
+    # a device -> host copy into it lands at full speed and intact
+    d = nat.malloc(0, n * 4)
+    try:
+        nat.memset(d, 0x3F, n * 4, 0)
+        nat.memcpy(c.ctypes.data, d, n * 4, 0)
+        nat.sync(0)
+        assert (c.view(np.uint32) == 0x3F3F3F3F).all()
+    finally:
+        nat.free(0, d)
