@@ -53,7 +53,7 @@ class DeviceArray:
     def numpy(self) -> np.ndarray:
         if self.buffer._host is not None:
             return np.array(self.buffer._data[: self.nbytes].view(self.dtype))
-        out = np.empty(self.n, dtype=self.dtype)
+        out = memctx.host_return_array(self.n, self.dtype)  # page-locked when large
         if out.nbytes:
             nat.memcpy(out.ctypes.data, self.ptr, out.nbytes, self.device)
             nat.sync(self.device)
