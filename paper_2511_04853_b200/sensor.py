@@ -312,9 +312,15 @@ def export_particles_from_collection(coll, stage=None) -> tuple[np.ndarray, list
     copy_collection(stage, coll)
     n = stage.size()
     lay = stage.layout
-    # a plain byte copy, then the record view (copying through the structured dtype is 7x slower)
-    recs = np.array(lay._struct_buf._data[: n * PARTICLE_AOS_DTYPE.itemsize]).view(PARTICLE_AOS_DTYPE)
-    pool = np.array(lay._plane_view(stage.plan.leaf("sensors.value"), 0))
+    # plain byte copies into recycled page-locked arrays, then the record view (copying through the
+    # structured dtype is 7x slower, fresh pageable arrays fault in every page)
+    nrec = n * PARTICLE_AOS_DTYPE.itemsize
+    recs = memctx.host_return_array(nrec, np.uint8)
+    recs[:] = lay._struct_buf._data[:nrec]
+    recs = recs.view(PARTICLE_AOS_DTYPE)
+    src_pool = lay._plane_view(stage.plan.leaf("sensors.value"), 0)
+    pool = memctx.host_return_array(src_pool.size, src_pool.dtype)
+    pool[:] = src_pool
     b = np.array(lay._plane_view(stage.plan.leaf("sensors.prefix_sum"), 0)).astype(np.int64)
     try:  # one view of the pool per particle, made in C (csrc/segpack.cpp)
         from . import _segpack
