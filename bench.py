@@ -1014,6 +1014,23 @@ def run_extras(args, dev: int) -> dict:
                                                   "frac": round(n4 * 76 / ms / 1e6 / peak, 3),
                                                   "parity": verify_aosoa_tiles(ao, n4, fields, dev, samples=8)}
         ao.free()
+    # the same conversion from HOST records: a 16M-track pinned sample through the API, the H2D chunked
+    # and overlapped with the conversion on the device (first and last tiles checked)
+    nh = 16_000_000
+    h4 = coll(wl.TRACK_SCHEMA, ly.AOS, nh, mc.ContextInfo.pinned())
+    nat.memcpy(h4.layout._struct_buf._data.ctypes.data, a4.layout._struct_buf.ptr, nh * 60, dev)
+    nat.sync(dev)
+    ao = sk.Aosoa(nh, 128, fields, cuda)
+    ms_h = timed(lambda: sk.to_aosoa(h4, fields, 128, out=ao), steps=5, warmup=1)
+    out["config4_aosoa_100M"]["host_input_e2e"] = {
+        "objects": nh, "ms": round(ms_h, 3), "objects_per_s": round(nh / ms_h * 1e3),
+        "gbs": round(nh * 76 / ms_h / 1e6, 1), "h2d_gbs": round(nh * 60 / ms_h / 1e6, 1),
+        "h2d_bytes": nh * 60, "parity": verify_aosoa_tiles(ao, nh, fields, dev, samples=4),
+        "note": "to_aosoa(pinned Track AoS collection, fields, 128, out=device Aosoa): the host records go "
+                "over the link in chunks overlapped with the AoSoA conversion on the device; gbs counts the "
+                "same 76 algorithmic bytes per object as the device-resident line"}
+    ao.free()
+    h4.free()
     a4.free()
     busy.free()
     return out
