@@ -1307,22 +1307,14 @@ __device__ __forceinline__ void rg_wait_tile0(const RegArgs& F, unsigned long lo
   while ((ld_acquire(&F.status[0].tag) & ~3ull) != gen2) __nanosleep(32);
 }
 
-// a queued group's members [m_begin, m_end): its records' prefixes are rebuilt
-// from the lengths (64-bit search: such a group may exceed 2^31 members)
+// members [m_begin, m_end) of a group of up to 32 records whose group-local exclusive prefixes are `ex`
+// (lane = record) and source bases `d` (= src_off - ex): member m of the group goes to dst[out0 + m].
+// 64-bit search: such a group may exceed 2^31 members.
 template <int MS, bool PACKED>
-__device__ __forceinline__ void rg_gather_big(const RegArgs& F, const RegEntry& ent, int64_t m_begin, int64_t m_end) {
+__device__ __forceinline__ void span_gather(const uint8_t* src, int64_t stride, uint8_t* dst, int64_t ex, int64_t d,
+                                            int64_t out0, int64_t m_begin, int64_t m_end) {
   using V = typename MemberWord<MS>::T;
   const int lane = threadIdx.x & 31;
-  const int64_t r = ent.rec0 + lane;
-  const int64_t len = lane < ent.cnt ? load_int(F.lens, F.lens_type, r) : 0;
-  const int64_t off = lane < ent.cnt ? F.src_off[r] : 0;
-  int64_t x = len;
-#pragma unroll
-  for (int s = 1; s < 32; s <<= 1) {
-    const int64_t y = __shfl_up_sync(0xffffffffu, x, s);
-    if (lane >= s) x += y;
-  }
-  const int64_t ex = x - len, d = off - ex;
   for (int64_t m0 = m_begin; m0 < m_end; m0 += 32 * RG_K) {
     V v[RG_K];
 #pragma unroll
@@ -1336,15 +1328,32 @@ __device__ __forceinline__ void rg_gather_big(const RegArgs& F, const RegEntry& 
           if (e <= m) lo += s;
         }
         const int64_t dd = __shfl_sync(0xffffffffu, d, lo);
-        if (m < m_end) v[q] = rg_load<MS, PACKED>(F, dd + m);
+        if (m < m_end)
+          v[q] = PACKED ? reinterpret_cast<const V*>(src)[dd + m] : *reinterpret_cast<const V*>(src + (dd + m) * stride);
       }
     }
 #pragma unroll
     for (int q = 0; q < RG_K; ++q) {
       const int64_t m = m0 + q * 32 + lane;
-      if (m < m_end) rg_store<MS>(F, ent.out0 + m, v[q]);
+      if (m < m_end) __stcs(reinterpret_cast<V*>(dst) + out0 + m, v[q]);
     }
   }
+}
+
+// a queued group's members [m_begin, m_end): its records' prefixes are rebuilt from the lengths
+template <int MS, bool PACKED>
+__device__ __forceinline__ void rg_gather_big(const RegArgs& F, const RegEntry& ent, int64_t m_begin, int64_t m_end) {
+  const int lane = threadIdx.x & 31;
+  const int64_t r = ent.rec0 + lane;
+  const int64_t len = lane < ent.cnt ? load_int(F.lens, F.lens_type, r) : 0;
+  const int64_t off = lane < ent.cnt ? F.src_off[r] : 0;
+  int64_t x = len;
+#pragma unroll
+  for (int s = 1; s < 32; s <<= 1) {
+    const int64_t y = __shfl_up_sync(0xffffffffu, x, s);
+    if (lane >= s) x += y;
+  }
+  span_gather<MS, PACKED>(F.src, F.member_stride, F.dst, x - len, off - (x - len), ent.out0, m_begin, m_end);
 }
 
 // WIDE: 64-bit or u32 lengths (held as int64 while the loads fly); otherwise int32
@@ -1584,6 +1593,141 @@ __global__ void __launch_bounds__(RG_NW * 32, 4) pack_reg_kernel(const __grid_co
       if (static_cast<int64_t>(c) >= nch) break;
       const int64_t mb = static_cast<int64_t>(c) * RG_CHUNK;
       rg_gather_big<MS, PACKED>(F, ent, mb, min(ent.T, mb + RG_CHUNK));
+    }
+  }
+}
+
+// ---- gather over a given prefix, register version (sk_jagged_scatter, one 4/8-byte field) ----
+//
+// A warp takes groups of 32 records (grid-stride): the group's base and end come from the prefix, each
+// lane's record offset inside the group from its prefix element, and the members move as in
+// pack_reg_kernel (12 register rounds in flight per warp). A group over RG_BIG members is queued and its
+// 1536-member chunks shared out by every warp that finishes (an entry queued later is drained by its
+// owner). tools/jag_micro.cu measured this structure at 37.9 us on config 3 (the window gather: 55 us).
+struct ScatRegArgs {
+  int64_t n;
+  const void* prefix;  // non-wrapped
+  const int64_t* src_off;
+  const uint8_t* src;  // pool + field offset
+  int64_t member_stride;
+  uint8_t* dst;
+  int64_t total;       // members gathered: positions >= total are skipped
+  RegEntry* q;
+  unsigned int* nq;    // zeroed by block 0, which then publishes `ready` with this launch's generation
+  RegStatus* ready;
+  int64_t qmax;
+  unsigned long long gen;
+};
+
+// block 0 has zeroed the queue counter of this launch
+__device__ __forceinline__ void scat_wait_ready(const ScatRegArgs& A) {
+  while ((ld_acquire(&A.ready->tag) & ~3ull) != (A.gen << 2)) __nanosleep(32);
+}
+
+// a group over RG_BIG members: queued for every warp to share (a full queue: gathered here)
+template <int MS, bool PACKED>
+__device__ __forceinline__ void scatter_big_group(const ScatRegArgs& A, int64_t r0, int cnt, int64_t B, int64_t T,
+                                               int64_t ex, int64_t d) {
+  const int lane = threadIdx.x & 31;
+  unsigned slot = 0;
+  if (lane == 0) {
+    scat_wait_ready(A);
+    slot = atomicAdd(A.nq, 1u);
+  }
+  slot = __shfl_sync(0xffffffffu, slot, 0);
+  if (slot < A.qmax) {
+    if (lane == 0) {
+      RegEntry& qe = A.q[slot];
+      qe.rec0 = r0;
+      qe.cnt = cnt;
+      qe.out0 = B;
+      qe.T = T;
+      qe.next = 0;
+      __threadfence();
+      st_release(&qe.ready, A.gen);
+    }
+  } else {
+    span_gather<MS, PACKED>(A.src, A.member_stride, A.dst, ex, d, B, 0, T);
+  }
+}
+
+template <class PT, int MS, bool PACKED>
+__global__ void __launch_bounds__(256, 4) scatter_reg_kernel(const __grid_constant__ ScatRegArgs A) {
+  using V = typename MemberWord<MS>::T;
+  const int lane = threadIdx.x & 31;
+  const PT* P = static_cast<const PT*>(A.prefix);
+  const int64_t ngroups = (A.n + 31) / 32;
+  const int64_t nw = static_cast<int64_t>(gridDim.x) * (blockDim.x / 32);
+  pdl_wait_prior();
+  if (blockIdx.x == 0 && threadIdx.x == 0) {  // the queue buffer is fresh: no zeroing launch
+    *A.nq = 0;
+    __threadfence();
+    st_status(A.ready, 0, A.gen << 2 | 2);
+  }
+#pragma unroll 1
+  for (int64_t g = static_cast<int64_t>(blockIdx.x) * (blockDim.x / 32) + (threadIdx.x >> 5); g < ngroups; g += nw) {
+    const int64_t r0 = g * 32, r = r0 + lane;
+    const int cnt = static_cast<int>(min(static_cast<int64_t>(32), A.n - r0));
+    const int64_t B = static_cast<int64_t>(P[r0]);
+    const int64_t Pe = static_cast<int64_t>(P[r0 + cnt]);
+    const int64_t T = min(Pe, A.total) - B;  // past the total: not gathered
+    if (T <= 0) continue;
+    const int64_t pr = lane < cnt ? static_cast<int64_t>(P[r]) : Pe;
+    const int64_t d64 = (lane < cnt ? A.src_off[r] : 0) - (pr - B);
+    if (T > RG_BIG) {
+      scatter_big_group<MS, PACKED>(A, r0, cnt, B, T, pr - B, d64);
+      continue;
+    }
+    const int ex = static_cast<int>(pr - B);
+    const int Ti = static_cast<int>(T);
+#pragma unroll 1
+    for (int m0 = 0; m0 < Ti; m0 += 32 * RG_K) {
+      V v[RG_K];
+#pragma unroll
+      for (int q = 0; q < RG_K; ++q) {
+        const int m = m0 + q * 32 + lane;
+        if (m0 + q * 32 < Ti) {
+          int lo = 0;
+#pragma unroll
+          for (int s = 16; s >= 1; s >>= 1) {
+            const int ee = __shfl_sync(0xffffffffu, ex, lo + s);
+            if (ee <= m) lo += s;
+          }
+          const int64_t dd = __shfl_sync(0xffffffffu, d64, lo);
+          if (m < Ti)
+            v[q] = PACKED ? reinterpret_cast<const V*>(A.src)[dd + m]
+                          : *reinterpret_cast<const V*>(A.src + (dd + m) * A.member_stride);
+        }
+      }
+      V* ob = reinterpret_cast<V*>(A.dst) + B;
+#pragma unroll
+      for (int q = 0; q < RG_K; ++q) {
+        const int m = m0 + q * 32 + lane;
+        if (m < Ti) __stcs(ob + m, v[q]);
+      }
+    }
+  }
+  // queued groups seen so far (this warp's own included: it reads the count after queueing)
+  if (lane == 0) scat_wait_ready(A);
+  __syncwarp();
+  const unsigned nq = min(static_cast<unsigned>(A.qmax), *reinterpret_cast<volatile unsigned int*>(A.nq));
+  for (unsigned dq = 0; dq < nq; ++dq) {
+    if (lane == 0)
+      while (ld_acquire(&A.q[dq].ready) != A.gen) __nanosleep(64);
+    __syncwarp();
+    const RegEntry ent = A.q[dq];
+    const int64_t r = ent.rec0 + lane;
+    const int64_t Pe = static_cast<int64_t>(P[ent.rec0 + ent.cnt]);
+    const int64_t pr = lane < ent.cnt ? static_cast<int64_t>(P[r]) : Pe;
+    const int64_t ex = pr - ent.out0, d = (lane < ent.cnt ? A.src_off[r] : 0) - ex;
+    const int64_t nch = (ent.T + RG_CHUNK - 1) / RG_CHUNK;
+    while (true) {
+      unsigned long long c = 0;
+      if (lane == 0) c = atomicAdd(&A.q[dq].next, 1ull);
+      c = __shfl_sync(0xffffffffu, c, 0);
+      if (static_cast<int64_t>(c) >= nch) break;
+      const int64_t mb = static_cast<int64_t>(c) * RG_CHUNK;
+      span_gather<MS, PACKED>(A.src, A.member_stride, A.dst, ex, d, ent.out0, mb, min(ent.T, mb + RG_CHUNK));
     }
   }
 }
@@ -1942,6 +2086,55 @@ static int launch_gather(const jag::ScatterArgs& A, int64_t ntasks, cudaStream_t
   }
 }
 
+template <class PT, int MS, bool PACKED>
+static int launch_scatter_reg_t(const jag::ScatRegArgs& R, cudaStream_t s, const DeviceState* ds) {
+  const int64_t groups = (R.n + 31) / 32;
+  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((groups + 7) / 8, static_cast<int64_t>(ds->sm_count) * 8));
+  SK_TRY(launch_pdl(jag::scatter_reg_kernel<PT, MS, PACKED>, dim3(static_cast<unsigned>(grid)), dim3(256), s, R));
+  return SK_OK;
+}
+
+template <class PT>
+static int launch_scatter_reg_p(const jag::ScatRegArgs& R, int ms, cudaStream_t s, const DeviceState* ds) {
+  const bool packed = R.member_stride == ms;
+  if (ms == 8)
+    return packed ? launch_scatter_reg_t<PT, 8, true>(R, s, ds) : launch_scatter_reg_t<PT, 8, false>(R, s, ds);
+  return packed ? launch_scatter_reg_t<PT, 4, true>(R, s, ds) : launch_scatter_reg_t<PT, 4, false>(R, s, ds);
+}
+
+// sk_jagged_scatter with one naturally aligned 4/8-byte field: the register gather over the given prefix
+static int launch_scatter_reg(const jag::ScatterArgs& A, cudaStream_t s, int dev) {
+  DeviceState* ds = nullptr;
+  if (int rc = device_state(dev, &ds)) return rc;
+  jag::ScatRegArgs R{};
+  R.n = A.n;
+  R.prefix = A.prefix;
+  R.src_off = A.src_off;
+  R.src = A.src_pool + A.field_off[0];
+  R.member_stride = A.member_stride;
+  R.dst = A.dst[0];
+  R.total = A.total;
+  R.qmax = reg_queue_entries(A.n);
+  R.gen = next_generation();
+  uint8_t* qbuf = nullptr;
+  const size_t qbytes = 64 + static_cast<size_t>(R.qmax) * sizeof(jag::RegEntry);
+  SK_TRY(cudaMallocAsync(reinterpret_cast<void**>(&qbuf), qbytes, s));
+  R.ready = reinterpret_cast<jag::RegStatus*>(qbuf);
+  R.nq = reinterpret_cast<unsigned int*>(qbuf + 16);
+  R.q = reinterpret_cast<jag::RegEntry*>(qbuf + 64);
+  int rc;
+  switch (A.prefix_type) {
+    case SK_U8: case SK_BOOL: rc = launch_scatter_reg_p<uint8_t>(R, A.field_size[0], s, ds); break;
+    case SK_U16: rc = launch_scatter_reg_p<uint16_t>(R, A.field_size[0], s, ds); break;
+    case SK_U32: rc = launch_scatter_reg_p<uint32_t>(R, A.field_size[0], s, ds); break;
+    case SK_I32: rc = launch_scatter_reg_p<int32_t>(R, A.field_size[0], s, ds); break;
+    case SK_U64: rc = launch_scatter_reg_p<uint64_t>(R, A.field_size[0], s, ds); break;
+    default: rc = launch_scatter_reg_p<int64_t>(R, A.field_size[0], s, ds); break;
+  }
+  SK_TRY(cudaFreeAsync(qbuf, s));
+  return rc;
+}
+
 extern "C" {
 
 int sk_jagged_scatter(int64_t n, const void* prefix, int prefix_type, const int64_t* src_off, const void* src_pool,
@@ -1955,6 +2148,9 @@ int sk_jagged_scatter(int64_t n, const void* prefix, int prefix_type, const int6
   int dev = 0;
   SK_TRY(cudaGetDevice(&dev));
   cudaStream_t s = resolve_stream(dev, stream);
+  if (reg_pack_ok() && nfields == 1 && A.aligned[0] && (A.field_size[0] == 4 || A.field_size[0] == 8) &&
+      reinterpret_cast<uintptr_t>(A.dst[0]) % A.field_size[0] == 0)
+    return launch_scatter_reg(A, s, dev);
   const int64_t ntasks = (total + jag::W - 1) / jag::W;
   // starts[0..ntasks) from a search over the given prefix, starts[ntasks] = 1 + last non-empty record
   int64_t* starts = nullptr;
