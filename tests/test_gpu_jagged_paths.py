@@ -467,3 +467,15 @@ def test_single_field_of_a_wider_member_record(stride, field):
     p, got, t = _pack(lens, offs, pool, stride, [field], "u32", cap_extra=3)
     pw, want, tw = _expect(lens, offs, pool, stride, [field], "u32")
     assert t == tw and p.tobytes() == pw.tobytes() and got == want
+
+
+def test_fused_pack_ten_million_records():
+    """config 3 at 10M clusters (~100M u64 members, shuffled segments with slack): the whole prefix and
+    pool byte-exact against the numpy restatement"""
+    lens, offs, plen = _inputs(10_000_000, 20, seed=77)
+    pool = np.random.default_rng(78).integers(0, np.iinfo(np.uint64).max, plen, dtype=np.uint64,
+                                              endpoint=True).view(np.uint8)
+    p, got, t = _pack(lens, offs, pool, 8, [(0, 8)], "i32", cap_extra=1)
+    pw, want, tw = _expect(lens, offs, pool, 8, [(0, 8)], "i32")
+    assert t == tw and p.tobytes() == pw.tobytes()
+    assert got == want
