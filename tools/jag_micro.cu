@@ -4,6 +4,7 @@
 // policies reach, to pick the design of pack_fused_kernel.
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 tools/jag_micro.cu -o build/jag_micro
 #include <cuda_runtime.h>
+#include <cub/cub.cuh>
 #include <cstdio>
 #include <cstdint>
 #include <cstdlib>
@@ -778,6 +779,91 @@ __global__ void __launch_bounds__(256, MINB) fused_b(int64_t n, const int* __res
   }
 }
 
+__device__ __forceinline__ uint32_t su32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void mb_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mb_expect(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mb_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  do {
+    asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+                 : "=r"(done) : "r"(su32(bar)), "r"(parity) : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void bulk_g2s(void* s, const void* g, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(su32(s)), "l"(g), "r"(bytes), "r"(su32(bar)) : "memory");
+}
+
+// TMA-bulk gather with the prefix given: a warp per group of 32 records, NS groups in flight per warp,
+// each record's 16-byte-aligned covering span copied by one bulk op into the warp's stage
+template <int NS, int NW, int STAGE>
+__global__ void __launch_bounds__(NW * 32, 1) tma_gather(int64_t n, const int* __restrict__ lens,
+    const int64_t* __restrict__ off, const int64_t* __restrict__ P, const uint64_t* __restrict__ pool,
+    uint64_t* __restrict__ out) {
+  extern __shared__ __align__(128) uint8_t dsm_t[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint8_t* stage = dsm_t + warp * NS * STAGE;
+  __shared__ uint64_t bars[NW][NS];
+  __shared__ int sEx[NW][NS][33];
+  __shared__ int sBase[NW][NS][32];
+  __shared__ int64_t sB[NW][NS];
+  if (lane < NS) mb_init(&bars[warp][lane], 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncwarp();
+  const int64_t ngroups = (n + 31) / 32;
+  const int64_t nw = (int64_t)gridDim.x * NW;
+  const int64_t g0 = (int64_t)blockIdx.x * NW + warp;
+  const int64_t mine = g0 < ngroups ? (ngroups - g0 + nw - 1) / nw : 0;
+  auto issue = [&](int64_t i) {  // the warp's i-th group into stage i % NS
+    const int st = int(i % NS);
+    const int64_t g = g0 + i * nw;
+    const int64_t r = g * 32 + lane;
+    const int len = r < n ? lens[r] : 0;
+    const int64_t o = r < n ? off[r] : 0;
+    const int64_t a = (o * 8) & ~int64_t(15), b = ((o + len) * 8 + 15) & ~int64_t(15);
+    const int bytes = len ? int(b - a) : 0;
+    int x = bytes, e = len;
+#pragma unroll
+    for (int s = 1; s < 32; s <<= 1) {
+      const int y = __shfl_up_sync(~0u, x, s), z = __shfl_up_sync(~0u, e, s);
+      if (lane >= s) { x += y; e += z; }
+    }
+    const int tot = __shfl_sync(~0u, x, 31);
+    sEx[warp][st][lane] = e - len;
+    if (lane == 31) sEx[warp][st][32] = e;
+    sBase[warp][st][lane] = (x - bytes) + int((o * 8) & 15);
+    if (lane == 0) { sB[warp][st] = P[g * 32]; mb_expect(&bars[warp][st], uint32_t(tot)); }
+    __syncwarp();
+    if (bytes) bulk_g2s(stage + st * STAGE + (x - bytes), reinterpret_cast<const uint8_t*>(pool) + a, bytes, &bars[warp][st]);
+  };
+  for (int64_t i = 0; i < NS - 1 && i < mine; ++i) issue(i);
+  for (int64_t i = 0; i < mine; ++i) {
+    if (i + NS - 1 < mine) issue(i + NS - 1);
+    const int st = int(i % NS);
+    mb_wait(&bars[warp][st], uint32_t((i / NS) & 1));
+    const int T = sEx[warp][st][32];
+    const int ex = sEx[warp][st][lane], base = sBase[warp][st][lane];
+    const int64_t B = sB[warp][st];
+    const uint8_t* sg = stage + st * STAGE;
+    for (int m0 = 0; m0 < T; m0 += 32) {
+      const int m = m0 + lane;
+      int lo = 0;
+#pragma unroll
+      for (int s = 16; s >= 1; s >>= 1) {
+        const int ee = __shfl_sync(~0u, ex, lo + s);
+        if (ee <= m) lo += s;
+      }
+      const int bs = __shfl_sync(~0u, base, lo), es = __shfl_sync(~0u, ex, lo);
+      if (m < T) __stcs(out + B + m, *reinterpret_cast<const uint64_t*>(sg + bs + (m - es) * 8));
+    }
+    __syncwarp();
+  }
+}
+
 int main(int argc, char** argv) {
   const int64_t n = 1000000;
   const int inorder = argc > 1 ? atoi(argv[1]) : 0;
@@ -897,6 +983,30 @@ int main(int argc, char** argv) {
     ++launch_no;                                                                                     \
     fused_k<K, MB, SP, GPW, DBG, NW, OWN><<<nt, NW * 32>>>(n, dl, doff, dpool, dout, dPo, tk, (uint64_t*)((char*)tk + 64), dtot); \
   }, true);
+
+  {
+    // two kernels: cub exclusive scan of the lengths into int64, then the prefix-given gather
+    void* tmp = nullptr; size_t tb = 0;
+    cub::TransformInputIterator<int64_t, cub::CastOp<int64_t>, const int*> it(dl, cub::CastOp<int64_t>());
+    cub::DeviceScan::ExclusiveSum(tmp, tb, it, dP, n + 1);
+    CK(cudaMalloc(&tmp, tb));
+    run("cub scan only", [&] { cub::DeviceScan::ExclusiveSum(tmp, tb, it, dP, n + 1); }, false);
+    run("cub scan + gather K12 grid8", [&] {
+      cub::DeviceScan::ExclusiveSum(tmp, tb, it, dP, n + 1);
+      gather_k<12, 0, 1><<<nsm * 8, 256>>>(n, dl, doff, dP, dpool, dout);
+    }, true);
+  }
+
+#define TG(NS, NW, STAGE)                                                                                       \
+  {                                                                                                             \
+    const size_t smem = (size_t)NS * NW * STAGE;                                                                \
+    CK(cudaFuncSetAttribute(tma_gather<NS, NW, STAGE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));  \
+    run("tma gather ns" #NS " nw" #NW, [&] { tma_gather<NS, NW, STAGE><<<nsm, NW * 32, smem>>>(n, dl, doff, dP, dpool, dout); }, true); \
+  }
+  TG(4, 8, 6144)
+  TG(8, 4, 6144)
+  TG(3, 10, 6144)
+  TG(2, 16, 6144)
   run("gather K12 pol0 sp1 grid489", [&] { gather_k<12, 0, 1><<<489, 256>>>(n, dl, doff, dP, dpool, dout); }, true);
   F(12, 4, 1, 8)
   FD(12, 4, 1, 8, 4, 8, 0)
