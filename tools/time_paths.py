@@ -11,7 +11,10 @@ from paper_2511_04853_b200 import _native as nat, layouts as ly, sensor, transfe
 PEAK = 6546.9
 cases = [("sensor", sensor.SENSOR_SCHEMA, 30, 64 * 436 * 436), ("particle", sensor.PARTICLE_SCHEMA, 64, 50_000_000),
          ("track", wl.TRACK_SCHEMA, 60, 100_000_000)]
+only = os.environ.get("CASES")
 for name, schema, stride, n in cases:
+    if only and name not in only.split(","):
+        continue
     a, p = coll(schema, ly.AOS, n), coll(schema, ly.PER_FIELD, n)
     wl.fill_random_device(a.layout._struct_buf.ptr, n * stride // 8 * 8, 5, 0)
     for direction, fn in (("a2p", lambda: tr.copy_collection(p, a, {"async": True})),
