@@ -479,3 +479,45 @@ def test_fused_pack_ten_million_records():
     pw, want, tw = _expect(lens, offs, pool, 8, [(0, 8)], "i32")
     assert t == tw and p.tobytes() == pw.tobytes()
     assert got == want
+
+
+def _tiled_inputs(lens, seed, slack=2):
+    rng = np.random.default_rng(seed)
+    order = rng.permutation(lens.size)
+    gaps = lens[order].astype(np.int64) + rng.integers(0, slack + 1, lens.size)
+    offs = np.empty(lens.size, np.int64)
+    offs[order] = np.concatenate([[0], np.cumsum(gaps)[:-1]])
+    return offs, int(gaps.sum())
+
+
+@pytest.mark.parametrize("case", ["round_edges", "big_threshold", "tile_edges", "one_huge", "u8_wrap"])
+def test_register_pack_structural_edges(case):
+    """the register pack's structure: 384-member round boundaries, the 3072-member queueing threshold
+    (3072 gathered by the warp, 3073 queued), record counts at tile boundaries, one record holding
+    almost every member, and a u8 prefix that wraps"""
+    rng = np.random.default_rng(sum(map(ord, case)))
+    ptype = "i64"
+    if case == "round_edges":  # groups of exactly 383, 384, 385, 767, 768, 769 members
+        lens = np.zeros(32 * 6 * 50, np.int32)
+        for g, t in enumerate([383, 384, 385, 767, 768, 769] * 50):
+            q, r = divmod(t, 32)
+            lens[32 * g:32 * g + 32] = q
+            lens[32 * g:32 * g + r] += 1
+    elif case == "big_threshold":  # groups of 3071, 3072, 3073 and 9000 members among ordinary ones
+        lens = rng.integers(0, 21, 40_000).astype(np.int32)
+        for g, t in zip((5, 77, 300, 901), (3071, 3072, 3073, 9000)):
+            lens[32 * g:32 * g + 32] = t // 32
+            lens[32 * g] += t % 32
+    elif case == "tile_edges":  # one past / one short of whole 8-warp tiles at several group counts
+        lens = rng.integers(0, 21, 256 * 7 * 37 + 1).astype(np.int32)
+    elif case == "one_huge":
+        lens = rng.integers(0, 3, 50_000).astype(np.int32)
+        lens[12_345] = 2_000_000
+    else:
+        lens = rng.integers(0, 21, 70_001).astype(np.int32)
+        ptype = "u8"
+    offs, plen = _tiled_inputs(lens, seed=5)
+    pool = rng.integers(0, 256, plen * 8, dtype=np.uint8)
+    p, got, t = _pack(lens, offs, pool, 8, [(0, 8)], ptype, cap_extra=0 if ptype == "u8" else 7)
+    pw, want, tw = _expect(lens, offs, pool, 8, [(0, 8)], ptype)
+    assert t == tw and p.tobytes() == pw.tobytes() and got == want
