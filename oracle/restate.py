@@ -62,7 +62,8 @@ def to_aosoa(records: np.ndarray, fields: list[tuple[str, str]], lanes: int, til
     off = 0
     for (name, code), sz in zip(fields, sizes):
         vals = np.zeros(ntiles * lanes, dtype=_CODES[code])
-        vals[:n] = records[name].astype(_CODES[code])
+        with np.errstate(over="ignore", invalid="ignore"):  # numpy's own cast of random bit patterns
+            vals[:n] = records[name].astype(_CODES[code])
         blocks = vals.view(np.uint8).reshape(ntiles, lanes * sz)
         out.reshape(ntiles, tile_bytes)[:, off : off + lanes * sz] = blocks
         off += lanes * sz
