@@ -618,6 +618,7 @@ static bool peer_bulk() {
 }
 
 constexpr int64_t CHUNK_TARGET = 32ll << 20;  // bytes of the larger side per pipeline chunk
+// (splitting one 5.7 MB event into 4 chunks measured slower: 0.151 -> 0.163 ms per event)
 constexpr int NSLOT = 2;
 
 int run(const sk_conv_desc& d, int device, cudaStream_t s, int epi, float* extra, const int* epi_fields) {
@@ -674,14 +675,16 @@ int run(const sk_conv_desc& d, int device, cudaStream_t s, int epi, float* extra
     ds->staging_bytes = need;
   }
   uint8_t* base = static_cast<uint8_t*>(ds->staging);
-  cudaEvent_t start, in_ready[NSLOT], in_free[NSLOT], out_ready[NSLOT], out_free[NSLOT];
-  SK_TRY(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
-  for (int k = 0; k < NSLOT; ++k) {
-    SK_TRY(cudaEventCreateWithFlags(&in_ready[k], cudaEventDisableTiming));
-    SK_TRY(cudaEventCreateWithFlags(&in_free[k], cudaEventDisableTiming));
-    SK_TRY(cudaEventCreateWithFlags(&out_ready[k], cudaEventDisableTiming));
-    SK_TRY(cudaEventCreateWithFlags(&out_free[k], cudaEventDisableTiming));
-  }
+  // the pipeline's events live with the device state (created once; every use is stream-ordered on the
+  // device's own helper streams, like the staging buffer)
+  static_assert(1 + 4 * NSLOT <= 9, "pipe_events");
+  if (!ds->pipe_events[0])
+    for (cudaEvent_t& e : ds->pipe_events) SK_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  cudaEvent_t start = ds->pipe_events[0];
+  cudaEvent_t* in_ready = ds->pipe_events + 1;
+  cudaEvent_t* in_free = in_ready + NSLOT;
+  cudaEvent_t* out_ready = in_free + NSLOT;
+  cudaEvent_t* out_free = out_ready + NSLOT;
   // the helper streams start after everything already queued on s
   SK_TRY(cudaEventRecord(start, s));
   // fork only the helper streams that get work (an idle fork would be an
@@ -730,13 +733,6 @@ int run(const sk_conv_desc& d, int device, cudaStream_t s, int epi, float* extra
     }
   }
   if (dh) SK_TRY(cudaStreamWaitEvent(s, out_free[(nchunks - 1) % NSLOT], 0));
-  cudaEventDestroy(start);
-  for (int k = 0; k < NSLOT; ++k) {
-    cudaEventDestroy(in_ready[k]);
-    cudaEventDestroy(in_free[k]);
-    cudaEventDestroy(out_ready[k]);
-    cudaEventDestroy(out_free[k]);
-  }
   return SK_OK;
 }
 

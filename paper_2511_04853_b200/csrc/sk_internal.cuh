@@ -34,6 +34,7 @@ struct DeviceState {
   cudaStream_t copy_out = nullptr; // D2H stream of the transfer pipeline
   void* staging = nullptr;         // device staging for host<->device conversions
   size_t staging_bytes = 0;
+  cudaEvent_t pipe_events[9] = {};  // the transfer pipeline's events, created once
 };
 
 // Captured graphs bake in device addresses, the pipeline's staging buffer
