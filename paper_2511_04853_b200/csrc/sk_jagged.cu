@@ -1485,7 +1485,7 @@ __global__ void __launch_bounds__(RG_NW * 32, 4) pack_reg_kernel(const __grid_co
   // RG_BIG members are set aside for the queue
   unsigned big = 0;
 #pragma unroll 1
-  for (int k = 0; k < RG_GPW && !bad; ++k) {
+  for (int k = 0; k < RG_GPW && !bad && F.capacity > 0; ++k) {  // capacity 0: the prefix only
     const int g = warp * RG_GPW + k;
     const int64_t g0 = sGb[g];
     const int64_t T = (k + 1 < RG_GPW ? sGb[g + 1] : sWt[warp]) - g0;

@@ -196,7 +196,6 @@ def pack(coll, path: str, lens, src_offsets, src_pool, member_stride: int | None
     pool_bytes = src_pool.nbytes if isinstance(src_pool, DeviceArray) else np.asarray(src_pool).nbytes
     members = pool_bytes // int(member_stride) if member_stride else 0
     pool_d = _as_device(src_pool, None, dev, keep)
-    checked = False
     if not isinstance(lens, DeviceArray) and not isinstance(src_offsets, DeviceArray):
         # host inputs were copied to the device above: validate them there before anything is written
         # (one small kernel instead of a numpy pass over every record; the reference raises before it
@@ -207,7 +206,6 @@ def pack(coll, path: str, lens, src_offsets, src_pool, member_stride: int | None
                 t.free()
             _check_host_segments(lens, src_offsets, members)  # names the first offending record
             raise _invalid_segments(bad)
-        checked = True
 
     pleaf = plan.leaf(path + ".prefix_sum")
     pcode = pleaf.value_type.storage_code
@@ -222,22 +220,25 @@ def pack(coll, path: str, lens, src_offsets, src_pool, member_stride: int | None
     nf = len(leaves)
     offs = (C.c_int64 * nf)(*[member_offsets[lf.dotted] for lf in leaves])
     sizes = (C.c_int32 * nf)(*[lf.value_type.size_bytes for lf in leaves])
-    if device_resident and lay.capacity(path) > 0:
-        # fused scan + gather bounded by the current pool capacity: one sync
-        cap = lay.capacity(path)
-        ws = _workspace(dev)
-        need = C.c_size_t(0)
-        nat.call("sk_jagged_scratch_bytes", n, C.byref(need))
-        starts_bytes = ((cap + 255) // 256 + 1) * 8  # the gather's work split (one entry per 256 members)
-        scratch = ws.scratch_for(-(-need.value // 256) * 256 + starts_bytes)
-        ptrs = (C.c_void_p * nf)(*[lay.plane_address(lf, 0) for lf in leaves])
-        nat.call("sk_jagged_pack", n, lens_d.ptr, nat.TYPE_CODES[_NP_CODE[lens_d.dtype]], prefix_ptr,
-                 nat.TYPE_CODES[pcode], off_d.ptr, pool_d.ptr, members, int(member_stride), nf, offs, sizes, ptrs,
-                 cap, scratch.ptr, scratch.n, ws.total.ptr, nat.stream(dev))
-        nat.memcpy(ws.host_total.ptr, ws.total.ptr, 16, dev)
-        nat.sync(dev)
-        total, bad = (int(v) for v in ws.host_total._data.view(np.int64)[:2])
-        if bad:
+    # one launch computes the prefix (into the prefix plane, or a device temp for host-visible layouts),
+    # counts invalid device segments and gathers whatever fits the pools' current capacity: a device-resident
+    # vector whose pools are large enough is done after one sync; otherwise the prefix is already complete
+    # and only the pools have to grow before the gather
+    cap = lay.capacity(path) if device_resident else 0
+    ws = _workspace(dev)
+    need = C.c_size_t(0)
+    nat.call("sk_jagged_scratch_bytes", n, C.byref(need))
+    starts_bytes = ((cap + 255) // 256 + 1) * 8  # the two-kernel path's work split (one entry per 256 members)
+    scratch = ws.scratch_for(-(-need.value // 256) * 256 + starts_bytes)
+    ptrs = (C.c_void_p * nf)(*[lay.plane_address(lf, 0) if cap else 0 for lf in leaves])
+    nat.call("sk_jagged_pack", n, lens_d.ptr, nat.TYPE_CODES[_NP_CODE[lens_d.dtype]], prefix_ptr,
+             nat.TYPE_CODES[pcode], off_d.ptr, pool_d.ptr, members, int(member_stride), nf, offs, sizes, ptrs,
+             cap, scratch.ptr, scratch.n, ws.total.ptr, nat.stream(dev))
+    nat.memcpy(ws.host_total.ptr, ws.total.ptr, 16, dev)
+    nat.sync(dev)
+    total, bad = (int(v) for v in ws.host_total._data.view(np.int64)[:2])
+    if bad:
+        if device_resident:
             # device inputs were checked by the kernel, which already wrote the prefix plane: leave the
             # vector empty and consistent (prefix all zero), then raise
             nat.call("sk_memset_async", prefix_ptr, 0, (n + 1) * psz, nat.stream(dev))
@@ -245,27 +246,16 @@ def pack(coll, path: str, lens, src_offsets, src_pool, member_stride: int | None
                 lay._set_sizes_for_engine({path: 0})
             coll._bump()
             nat.sync(dev)
-            for t in keep:
-                t.free()
-            raise _invalid_segments(bad)
-        checked = True
-        if total <= cap:
-            coll._bump()
-            with lay.engine_ops():
-                lay._set_sizes_for_engine({path: total})
-            for t in keep:
-                t.free()
-            return total
-        # overflow: the pools must grow first -- redo as scan, resize, gather
-
-    if not checked:  # device inputs on the scan + gather path: validate before anything is written
-        bad = _validate_on_device(lens_d, off_d, members, dev)
-        if bad:
-            for t in keep:
-                t.free()
-            raise _invalid_segments(bad)
-    total = scan(lens_d, prefix_ptr, pcode, dev, keep)
-
+        for t in keep:
+            t.free()
+        raise _invalid_segments(bad)
+    if device_resident and total <= cap:
+        coll._bump()
+        with lay.engine_ops():
+            lay._set_sizes_for_engine({path: total})
+        for t in keep:
+            t.free()
+        return total
     coll._bump()
     with lay.engine_ops():
         lay.reserve(path, total)

@@ -108,4 +108,15 @@ from paper_2511_04853_b200 import _native as nat  # noqa: E402
 cnt = DeviceArray(1, np.uint64, CUDA)
 nat.call("sk_compare_bytes", a.layout._struct_buf.ptr, a.layout._struct_buf.ptr + 3, 1001, cnt.ptr, nat.stream(0))
 nat.sync(0)
+# first fill of a fresh device collection: the prefix-only pack (capacity 0), grow, then the register
+# scatter over the prefix, with a skewed record (queued group)
+from paper_2511_04853_b200 import jagged as _jg  # noqa: E402
+
+_fl = np.random.default_rng(11).integers(0, 6, 3000).astype(np.int32)
+_fl[700] = 9000
+_fo, _fp = J._tiled_inputs(_fl, seed=12)
+_fc = sk.Collection(wl.CLUSTER_SCHEMA, ly.PER_FIELD, mc.ContextInfo.cuda(0))
+with mc.execution_scope(mc.CUDA):
+    _fc.resize(_fl.size)
+_jg.pack(_fc, "members", _fl, _fo, np.random.default_rng(13).integers(0, 2**63, _fp, dtype=np.uint64))
 print("sanitize paths done", len(parts))
