@@ -26,7 +26,8 @@ length soakit's bookkeeping reads and raises soakit's AccessError on any
 attempt to index device memory from Python.
 
 Divergences, by design: get_noise() on a cuda collection returns a host
-numpy array (the reference's type) computed on the device; host <-> host and
+numpy array (the reference's type) computed on the device, in page-locked
+memory that is recycled once the caller drops it; host <-> host and
 mockdev pairs stay on the reference's CPU path (the plugin takes only pairs
 with a cuda or pinned endpoint). INTEGRATION.md shows the same registration
 as a maintainer would write it.
