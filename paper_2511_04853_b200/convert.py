@@ -53,30 +53,49 @@ def _side(layout: ly.LayoutInstance):
     return nat.KIND_PLANES, 0, 0
 
 
+_SLOT_TABLES: dict[int, tuple] = {}
+
+
+def _slot_table(plan) -> list:
+    """(leaf, slot, type code, slot byte offset) of every main-tag record slot, per plan (plans are
+    immutable; the descriptor is rebuilt on every transfer, so its static part is computed once)."""
+    e = _SLOT_TABLES.get(id(plan))
+    if e is None or e[0] is not plan:
+        rows = [(lf, k, type_code(lf.value_type), k * lf.value_type.size_bytes)
+                for lf in plan.leaves if lf.size_tag == MAIN_TAG and lf.role == ROLE_ELEMENT
+                for k in range(lf.extent_multiplier)]
+        e = _SLOT_TABLES[id(plan)] = (plan, rows)
+    return e[1]
+
+
 def plan_desc(dst: ly.LayoutInstance, src: ly.LayoutInstance, n: int) -> nat.ConvDesc | None:
     """Descriptor converting records [0, n) of src into dst (same plan)."""
-    slots = main_slots(src)
-    if not slots:
+    rows = _slot_table(src.plan)
+    if not rows:
         return None
-    if len(slots) > nat.MAX_FIELDS:
-        raise UnsupportedTransferError(f"plan has {len(slots)} record slots; the engine takes at most {nat.MAX_FIELDS}")
+    if len(rows) > nat.MAX_FIELDS:
+        raise UnsupportedTransferError(f"plan has {len(rows)} record slots; the engine takes at most {nat.MAX_FIELDS}")
     d = nat.ConvDesc()
     d.n = n
     d.src_kind, d.src, d.src_stride = _side(src)
     d.dst_kind, d.dst, d.dst_stride = _side(dst)
-    d.nfields = len(slots)
-    for i, (leaf, k) in enumerate(slots):
+    d.nfields = len(rows)
+    s_struct = src._struct_set if isinstance(src, ly.AosLayout) else ()
+    d_struct = dst._struct_set if isinstance(dst, ly.AosLayout) else ()
+    s_addr = None if s_struct else src.main_slot_addresses([(r[0], r[1]) for r in rows])
+    d_addr = None if d_struct else dst.main_slot_addresses([(r[0], r[1]) for r in rows])
+    for i, (leaf, k, tc, koff) in enumerate(rows):
         f = d.fields[i]
-        f.src_type = f.dst_type = type_code(leaf.value_type)
-        isz = leaf.value_type.size_bytes
-        if _is_struct(src, leaf):
-            f.src_off = src.struct_offsets[leaf.dotted] + k * isz
+        f.src_type = f.dst_type = tc
+        name = leaf.dotted
+        if name in s_struct:
+            f.src_off = src.struct_offsets[name] + koff
         else:
-            f.src_plane = src.plane_address(leaf, k)
-        if _is_struct(dst, leaf):
-            f.dst_off = dst.struct_offsets[leaf.dotted] + k * isz
+            f.src_plane = s_addr[i] if s_addr is not None else src.plane_address(leaf, k)
+        if name in d_struct:
+            f.dst_off = dst.struct_offsets[name] + koff
         else:
-            f.dst_plane = dst.plane_address(leaf, k)
+            f.dst_plane = d_addr[i] if d_addr is not None else dst.plane_address(leaf, k)
     return d
 
 

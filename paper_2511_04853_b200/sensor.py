@@ -89,16 +89,15 @@ def transfer_calibrate(dst, src, noise: DeviceArray | None = None, sync: bool = 
         raise AccessError("fused sensor path writes a device-resident destination")
     if dst.plan != src.plan or dst.plan != SENSOR_PLAN:
         raise UnsupportedTransferError("fused sensor path needs the Sensor plan on both sides")
-    from .transfer import _match_sizes  # same reserve-then-size contract as copy_collection
+    from .transfer import _cached_desc, _match_sizes  # same reserve-then-size contract as copy_collection
 
     _match_sizes(dst, src)
     n = sl.size(sc.MAIN_TAG)
     dev = dl.device
     if noise is None:
         noise = DeviceArray(n, np.float32, memctx.ContextInfo.cuda(dev))
-    desc = cv.plan_desc(dl, sl, n)
-    names = [lf.dotted for lf, _ in cv.main_slots(sl)]
-    idx = [names.index(k) for k in (_COUNTS, _ENERGY, _NOISY, _A, _B, _NA, _NB)]
+    desc = _cached_desc(dl, sl, n)
+    idx = _FUSED_FIELDS
     if n:
         nat.call("sk_sensor_convert_calibrate", C.byref(desc), *idx, noise.ptr, dev, nat.stream(dev))
     dst._bump()
@@ -467,3 +466,6 @@ PARTICLE_SCHEMA = sc.Schema("Particle", (
 
 SENSOR_PLAN = sc.flatten(SENSOR_SCHEMA)
 PARTICLE_PLAN = sc.flatten(PARTICLE_SCHEMA)
+# record-slot indices of the seven case-study inputs/outputs in the Sensor descriptor (plan order)
+_FUSED_FIELDS = [[lf.dotted for lf, _, _, _ in cv._slot_table(SENSOR_PLAN)].index(k)
+                 for k in (_COUNTS, _ENERGY, _NOISY, _A, _B, _NA, _NB)]

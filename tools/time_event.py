@@ -45,3 +45,9 @@ for _ in range(200):
     sensor.transfer_calibrate(d1, src, n1)
 pr.disable()
 pstats.Stats(pr).sort_stats("tottime").print_stats(18)
+pr = cProfile.Profile()
+pr.enable()
+for _ in range(200):
+    tr.copy_collection(d1, src)
+pr.disable()
+pstats.Stats(pr).sort_stats("cumulative").print_stats(25)
