@@ -52,6 +52,8 @@ def _device_planes(coll) -> tuple[int, dict]:
     if isinstance(lay, ly.AosLayout):
         raise UnsupportedTransferError("case-study kernel reads per_field/arena planes; convert the AoS collection first")
     names = (_COUNTS, _ENERGY, _NOISY, _A, _B, _NA, _NB)
+    if coll.plan is SENSOR_PLAN or coll.plan == SENSOR_PLAN:  # the usual case: one batched address pass
+        return lay.device, dict(zip(names, lay.main_slot_addresses(_SENSOR_SLOTS)))
     return lay.device, {k: lay.plane_address(coll.plan.leaf(k), 0) for k in names}
 
 
@@ -466,6 +468,7 @@ PARTICLE_SCHEMA = sc.Schema("Particle", (
 
 SENSOR_PLAN = sc.flatten(SENSOR_SCHEMA)
 PARTICLE_PLAN = sc.flatten(PARTICLE_SCHEMA)
+_SENSOR_SLOTS = [(SENSOR_PLAN.leaf(k), 0) for k in (_COUNTS, _ENERGY, _NOISY, _A, _B, _NA, _NB)]
 # record-slot indices of the seven case-study inputs/outputs in the Sensor descriptor (plan order)
 _FUSED_FIELDS = [[lf.dotted for lf, _, _, _ in cv._slot_table(SENSOR_PLAN)].index(k)
                  for k in (_COUNTS, _ENERGY, _NOISY, _A, _B, _NA, _NB)]
