@@ -317,3 +317,57 @@ def test_skev_event_files_round_trip_with_the_reference(tmp_path):
     bad.write_bytes(paths[0].read_bytes() + b"x")
     with pytest.raises(ValueError):
         sensor.load_events([bad], coll)
+
+
+def test_return_pool_recycles_and_survives_finalizers_inside_allocation(monkeypatch):
+    """memctx.host_return_array's pool on host stand-ins for page-locked memory: buffers come back only when
+    every array viewing them is gone, the pool keeps at most keep_bytes, and a garbage-collector finalizer
+    that runs while the pool is handing out a buffer cannot deadlock it (finalizers take no lock)."""
+    import gc
+
+    live = {}
+
+    def alloc(nbytes):
+        buf = (ctypes.c_uint8 * nbytes)()
+        ptr = ctypes.addressof(buf)
+        live[ptr] = buf
+        return ptr
+
+    freed = []
+    monkeypatch.setattr(mc.nat, "host_alloc_pinned", alloc)
+    monkeypatch.setattr(mc.nat, "host_free_pinned", lambda p: freed.append(live.pop(p) is not None))
+    pool = mc._ReturnPool(keep_bytes=8 << 20)
+    n = (3 << 20) // 4  # 3 MB of float32 -> the 4 MB size class
+    a = pool.array(n, np.float32)
+    a[:] = 1.0
+    view = a[5:9]
+    pa = a.ctypes.data
+    del a
+    gc.collect()
+    b = pool.array(n, np.float32)
+    assert b.ctypes.data != pa and view.tolist() == [1.0] * 4  # the view keeps the first buffer out
+    del view, b
+    gc.collect()
+    c = pool.array(n, np.float32)
+    assert c.ctypes.data in live  # recycled
+    # a cycle whose collection releases a pooled buffer, collected from inside array() (gc.collect runs
+    # finalizers synchronously): array() must not deadlock, and the buffer comes back on the next call
+    holder = [pool.array(n, np.float32)]
+    holder.append(holder)
+    del holder
+    orig_alloc = mc.nat.host_alloc_pinned
+
+    def alloc_and_collect(nbytes):
+        gc.collect()
+        return orig_alloc(nbytes)
+
+    monkeypatch.setattr(mc.nat, "host_alloc_pinned", alloc_and_collect)
+    d = pool.array(1 << 20, np.uint8)  # a new size class: allocates, which collects the cycle
+    assert d.size == 1 << 20
+    # beyond keep_bytes returned buffers are freed rather than kept
+    many = [pool.array(n, np.float32) for _ in range(4)]
+    del many, c, d
+    gc.collect()
+    pool.array(16, np.uint8)  # below RETURN_POOL_MIN: plain numpy, but drains nothing
+    pool.array(n, np.float32)  # drains the returns: 8 MB kept, the rest freed
+    assert pool._kept <= 8 << 20 and freed
