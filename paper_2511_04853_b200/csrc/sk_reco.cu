@@ -126,6 +126,19 @@ __constant__ int16_t kRing[80] = {
     -260, -259, -258, -257, -256, -255, -254, -253, -252, -196, -188, -132, -124, -68, -60, -4, 4, 60, 68, 124,
     132, 188, 196, 252, 253, 254, 255, 256, 257, 258, 259, 260};
 
+// numpy's f32 `e / z > 5` (SEED_THRESHOLD, reconstruct.py:62-66) without the division: the rounded
+// quotient exceeds 5 iff the exact one exceeds the midpoint 5 + 2^-22 between 5 and the next float (a tie
+// rounds to 5, whose significand is even). z * (5 + 2^-22) is exact in f64 (24 x 25 significant bits), so
+// for z != 0 the test is one f64 product and compare, with the inequality flipped for z < 0. z = +-0: e / z
+// is an infinity of the sign of e XOR z (> 5 iff that is +inf), or NaN for e = 0; NaN anywhere: false.
+__device__ __forceinline__ bool seed_ratio(float e, float z) {
+  const double t = static_cast<double>(z) * (5.0 + 0x1p-22);
+  if (z > 0.0f) return static_cast<double>(e) > t;
+  if (z < 0.0f) return static_cast<double>(e) < t;
+  if (z == 0.0f) return e != 0.0f && e == e && ((e > 0.0f) != static_cast<bool>(signbit(z)));
+  return false;  // z is NaN
+}
+
 template <bool VEC>
 __global__ void __launch_bounds__(NT, 5) tile_kernel(Args A, int tiles_x, int tiles_per_event) {
   pdl_enter();
@@ -167,10 +180,10 @@ __global__ void __launch_bounds__(NT, 5) tile_kernel(Args A, int tiles_x, int ti
       const int hy = rg + r * RG, y = ty0 - HALO + hy;
       const bool in = xin && y >= 0 && y < h;
       // numpy f32 division (IEEE); NaN is no candidate
-      const uint32_t cand = in ? (static_cast<uint32_t>(__fdiv_rn(e[r].x, z[r].x) > 5.0f) |
-                                  static_cast<uint32_t>(__fdiv_rn(e[r].y, z[r].y) > 5.0f) << 8 |
-                                  static_cast<uint32_t>(__fdiv_rn(e[r].z, z[r].z) > 5.0f) << 16 |
-                                  static_cast<uint32_t>(__fdiv_rn(e[r].w, z[r].w) > 5.0f) << 24)
+      const uint32_t cand = in ? (static_cast<uint32_t>(seed_ratio(e[r].x, z[r].x)) |
+                                  static_cast<uint32_t>(seed_ratio(e[r].y, z[r].y)) << 8 |
+                                  static_cast<uint32_t>(seed_ratio(e[r].z, z[r].z)) << 16 |
+                                  static_cast<uint32_t>(seed_ratio(e[r].w, z[r].w)) << 24)
                                : 0u;
       if (in && xint && hy >= HALO && hy < HALO + TY)  // PENDING == 1: the candidate bytes are the flags
         *reinterpret_cast<uint32_t*>(F + static_cast<int64_t>(y) * w + x) = cand;
@@ -201,7 +214,7 @@ __global__ void __launch_bounds__(NT, 5) tile_kernel(Args A, int tiles_x, int ti
       for (int ch = 0; ch < 2; ++ch) {
         const int hx = ch * 32 + lane0, x = tx0 - HALO + hx;
         const bool in = y >= 0 && y < h && x >= 0 && x < w;
-        const bool cand = in && __fdiv_rn(e[r][ch], nz[r][ch]) > 5.0f;  // numpy f32 division; NaN: no candidate
+        const bool cand = in && seed_ratio(e[r][ch], nz[r][ch]);  // numpy f32 e / z > 5; NaN: no candidate
         if (in && hy >= HALO && hy < HALO + TY && hx >= HALO && hx < HALO + TX)
           F[static_cast<int64_t>(y) * w + x] = cand ? PENDING : 0;  // read by the rounds (later launches)
         se[hy * HX + hx] = e[r][ch];

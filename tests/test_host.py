@@ -371,3 +371,30 @@ def test_return_pool_recycles_and_survives_finalizers_inside_allocation(monkeypa
     pool.array(16, np.uint8)  # below RETURN_POOL_MIN: plain numpy, but drains nothing
     pool.array(n, np.float32)  # drains the returns: 8 MB kept, the rest freed
     assert pool._kept <= 8 << 20 and freed
+
+
+def _seed_ratio(e, z):
+    """the reconstruction tile pass's division-free seed test (sk_reco.cu seed_ratio), restated"""
+    t = z.astype(np.float64) * (5.0 + 2.0 ** -22)
+    ed = e.astype(np.float64)
+    zero = (z == 0) & (e != 0) & ~np.isnan(e) & ((e > 0) != np.signbit(z))
+    return np.where(z > 0, ed > t, np.where(z < 0, ed < t, zero))
+
+
+def test_division_free_seed_test_equals_numpy_f32_division():
+    """e / z > 5 in numpy f32 (reconstruct.py:62-66) == the f64 product test, on random values, values one
+    ulp either side of the 5 + 2^-22 midpoint, denormals, zeros of both signs, infinities and NaN"""
+    rng = np.random.default_rng(5)
+    z = rng.standard_normal(2_000_000).astype(np.float32) * np.float32(10) ** rng.integers(-40, 38, 2_000_000)
+    z = z.astype(np.float32)
+    e = (z.astype(np.float64) * (5.0 + 2.0 ** -22)).astype(np.float32)  # right at the rounding boundary
+    e = np.concatenate([e, np.nextafter(e, np.float32(np.inf)), np.nextafter(e, np.float32(-np.inf)),
+                        rng.standard_normal(2_000_000).astype(np.float32) * 50])
+    z = np.concatenate([z, z, z, z])
+    specials = np.array([0.0, -0.0, np.inf, -np.inf, np.nan, 1e-45, -1e-45, 3.4e38, -3.4e38, 5.0, 1.0],
+                        np.float32)
+    e = np.concatenate([e, np.repeat(specials, specials.size)])
+    z = np.concatenate([z, np.tile(specials, specials.size)])
+    with np.errstate(divide="ignore", invalid="ignore", over="ignore"):
+        want = (e / z) > np.float32(5)
+    assert np.array_equal(_seed_ratio(e, z), want)
