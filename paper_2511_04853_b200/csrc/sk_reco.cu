@@ -506,8 +506,9 @@ __global__ void __launch_bounds__(NT) check_kernel(Args A, int parity) {
   }
   if (last_cta(&A.counters[C_DONE]) && threadIdx.x == 0) {
     A.counters[C_PASSES] += m != 0;
-    A.counters[C_CUR] = A.counters[C_NEXT];
-    A.counters[C_NEXT] = 0;
+    // C_NEXT was built by every CTA's atomics in this kernel: read and reset it atomically (a plain load
+    // may be served a stale L1 line)
+    A.counters[C_CUR] = atomicExch(&A.counters[C_NEXT], 0ull);
     A.counters[C_DONE] = 0;
   }
 }
