@@ -1166,7 +1166,11 @@ __global__ void __launch_bounds__(F_NT, 3) pack_fused_kernel(const __grid_consta
     if (tid == 0)
       while (ld_acquire(&F.defer[d].ready) != F.gen) __nanosleep(64);
     __syncthreads();
-    const DeferEntry ent = F.defer[d];
+    DeferEntry ent;  // published by another CTA: read through L2 (see load_entry)
+    ent.rec0 = __ldcg(&F.defer[d].rec0);
+    ent.cnt = __ldcg(&F.defer[d].cnt);
+    ent.E = __ldcg(&F.defer[d].E);
+    ent.A = __ldcg(&F.defer[d].A);
     const int64_t k0 = first_window(ent.E), nwin = end_window(ent.E, ent.A) - k0;
     const int64_t nchunks = (nwin + DEFER_CHUNK - 1) / DEFER_CHUNK;
     while (true) {
@@ -1268,6 +1272,20 @@ struct RegEntry {
   int pad0;
   int64_t pad[2];
 };
+
+// a queue entry published by another CTA (release on `ready`, acquired by this warp's lane 0): its fields are
+// read through L2 (ld.global.cg) -- the acquire by one lane does not make the other lanes' plain loads skip a
+// stale L1 copy of the entry's line
+__device__ __forceinline__ RegEntry load_entry(const RegEntry* e) {
+  RegEntry r;
+  r.rec0 = __ldcg(&e->rec0);
+  r.out0 = __ldcg(&e->out0);
+  r.T = __ldcg(&e->T);
+  r.cnt = __ldcg(&e->cnt);
+  r.next = 0;
+  r.ready = 0;
+  return r;
+}
 
 struct RegArgs {
   int64_t n;
@@ -1584,7 +1602,7 @@ __global__ void __launch_bounds__(RG_NW * 32, 4) pack_reg_kernel(const __grid_co
     if (lane == 0)
       while (ld_acquire(&F.q[dq].ready) != F.gen) __nanosleep(64);
     __syncwarp();
-    const RegEntry ent = F.q[dq];
+    const RegEntry ent = load_entry(&F.q[dq]);
     const int64_t nch = (ent.T + RG_CHUNK - 1) / RG_CHUNK;
     while (true) {
       unsigned long long c = 0;
@@ -1601,9 +1619,10 @@ __global__ void __launch_bounds__(RG_NW * 32, 4) pack_reg_kernel(const __grid_co
 //
 // A warp takes groups of 32 records (grid-stride): the group's base and end come from the prefix, each
 // lane's record offset inside the group from its prefix element, and the members move as in
-// pack_reg_kernel (12 register rounds in flight per warp). A group over RG_BIG members is queued and its
-// 1536-member chunks shared out by every warp that finishes (an entry queued later is drained by its
-// owner). tools/jag_micro.cu measured this structure at 37.9 us on config 3 (the window gather: 55 us).
+// pack_reg_kernel (12 register rounds in flight per warp). A group over RG_BIG members is only listed
+// (one atomic append); scatter_big_kernel, launched right behind, shares the listed groups' 1536-member
+// chunks over its whole grid. Nothing waits on anything inside either kernel. tools/jag_micro.cu measured
+// this structure at 37.9 us on config 3 (the window gather: 55 us).
 struct ScatRegArgs {
   int64_t n;
   const void* prefix;  // non-wrapped
@@ -1612,44 +1631,10 @@ struct ScatRegArgs {
   int64_t member_stride;
   uint8_t* dst;
   int64_t total;       // members gathered: positions >= total are skipped
-  RegEntry* q;
-  unsigned int* nq;    // zeroed by block 0, which then publishes `ready` with this launch's generation
-  RegStatus* ready;
-  int64_t qmax;
-  unsigned long long gen;
+  RegEntry* q;         // the listed groups (rec0, cnt, out0, T)
+  unsigned int* nq;    // zeroed by the launcher
+  int64_t qmax;        // > total / (RG_BIG + 1): the list cannot overflow with a valid prefix
 };
-
-// block 0 has zeroed the queue counter of this launch
-__device__ __forceinline__ void scat_wait_ready(const ScatRegArgs& A) {
-  while ((ld_acquire(&A.ready->tag) & ~3ull) != (A.gen << 2)) __nanosleep(32);
-}
-
-// a group over RG_BIG members: queued for every warp to share (a full queue: gathered here)
-template <int MS, bool PACKED>
-__device__ __forceinline__ void scatter_big_group(const ScatRegArgs& A, int64_t r0, int cnt, int64_t B, int64_t T,
-                                               int64_t ex, int64_t d) {
-  const int lane = threadIdx.x & 31;
-  unsigned slot = 0;
-  if (lane == 0) {
-    scat_wait_ready(A);
-    slot = atomicAdd(A.nq, 1u);
-  }
-  slot = __shfl_sync(0xffffffffu, slot, 0);
-  if (slot < A.qmax) {
-    if (lane == 0) {
-      RegEntry& qe = A.q[slot];
-      qe.rec0 = r0;
-      qe.cnt = cnt;
-      qe.out0 = B;
-      qe.T = T;
-      qe.next = 0;
-      __threadfence();
-      st_release(&qe.ready, A.gen);
-    }
-  } else {
-    span_gather<MS, PACKED>(A.src, A.member_stride, A.dst, ex, d, B, 0, T);
-  }
-}
 
 template <class PT, int MS, bool PACKED>
 __global__ void __launch_bounds__(256, 4) scatter_reg_kernel(const __grid_constant__ ScatRegArgs A) {
@@ -1659,11 +1644,6 @@ __global__ void __launch_bounds__(256, 4) scatter_reg_kernel(const __grid_consta
   const int64_t ngroups = (A.n + 31) / 32;
   const int64_t nw = static_cast<int64_t>(gridDim.x) * (blockDim.x / 32);
   pdl_wait_prior();
-  if (blockIdx.x == 0 && threadIdx.x == 0) {  // the queue buffer is fresh: no zeroing launch
-    *A.nq = 0;
-    __threadfence();
-    st_status(A.ready, 0, A.gen << 2 | 2);
-  }
 #pragma unroll 1
   for (int64_t g = static_cast<int64_t>(blockIdx.x) * (blockDim.x / 32) + (threadIdx.x >> 5); g < ngroups; g += nw) {
     const int64_t r0 = g * 32, r = r0 + lane;
@@ -1672,12 +1652,21 @@ __global__ void __launch_bounds__(256, 4) scatter_reg_kernel(const __grid_consta
     const int64_t Pe = static_cast<int64_t>(P[r0 + cnt]);
     const int64_t T = min(Pe, A.total) - B;  // past the total: not gathered
     if (T <= 0) continue;
-    const int64_t pr = lane < cnt ? static_cast<int64_t>(P[r]) : Pe;
-    const int64_t d64 = (lane < cnt ? A.src_off[r] : 0) - (pr - B);
-    if (T > RG_BIG) {
-      scatter_big_group<MS, PACKED>(A, r0, cnt, B, T, pr - B, d64);
+    if (T > RG_BIG) {  // listed for scatter_big_kernel
+      if (lane == 0) {
+        const unsigned slot = atomicAdd(A.nq, 1u);
+        if (slot < A.qmax) {  // (only a non-monotone, invalid prefix could overflow the list)
+          RegEntry& qe = A.q[slot];
+          qe.rec0 = r0;
+          qe.cnt = cnt;
+          qe.out0 = B;
+          qe.T = T;
+        }
+      }
       continue;
     }
+    const int64_t pr = lane < cnt ? static_cast<int64_t>(P[r]) : Pe;
+    const int64_t d64 = (lane < cnt ? A.src_off[r] : 0) - (pr - B);
     const int ex = static_cast<int>(pr - B);
     const int Ti = static_cast<int>(T);
 #pragma unroll 1
@@ -1707,26 +1696,27 @@ __global__ void __launch_bounds__(256, 4) scatter_reg_kernel(const __grid_consta
       }
     }
   }
-  // queued groups seen so far (this warp's own included: it reads the count after queueing)
-  if (lane == 0) scat_wait_ready(A);
-  __syncwarp();
-  const unsigned nq = min(static_cast<unsigned>(A.qmax), *reinterpret_cast<volatile unsigned int*>(A.nq));
+}
+
+// the listed groups: every warp of the grid takes 1536-member chunks of each group in turn
+template <class PT, int MS, bool PACKED>
+__global__ void __launch_bounds__(256) scatter_big_kernel(const __grid_constant__ ScatRegArgs A) {
+  const int lane = threadIdx.x & 31;
+  const PT* P = static_cast<const PT*>(A.prefix);
+  pdl_wait_prior();
+  const unsigned nq = min(static_cast<unsigned>(A.qmax), *A.nq);
+  const int64_t gw = static_cast<int64_t>(blockIdx.x) * (blockDim.x / 32) + (threadIdx.x >> 5);
+  const int64_t nw = static_cast<int64_t>(gridDim.x) * (blockDim.x / 32);
   for (unsigned dq = 0; dq < nq; ++dq) {
-    if (lane == 0)
-      while (ld_acquire(&A.q[dq].ready) != A.gen) __nanosleep(64);
-    __syncwarp();
     const RegEntry ent = A.q[dq];
+    const int64_t nch = (ent.T + RG_CHUNK - 1) / RG_CHUNK;
+    if (gw >= nch) continue;
     const int64_t r = ent.rec0 + lane;
     const int64_t Pe = static_cast<int64_t>(P[ent.rec0 + ent.cnt]);
     const int64_t pr = lane < ent.cnt ? static_cast<int64_t>(P[r]) : Pe;
     const int64_t ex = pr - ent.out0, d = (lane < ent.cnt ? A.src_off[r] : 0) - ex;
-    const int64_t nch = (ent.T + RG_CHUNK - 1) / RG_CHUNK;
-    while (true) {
-      unsigned long long c = 0;
-      if (lane == 0) c = atomicAdd(&A.q[dq].next, 1ull);
-      c = __shfl_sync(0xffffffffu, c, 0);
-      if (static_cast<int64_t>(c) >= nch) break;
-      const int64_t mb = static_cast<int64_t>(c) * RG_CHUNK;
+    for (int64_t c = gw; c < nch; c += nw) {
+      const int64_t mb = c * RG_CHUNK;
       span_gather<MS, PACKED>(A.src, A.member_stride, A.dst, ex, d, ent.out0, mb, min(ent.T, mb + RG_CHUNK));
     }
   }
@@ -2091,6 +2081,11 @@ static int launch_scatter_reg_t(const jag::ScatRegArgs& R, cudaStream_t s, const
   const int64_t groups = (R.n + 31) / 32;
   const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((groups + 7) / 8, static_cast<int64_t>(ds->sm_count) * 8));
   SK_TRY(launch_pdl(jag::scatter_reg_kernel<PT, MS, PACKED>, dim3(static_cast<unsigned>(grid)), dim3(256), s, R));
+  // the listed groups (usually none: the kernel returns at once); chunks of the largest possible group
+  // spread over up to 4 CTAs per SM
+  const int64_t chunks = (R.total + jag::RG_CHUNK - 1) / jag::RG_CHUNK;
+  const int64_t bgrid = std::max<int64_t>(1, std::min<int64_t>((chunks + 7) / 8, static_cast<int64_t>(ds->sm_count) * 4));
+  SK_TRY(launch_pdl(jag::scatter_big_kernel<PT, MS, PACKED>, dim3(static_cast<unsigned>(bgrid)), dim3(256), s, R));
   return SK_OK;
 }
 
@@ -2114,13 +2109,13 @@ static int launch_scatter_reg(const jag::ScatterArgs& A, cudaStream_t s, int dev
   R.member_stride = A.member_stride;
   R.dst = A.dst[0];
   R.total = A.total;
-  R.qmax = reg_queue_entries(A.n);
-  R.gen = next_generation();
+  // every listed group holds more than RG_BIG of the `total` members: the list cannot overflow
+  R.qmax = std::min<int64_t>((A.n + 31) / 32, A.total / (jag::RG_BIG + 1) + 1);
   uint8_t* qbuf = nullptr;
   const size_t qbytes = 64 + static_cast<size_t>(R.qmax) * sizeof(jag::RegEntry);
   SK_TRY(cudaMallocAsync(reinterpret_cast<void**>(&qbuf), qbytes, s));
-  R.ready = reinterpret_cast<jag::RegStatus*>(qbuf);
-  R.nq = reinterpret_cast<unsigned int*>(qbuf + 16);
+  SK_TRY(cudaMemsetAsync(qbuf, 0, 4, s));
+  R.nq = reinterpret_cast<unsigned int*>(qbuf);
   R.q = reinterpret_cast<jag::RegEntry*>(qbuf + 64);
   int rc;
   switch (A.prefix_type) {
