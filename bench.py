@@ -983,10 +983,11 @@ def run_extras(args, dev: int) -> dict:
                            "note": "jagged.pack(collection, lens, offsets, pool) with numpy inputs in pinned / "
                                    "pageable host memory: host-side validation (collection.py:546 raises before "
                                    "mutating), H2D of the inputs, the fused pack, member total read back"},
-        "note": "device_ms: sk_jagged_pack (one fused kernel: block sums, prefixes, gather) queued on the device; "
-                "api_ms: jagged.pack on a "
-                "Collection, incl. the host readback of the member total that sizes the pool; source segments "
-                "in shuffled order with slack, so ~125 MB of 32 B sectors are read for 92 MB of payload",
+        "note": "device_ms: sk_jagged_pack queued on the device: one launch of pack_reg_kernel (1792-record tiles, "
+                "decoupled look-back for the prefix, register gather); api_ms: jagged.pack on a Collection, incl. "
+                "the host readback of the member total and invalid-segment count; source segments in shuffled "
+                "order with slack: ncu counts 133 MB of DRAM reads for 92 MB of algorithmic reads "
+                "(64-byte fetch granularity, profiles/r02_jagged_redesign.md)",
         "parity": "whole prefix (1,000,001 x i32) and pool byte-exact vs oracle/restate.jagged_pack",
         "roofline": _cfg_roofline("config3_jagged_1M", algo, ms, 1, peak)}
     c3.free()
