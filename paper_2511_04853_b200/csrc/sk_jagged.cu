@@ -1620,7 +1620,7 @@ __global__ void __launch_bounds__(RG_NW * 32, 4) pack_reg_kernel(const __grid_co
 // A warp takes groups of 32 records (grid-stride): the group's base and end come from the prefix, each
 // lane's record offset inside the group from its prefix element, and the members move as in
 // pack_reg_kernel (12 register rounds in flight per warp). A group over RG_BIG members is only listed
-// (one atomic append); scatter_big_kernel, launched right behind, shares the listed groups' 1536-member
+// (one tagged atomic append, no zeroing launch); scatter_big_kernel, launched right behind, shares the listed groups' 1536-member
 // chunks over its whole grid. Nothing waits on anything inside either kernel. tools/jag_micro.cu measured
 // this structure at 37.9 us on config 3 (the window gather: 55 us).
 struct ScatRegArgs {
@@ -1632,9 +1632,28 @@ struct ScatRegArgs {
   uint8_t* dst;
   int64_t total;       // members gathered: positions >= total are skipped
   RegEntry* q;         // the listed groups (rec0, cnt, out0, T)
-  unsigned int* nq;    // zeroed by the launcher
+  unsigned long long* nq;  // list length, tagged: (gen & 2^40 - 1) << 24 | count; a stale tag counts as 0
   int64_t qmax;        // > total / (RG_BIG + 1): the list cannot overflow with a valid prefix
+  unsigned long long gen;
 };
+
+// next list slot: no zeroing of the counter between launches (the word carries this launch's tag)
+__device__ __forceinline__ unsigned scat_list_slot(const ScatRegArgs& A) {
+  const unsigned long long tag = (A.gen & ((1ull << 40) - 1)) << 24;
+  unsigned long long old = atomicAdd(A.nq, 0ull);
+  for (;;) {
+    const bool mine = (old & ~((1ull << 24) - 1)) == tag;
+    const unsigned slot = mine ? static_cast<unsigned>(old & ((1ull << 24) - 1)) : 0u;
+    const unsigned long long seen = atomicCAS(A.nq, old, tag | (slot + 1));
+    if (seen == old) return slot;
+    old = seen;
+  }
+}
+
+__device__ __forceinline__ unsigned scat_list_len(const ScatRegArgs& A) {
+  const unsigned long long w = *A.nq, tag = (A.gen & ((1ull << 40) - 1)) << 24;
+  return (w & ~((1ull << 24) - 1)) == tag ? static_cast<unsigned>(w & ((1ull << 24) - 1)) : 0u;
+}
 
 template <class PT, int MS, bool PACKED>
 __global__ void __launch_bounds__(256, 4) scatter_reg_kernel(const __grid_constant__ ScatRegArgs A) {
@@ -1654,7 +1673,7 @@ __global__ void __launch_bounds__(256, 4) scatter_reg_kernel(const __grid_consta
     if (T <= 0) continue;
     if (T > RG_BIG) {  // listed for scatter_big_kernel
       if (lane == 0) {
-        const unsigned slot = atomicAdd(A.nq, 1u);
+        const unsigned slot = scat_list_slot(A);
         if (slot < A.qmax) {  // (only a non-monotone, invalid prefix could overflow the list)
           RegEntry& qe = A.q[slot];
           qe.rec0 = r0;
@@ -1704,7 +1723,7 @@ __global__ void __launch_bounds__(256) scatter_big_kernel(const __grid_constant_
   const int lane = threadIdx.x & 31;
   const PT* P = static_cast<const PT*>(A.prefix);
   pdl_wait_prior();
-  const unsigned nq = min(static_cast<unsigned>(A.qmax), *A.nq);
+  const unsigned nq = min(static_cast<unsigned>(A.qmax), scat_list_len(A));
   const int64_t gw = static_cast<int64_t>(blockIdx.x) * (blockDim.x / 32) + (threadIdx.x >> 5);
   const int64_t nw = static_cast<int64_t>(gridDim.x) * (blockDim.x / 32);
   for (unsigned dq = 0; dq < nq; ++dq) {
@@ -2114,8 +2133,8 @@ static int launch_scatter_reg(const jag::ScatterArgs& A, cudaStream_t s, int dev
   uint8_t* qbuf = nullptr;
   const size_t qbytes = 64 + static_cast<size_t>(R.qmax) * sizeof(jag::RegEntry);
   SK_TRY(cudaMallocAsync(reinterpret_cast<void**>(&qbuf), qbytes, s));
-  SK_TRY(cudaMemsetAsync(qbuf, 0, 4, s));
-  R.nq = reinterpret_cast<unsigned int*>(qbuf);
+  R.gen = next_generation();  // tags the list counter: nothing is zeroed
+  R.nq = reinterpret_cast<unsigned long long*>(qbuf);
   R.q = reinterpret_cast<jag::RegEntry*>(qbuf + 64);
   int rc;
   switch (A.prefix_type) {
