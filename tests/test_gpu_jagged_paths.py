@@ -521,3 +521,30 @@ def test_register_pack_structural_edges(case):
     p, got, t = _pack(lens, offs, pool, 8, [(0, 8)], ptype, cap_extra=0 if ptype == "u8" else 7)
     pw, want, tw = _expect(lens, offs, pool, 8, [(0, 8)], ptype)
     assert t == tw and p.tobytes() == pw.tobytes() and got == want
+
+
+@pytest.mark.parametrize("msize,ptype", [(8, "i64"), (4, "u32")])
+def test_scatter_skewed_groups_and_total_bound(msize, ptype):
+    """sk_jagged_scatter over a caller prefix with skewed lengths (listed groups gathered by the second
+    kernel) and a member bound below the sum: members past `total` are not written"""
+    lens, offs, plen = _skewed_inputs(200_000, seed=23)
+    pool = np.random.default_rng(24).integers(0, 256, plen * msize, dtype=np.uint8)
+    pdt = np.int64 if ptype == "i64" else np.uint32
+    P = np.concatenate([[0], np.cumsum(lens.astype(np.int64))]).astype(pdt)
+    full = int(P[-1])
+    _, want, _ = _expect(lens, offs, pool, msize, [(0, msize)], "i64")
+    d_p, d_o, d_pool = (DeviceArray.from_numpy(x, CUDA) for x in (P, offs, pool))
+    try:
+        for total in (full, full // 2 + 12345):
+            out = DeviceArray.from_numpy(np.full(full * msize, 0xAB, np.uint8), CUDA)
+            foff, fsz, dst = (C.c_int64 * 1)(0), (C.c_int32 * 1)(msize), (C.c_void_p * 1)(out.ptr)
+            nat.call("sk_jagged_scatter", lens.size, d_p.ptr, TC[ptype], d_o.ptr, d_pool.ptr, msize, 1, foff, fsz,
+                     dst, total, nat.stream(0))
+            nat.sync(0)
+            got = out.numpy().tobytes()
+            assert got[:total * msize] == want[0][:total * msize]
+            assert set(got[total * msize:]) <= {0xAB}
+            out.free()
+    finally:
+        for a in (d_p, d_o, d_pool):
+            a.free()
